@@ -1,0 +1,214 @@
+/*
+ * covap_c.h — C-ABI of the B200-native COVAP gradient-synchronisation path.
+ *
+ * This is the drop-in boundary: plain C types, pointers and sizes, no torch
+ * types.  Host callers (the C++ drop-in layer under include/covap/, the
+ * Python host mirror in paper_2311_04499_b200/, or a DDP comm hook) bind these
+ * symbols from libcovap_b200.so.  Each entry point names the reference
+ * interface it replaces (paths relative to /root/reference/proj).
+ *
+ * Conventions
+ *  - Every function returns a covap_status (0 = OK).  The non-zero codes map
+ *    one-to-one onto the reference exception taxonomy (include/covap/errors.hpp
+ *    :9-36); covap_last_error() returns the message of the calling thread's
+ *    last failure.  The C++ layer rethrows the same exception classes.
+ *  - Device calls are asynchronous and stream-ordered on the cudaStream_t the
+ *    caller passes (as void*; NULL = legacy default stream).  One state per
+ *    device; a state must not be used from two host threads at once.
+ *  - dtype: COVAP_F32 (the production path) or COVAP_F64 (bit-exact check
+ *    against the reference's double arithmetic).
+ *  - Device pointers passed in must be 16-byte aligned.
+ */
+#ifndef COVAP_C_H
+#define COVAP_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int covap_status;
+enum {
+  COVAP_OK = 0,
+  COVAP_ERR_INVALID_INPUT = 1,      /* covap::InvalidInput      errors.hpp:13-16 */
+  COVAP_ERR_INVALID_STATE = 2,      /* covap::InvalidState      errors.hpp:18-21 */
+  COVAP_ERR_UNDEFINED_RATIO = 3,    /* covap::UndefinedRatio    errors.hpp:23-26 */
+  COVAP_ERR_INCOMPLETE_PROFILE = 4, /* covap::IncompleteProfile errors.hpp:28-31 */
+  COVAP_ERR_CONFIG = 5,             /* covap::ConfigError       errors.hpp:33-36 */
+  COVAP_ERR_GENERIC = 6,            /* covap::Error             errors.hpp:8-11  */
+  COVAP_ERR_CUDA = 10,              /* CUDA runtime failure (no reference equivalent) */
+  COVAP_ERR_NCCL = 11,              /* NCCL failure */
+  COVAP_ERR_NO_DEVICE = 12          /* no CUDA device: the path never falls back to CPU */
+};
+
+enum { COVAP_F32 = 0, COVAP_F64 = 1 };
+enum { COVAP_RULE_MATCH_STEP = 0, COVAP_RULE_PLUS_STEP = 1 }; /* compress.hpp:19 */
+enum { COVAP_GEN_NORMAL = 0, COVAP_GEN_INTEGER = 1 };
+
+/* EfSchedule (compress.hpp:26-31); defaults {1, 0.3, 100, 0.1}. */
+typedef struct covap_ef {
+  int enabled;
+  double init_value;
+  uint64_t ascend_steps;
+  double ascend_range;
+} covap_ef;
+
+typedef struct covap_plan covap_plan;   /* BucketPlan + effective tensors + per-phase send layout */
+typedef struct covap_state covap_state; /* CompressorState on one device (+ scratch, streams) */
+typedef struct covap_comm covap_comm;   /* one NCCL communicator rank */
+
+typedef struct covap_plan_info {
+  uint64_t n_layers;
+  uint64_t n_buckets;
+  uint64_t n_tensors;     /* effective tensors (shards count individually) */
+  uint64_t total_numel;   /* N */
+  uint64_t twice_median;  /* MedianNumel::twice, model.hpp:52-57 */
+  uint32_t interval;      /* K */
+  int32_t rule;
+  int32_t sharded;        /* shard_plan was applied (only when K > 1) */
+  int32_t align;          /* send-buffer alignment quantum, elements */
+  uint64_t max_send_elems;/* send-buffer capacity over all phases (with alignment gaps) */
+} covap_plan_info;
+
+typedef struct covap_bucket_range {
+  uint64_t bucket_begin, bucket_end; /* flat [begin,end) of the bucket */
+  uint64_t sel_begin, sel_end;       /* selected sub-range this phase (empty: begin == end) */
+  uint64_t send_offset;              /* element offset of sel_begin in the send buffer */
+} covap_bucket_range;
+
+const char* covap_last_error(void);
+int covap_version(void);
+/* Number of CUDA devices visible; COVAP_ERR_NO_DEVICE when none. */
+covap_status covap_device_count(int* count);
+
+/* ------------------------------------------------------------ planner --- */
+
+/* allocate_buckets (model.hpp:82-83, model.cpp:36-60) -> [shard_plan when
+ * interval > 1 (model.cpp:95-115; train() shards only then, trainer.cpp:
+ * 269-271)] -> effective_tensors (model.cpp:117-137) -> per-phase selection
+ * (select_tensors, compress.cpp:13-28) compiled into the device send layout.
+ * bytes_per_param may be NULL (all fp32).  shard: -1 = as train() does
+ * (interval > 1), 0 = never, 1 = always (shard_plan called directly). */
+covap_status covap_plan_create(const uint64_t* layer_numel, const uint32_t* bytes_per_param,
+                               size_t n_layers, uint64_t cap_bytes, uint32_t interval, int rule,
+                               int shard, covap_plan** out);
+void covap_plan_destroy(covap_plan* plan);
+covap_status covap_plan_get_info(const covap_plan* plan, covap_plan_info* info);
+/* Bucket::numel / flat begin / first layer / layer count (model.hpp:34-39). */
+covap_status covap_plan_buckets(const covap_plan* plan, uint64_t* numel, uint64_t* begin,
+                                uint64_t* first_layer, uint64_t* n_layers);
+/* EffectiveTensor list (model.hpp:71-77). */
+covap_status covap_plan_tensors(const covap_plan* plan, uint64_t* bucket, uint64_t* begin,
+                                uint64_t* end);
+/* keep[t] for the phase of num_steps (select_tensors over the plan). */
+covap_status covap_plan_selection(const covap_plan* plan, uint64_t num_steps, uint8_t* keep);
+/* Per-bucket selected range + send offset at the phase of num_steps. */
+covap_status covap_plan_bucket_range(const covap_plan* plan, uint64_t num_steps, size_t bucket,
+                                     covap_bucket_range* out);
+/* Send-buffer length (incl. alignment gaps) and payload elements
+ * (CompressedUpdate::payload_elements, compress.cpp:44-48) at num_steps. */
+covap_status covap_plan_send_elems(const covap_plan* plan, uint64_t num_steps,
+                                   uint64_t* send_elems, uint64_t* payload_elems);
+
+/* Functional forms of the reference scalar helpers. */
+covap_status covap_median_twice(const uint64_t* bucket_numel, size_t n, uint64_t* twice);
+covap_status covap_select_tensors(uint64_t num_steps, uint32_t interval, size_t count, int rule,
+                                  uint8_t* keep);                         /* compress.cpp:13 */
+covap_status covap_ef_coefficient(uint64_t num_steps, const covap_ef* ef, double* coeff);
+                                                                          /* compress.cpp:30 */
+covap_status covap_ccr(double comm_ms, double comp_ms, double* out);      /* perf.cpp:40 */
+covap_status covap_choose_interval(double ccr, uint32_t* out);            /* perf.cpp:49 */
+/* profile_ccr (sim.cpp:164-216) over gathered traces: comm_start is
+ * workers x n_coll arrivals, comm_end the shared completions, comp_ms worker
+ * 0's backward time.  workers != expected -> COVAP_ERR_INCOMPLETE_PROFILE. */
+covap_status covap_profile_ccr(const double* comm_start, const double* comm_end,
+                               size_t workers, size_t expected, size_t n_coll, double comp_ms,
+                               double* aligned_ms, double* naive_ms, double* ccr,
+                               uint32_t* interval);
+
+/* ------------------------------------------------------- device state --- */
+
+/* CompressorState::zeros (compress.cpp:37-42) on `device`: a zeroed flat
+ * residual arena of N elements (offsets = flat gradient offsets), num_steps
+ * = 0, the send scratch, the per-phase run tables and a comm side stream. */
+covap_status covap_state_create(const covap_plan* plan, int dtype, int device,
+                                const covap_ef* ef, covap_state** out);
+void covap_state_destroy(covap_state* state);
+covap_status covap_state_residual(covap_state* state, void** dev_ptr, uint64_t* n);
+covap_status covap_state_send(covap_state* state, void** dev_ptr, uint64_t* capacity);
+covap_status covap_state_get_step(const covap_state* state, uint64_t* num_steps);
+covap_status covap_state_set_step(covap_state* state, uint64_t num_steps);
+/* Zero the residual arena (stream-ordered). */
+covap_status covap_state_reset(covap_state* state, void* stream);
+
+/* K1 (filter_pack) over buckets [b0, b1): covap_compress's compensate /
+ * select / pack / residual write-back (compress.cpp:59-81) at the state's
+ * current step: c = g + coeff*r (mul then add, no FMA), selected -> send and
+ * r = 0, unselected -> r = c.  send may be NULL (state scratch). */
+covap_status covap_filter_pack(covap_state* state, const void* grad, void* send, size_t b0,
+                               size_t b1, void* stream);
+/* K2 (unpack_scale) over buckets [b0, b1): out[sel] = (0 + recv) * inv_world
+ * (allreduce_mean's sum-then-scale, trainer.cpp:41-45), out[unsel] = 0
+ * (covap_decompress's zero fill, compress.cpp:91-100).  recv may be NULL
+ * (state scratch, i.e. the in-place allreduce result).  out may alias grad. */
+covap_status covap_unpack(covap_state* state, const void* recv, void* out, double inv_world,
+                          size_t b0, size_t b1, void* stream);
+/* ++num_steps (compress.cpp:83). */
+covap_status covap_step_end(covap_state* state);
+
+/* The standalone sync step, trainer.cpp:365-386 for this rank: K1 over all
+ * buckets -> ncclAllReduce(sum) of the packed send buffer (skipped when comm
+ * is NULL or has one rank, or nothing is selected) -> K2 with 1/P -> ++step.
+ * All on `stream`. */
+covap_status covap_sync_step(covap_state* state, covap_comm* comm, const void* grad, void* out,
+                             void* stream);
+
+/* Overlapped schedule (the DDP-hook shape): bucket b's gradient is ready on
+ * `stream` -> K1(b) on `stream`, event -> on the state's comm stream:
+ * allreduce of b's selected range, K2(b).  covap_step_finish makes `stream`
+ * wait for the comm stream and advances the step. */
+covap_status covap_bucket_ready(covap_state* state, covap_comm* comm, size_t bucket,
+                                const void* grad, void* out, void* stream);
+covap_status covap_step_finish(covap_state* state, void* stream);
+/* Dense baseline (no compression, trainer.cpp:387-389): bucket b is
+ * allreduced in place on the comm stream, then out = (0 + sum) * 1/P. */
+covap_status covap_dense_bucket_ready(covap_state* state, covap_comm* comm, size_t bucket,
+                                      void* grad, void* out, void* stream);
+
+/* Per-collective timing of the last overlapped step (ms, CUDA events):
+ * dur[b] = this rank's (allreduce end - own arrival) for bucket b, -1 when
+ * the bucket sent nothing.  Used by the CCR controller. */
+covap_status covap_state_last_comm_ms(covap_state* state, double* dur, size_t n);
+
+/* ---------------------------------------------------- communicator ------ */
+
+covap_status covap_comm_unique_id(uint8_t id[128]);
+covap_status covap_comm_create(const uint8_t id[128], int nranks, int rank, int device,
+                               covap_comm** out);
+void covap_comm_destroy(covap_comm* comm);
+covap_status covap_comm_size(const covap_comm* comm, int* nranks, int* rank);
+/* In-place sum allreduce (C1) of count elements on stream. */
+covap_status covap_allreduce(covap_comm* comm, void* buf, uint64_t count, int dtype, void* stream);
+/* CCR controller exchange: aligned[c] = min over ranks of
+ * dur[c] (= end - last arrival, sim.cpp:202-203), comp = rank 0's comp_ms
+ * (sim.cpp:208-211).  Blocking.  comm NULL -> single rank. */
+covap_status covap_comm_profile_exchange(covap_comm* comm, const double* dur, size_t n_coll,
+                                         double comp_ms, double* aligned_ms, double* comp_out);
+
+/* ------------------------------------------------------ harness kernels -- */
+
+/* K0: synthetic gradients, element i = generator(key, begin + i); the
+ * oracle's oc_generate_* is the bit-identical host twin. */
+uint64_t covap_stream_key(uint64_t seed, uint64_t rank, uint64_t step);
+covap_status covap_generate(void* out, uint64_t n, int dtype, uint64_t key, int kind,
+                            uint64_t begin, void* stream);
+/* K3: backward emulator, spins `blocks` CTAs for `us` microseconds. */
+covap_status covap_spin(double us, int blocks, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COVAP_C_H */

@@ -1,0 +1,614 @@
+"""Python host mirror of the reference COVAP API over the B200 C-ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(paths relative to /root/reference/proj):
+
+=========================  =====================================================
+this module                reference
+=========================  =====================================================
+LayerSpec / ModelSpec      model.hpp:13-31
+allocate_buckets           model.hpp:82-83, model.cpp:36-60
+median_numel               model.hpp:87, model.cpp:66-82
+shard_plan                 model.hpp:89-92, model.cpp:95-115
+effective_tensors/_numels  model.hpp:94-95, model.cpp:117-143
+SelectionRule              compress.hpp:15-19
+select_tensors             compress.hpp:22-24, compress.cpp:13-28
+EfSchedule/ef_coefficient  compress.hpp:26-34, compress.cpp:30-35
+CovapConfig                compress.hpp:36-40
+CompressorState.zeros      compress.hpp:42-47, compress.cpp:37-42 (device arena)
+covap_compress             compress.hpp:57-61, compress.cpp:50-85  (kernel K1)
+covap_decompress           compress.hpp:63-65, compress.cpp:87-103 (kernel K2)
+allreduce_mean             trainer.hpp:56-58, trainer.cpp:35-47    (NCCL + K2)
+ccr / choose_interval      perf.hpp:24-28, perf.cpp:40-53
+profile_ccr                sim.hpp:84-96, sim.cpp:164-216
+=========================  =====================================================
+
+Data lives on the GPU as flat torch tensors laid out bucket by bucket (the
+layout train() builds with split_by_tensors, trainer.cpp:238-246); every
+compute call launches the sm_100a kernels of libcovap_b200.so on the current
+torch stream.  Nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+from . import _lib as L
+from .errors import InvalidInput, NoDeviceError
+
+_LAYOUT_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "layouts")
+DEFAULT_BUCKET_CAP_BYTES = 25 * 1024 * 1024  # model.hpp:26
+
+
+class SelectionRule:
+    """compress.hpp:15-19: kMatchStep keeps t at step s iff t == s (mod K)."""
+    kMatchStep = 0
+    kPlusStep = 1
+
+
+@dataclass
+class LayerSpec:
+    name: str
+    param_count: int
+    bytes_per_param: int = 4
+    backward_ms: float = 0.0
+
+    def bytes(self) -> int:
+        return self.param_count * self.bytes_per_param
+
+
+@dataclass
+class ModelSpec:
+    layers: List[LayerSpec] = field(default_factory=list)
+    bucket_cap_bytes: int = DEFAULT_BUCKET_CAP_BYTES
+    name: str = ""
+
+    def total_params(self) -> int:
+        return sum(l.param_count for l in self.layers)
+
+    @staticmethod
+    def from_json(doc) -> "ModelSpec":
+        """model_from_json (model.cpp:170-186)."""
+        if isinstance(doc, str):
+            doc = json.loads(doc)
+        if not isinstance(doc, dict) or not isinstance(doc.get("layers"), list):
+            raise InvalidInput("model JSON must be an object with a 'layers' array")
+        layers = []
+        for i, lj in enumerate(doc["layers"]):
+            name = lj.get("name", f"layer{i}")
+            if "param_count" not in lj:
+                raise InvalidInput(f"layer '{name}' missing param_count")
+            layers.append(LayerSpec(name, int(lj["param_count"]), int(lj.get("bytes_per_param", 4)),
+                                    float(lj.get("backward_ms", 0.0))))
+        return ModelSpec(layers, int(doc.get("bucket_cap_bytes", DEFAULT_BUCKET_CAP_BYTES)),
+                         doc.get("name", ""))
+
+
+def load_layout(name: str) -> ModelSpec:
+    """Gradient layouts of BASELINE.json's configs:
+    resnet50, vgg16, bert_large, tablev."""
+    with open(os.path.join(_LAYOUT_DIR, name + ".json")) as f:
+        return ModelSpec.from_json(json.load(f))
+
+
+@dataclass
+class EfSchedule:
+    enabled: bool = True
+    init_value: float = 0.3
+    ascend_steps: int = 100
+    ascend_range: float = 0.1
+
+    def c(self):
+        return L.EfC(1 if self.enabled else 0, float(self.init_value), int(self.ascend_steps),
+                     float(self.ascend_range))
+
+
+@dataclass
+class CovapConfig:
+    interval: int = 1
+    rule: int = SelectionRule.kMatchStep
+    ef: EfSchedule = field(default_factory=EfSchedule)
+
+
+@dataclass(frozen=True)
+class Bucket:
+    index: int
+    numel: int
+    begin: int
+    layer_refs: tuple
+
+
+@dataclass(frozen=True)
+class EffectiveTensor:
+    bucket: int
+    begin: int
+    end: int
+
+    def numel(self) -> int:
+        return self.end - self.begin
+
+
+def _u64(seq):
+    return (ctypes.c_uint64 * max(len(seq), 1))(*[int(x) for x in seq])
+
+
+class BucketPlan:
+    """A native covap_plan handle: buckets, effective tensors and the
+    per-phase send layout.  ``interval``/``rule`` fix the selection phases."""
+
+    def __init__(self, model: ModelSpec, cap_bytes: Optional[int] = None, interval: int = 1,
+                 rule: int = SelectionRule.kMatchStep, shard: int = -1):
+        lib = L.lib()
+        self.model = model
+        self.cap_bytes = int(model.bucket_cap_bytes if cap_bytes is None else cap_bytes)
+        numel = _u64([l.param_count for l in model.layers])
+        bpp = (ctypes.c_uint32 * max(len(model.layers), 1))(*[l.bytes_per_param for l in model.layers])
+        h = ctypes.c_void_p()
+        if int(interval) < 1:
+            raise InvalidInput("shard interval must be >= 1")
+        lib.covap_plan_create(numel, bpp, len(model.layers), self.cap_bytes, int(interval), int(rule),
+                              int(shard), ctypes.byref(h))
+        self._h = h
+        info = L.PlanInfoC()
+        lib.covap_plan_get_info(h, ctypes.byref(info))
+        self.info = info
+        nb, nt = info.n_buckets, info.n_tensors
+        bn, bb, bf, bl = (ctypes.c_uint64 * nb)(), (ctypes.c_uint64 * nb)(), (ctypes.c_uint64 * nb)(), (ctypes.c_uint64 * nb)()
+        lib.covap_plan_buckets(h, bn, bb, bf, bl)
+        self.buckets = [Bucket(i, bn[i], bb[i], tuple(range(bf[i], bf[i] + bl[i]))) for i in range(nb)]
+        tb, tbeg, tend = (ctypes.c_uint64 * nt)(), (ctypes.c_uint64 * nt)(), (ctypes.c_uint64 * nt)()
+        lib.covap_plan_tensors(h, tb, tbeg, tend)
+        self.tensors = [EffectiveTensor(tb[i], tbeg[i], tend[i]) for i in range(nt)]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and L._LIB is not None:
+            L._LIB.covap_plan_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def interval(self) -> int:
+        return self.info.interval
+
+    @property
+    def rule(self) -> int:
+        return self.info.rule
+
+    @property
+    def sharded(self) -> bool:
+        return bool(self.info.sharded)
+
+    @property
+    def twice_median(self) -> int:
+        return self.info.twice_median
+
+    @property
+    def max_send_elems(self) -> int:
+        return self.info.max_send_elems
+
+    def total_numel(self) -> int:
+        return self.info.total_numel
+
+    def selection(self, step: int) -> List[int]:
+        keep = (ctypes.c_uint8 * len(self.tensors))()
+        L.lib().covap_plan_selection(self._h, int(step), keep)
+        return [t for t in range(len(self.tensors)) if keep[t]]
+
+    def bucket_range(self, step: int, bucket: int) -> L.BucketRangeC:
+        r = L.BucketRangeC()
+        L.lib().covap_plan_bucket_range(self._h, int(step), int(bucket), ctypes.byref(r))
+        return r
+
+    def send_elems(self, step: int):
+        s, p = ctypes.c_uint64(), ctypes.c_uint64()
+        L.lib().covap_plan_send_elems(self._h, int(step), ctypes.byref(s), ctypes.byref(p))
+        return s.value, p.value
+
+    def payload_elements(self, step: int) -> int:
+        return self.send_elems(step)[1]
+
+
+# ------------------------------------------------------------------ planner
+
+def allocate_buckets(model: ModelSpec, cap_bytes: Optional[int] = None) -> BucketPlan:
+    """Greedy bucketing, no sharding (model.cpp:36-60)."""
+    return BucketPlan(model, cap_bytes, interval=1, shard=0)
+
+
+def median_numel(plan: BucketPlan) -> float:
+    """MedianNumel::value() (model.hpp:55) of the plan's buckets."""
+    return plan.twice_median / 2.0
+
+
+def shard_plan(plan: BucketPlan, interval: int, rule: int = SelectionRule.kMatchStep) -> BucketPlan:
+    """shard_plan (model.cpp:95-115); the result carries `interval` phases."""
+    return BucketPlan(plan.model, plan.cap_bytes, interval=interval, rule=rule, shard=1)
+
+
+def plan_for(model: ModelSpec, config: CovapConfig) -> BucketPlan:
+    """The plan train() builds: allocate, then shard only when K > 1
+    (trainer.cpp:266-271)."""
+    return BucketPlan(model, None, interval=config.interval, rule=config.rule, shard=-1)
+
+
+def effective_tensors(plan: BucketPlan) -> List[EffectiveTensor]:
+    return list(plan.tensors)
+
+
+def effective_numels(plan: BucketPlan) -> List[int]:
+    return [t.numel() for t in plan.tensors]
+
+
+# --------------------------------------------------------- scalar helpers
+
+def select_tensors(num_steps: int, interval: int, tensor_count: int,
+                   rule: int = SelectionRule.kMatchStep) -> List[int]:
+    if tensor_count < 1 or interval < 1:
+        keep = (ctypes.c_uint8 * 1)()
+    else:
+        keep = (ctypes.c_uint8 * tensor_count)()
+    L.lib().covap_select_tensors(int(num_steps), int(interval), int(tensor_count), int(rule), keep)
+    return [t for t in range(tensor_count) if keep[t]]
+
+
+def ef_coefficient(num_steps: int, schedule: EfSchedule) -> float:
+    out = ctypes.c_double()
+    ef = schedule.c()
+    L.lib().covap_ef_coefficient(int(num_steps), ctypes.byref(ef), ctypes.byref(out))
+    return out.value
+
+
+def ccr(comm_ms: float, comp_ms: float) -> float:
+    out = ctypes.c_double()
+    L.lib().covap_ccr(float(comm_ms), float(comp_ms), ctypes.byref(out))
+    return out.value
+
+
+def choose_interval(ccr_value: float) -> int:
+    out = ctypes.c_uint32()
+    L.lib().covap_choose_interval(float(ccr_value), ctypes.byref(out))
+    return out.value
+
+
+@dataclass
+class ProfileResult:
+    ccr: float
+    comp_ms: float
+    comm_aligned_ms: float
+    naive_comm_ms: List[float]
+    recommended_interval: int
+
+
+def profile_ccr(comm_start: Sequence[Sequence[float]], comm_end: Sequence[float],
+                comp_ms: float, expected_workers: int) -> ProfileResult:
+    """profile_ccr (sim.cpp:164-216) over gathered per-worker arrivals."""
+    W = len(comm_start)
+    C = len(comm_end)
+    starts = (ctypes.c_double * max(W * C, 1))(*[float(x) for row in comm_start for x in row])
+    ends = (ctypes.c_double * max(C, 1))(*[float(x) for x in comm_end])
+    naive = (ctypes.c_double * max(W, 1))()
+    aligned, c, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint32()
+    L.lib().covap_profile_ccr(starts, ends, W, int(expected_workers), C, float(comp_ms),
+                              ctypes.byref(aligned), naive, ctypes.byref(c), ctypes.byref(k))
+    return ProfileResult(c.value, float(comp_ms), aligned.value, list(naive[:W]), k.value)
+
+
+# ------------------------------------------------------------ device side
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(dtype) -> int:
+    torch = _torch()
+    if dtype == torch.float32:
+        return L.F32
+    if dtype == torch.float64:
+        return L.F64
+    raise InvalidInput("dtype must be torch.float32 or torch.float64")
+
+
+class _CudaArray:
+    """Zero-copy view of a device allocation owned by the native library."""
+
+    def __init__(self, ptr, n, dtype_code):
+        self.__cuda_array_interface__ = {
+            "shape": (int(n),), "typestr": "<f8" if dtype_code == L.F64 else "<f4",
+            "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _stream_ptr(stream=None, device=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def require_device():
+    n = ctypes.c_int()
+    L.lib().covap_device_count(ctypes.byref(n))  # raises NoDeviceError without a GPU
+    return n.value
+
+
+class CompressorState:
+    """CompressorState (compress.hpp:42-47) resident on one GPU: the flat
+    residual arena (offsets = flat gradient offsets), num_steps, the send
+    scratch and the comm side stream."""
+
+    def __init__(self, plan: BucketPlan, dtype=None, device: int = 0,
+                 ef: Optional[EfSchedule] = None):
+        torch = _torch()
+        require_device()
+        self.plan = plan
+        self.dtype = torch.float32 if dtype is None else dtype
+        self.dtype_code = _dtype_code(self.dtype)
+        self.device = int(device)
+        self.ef = ef if ef is not None else EfSchedule()
+        efc = self.ef.c()
+        h = ctypes.c_void_p()
+        L.lib().covap_state_create(plan.handle, self.dtype_code, self.device, ctypes.byref(efc),
+                                   ctypes.byref(h))
+        self._h = h
+        p, n = ctypes.c_void_p(), ctypes.c_uint64()
+        L.lib().covap_state_residual(h, ctypes.byref(p), ctypes.byref(n))
+        dev = torch.device("cuda", self.device)
+        self.residuals = torch.as_tensor(_CudaArray(p.value, n.value, self.dtype_code), device=dev)
+        L.lib().covap_state_send(h, ctypes.byref(p), ctypes.byref(n))
+        self.send = torch.as_tensor(_CudaArray(p.value, n.value, self.dtype_code), device=dev)
+
+    @staticmethod
+    def zeros(plan: BucketPlan, dtype=None, device: int = 0, ef=None) -> "CompressorState":
+        return CompressorState(plan, dtype, device, ef)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and L._LIB is not None:
+            L._LIB.covap_state_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def num_steps(self) -> int:
+        v = ctypes.c_uint64()
+        L.lib().covap_state_get_step(self._h, ctypes.byref(v))
+        return v.value
+
+    @num_steps.setter
+    def num_steps(self, v: int):
+        L.lib().covap_state_set_step(self._h, int(v))
+
+    def reset(self, stream=None):
+        L.lib().covap_state_reset(self._h, _stream_ptr(stream, self.device))
+
+    # -- kernels ---------------------------------------------------------
+    def filter_pack(self, grad, b0: int = 0, b1: Optional[int] = None, send=None, stream=None):
+        """K1 over buckets [b0, b1) at the current step."""
+        self._check(grad)
+        b1 = len(self.plan.buckets) if b1 is None else b1
+        L.lib().covap_filter_pack(self._h, _ptr(grad), None if send is None else _ptr(send),
+                                  int(b0), int(b1), _stream_ptr(stream, self.device))
+
+    def unpack(self, out, inv_world: float = 1.0, b0: int = 0, b1: Optional[int] = None,
+               recv=None, stream=None):
+        """K2 over buckets [b0, b1) at the current step."""
+        self._check(out)
+        b1 = len(self.plan.buckets) if b1 is None else b1
+        L.lib().covap_unpack(self._h, None if recv is None else _ptr(recv), _ptr(out),
+                             float(inv_world), int(b0), int(b1), _stream_ptr(stream, self.device))
+
+    def step_end(self):
+        L.lib().covap_step_end(self._h)
+
+    def _check(self, t):
+        if t.dtype != self.dtype or not t.is_cuda or not t.is_contiguous():
+            raise InvalidInput("tensor must be a contiguous CUDA tensor of the state's dtype")
+        if t.numel() != self.plan.total_numel():
+            raise InvalidState("gradient length does not match the plan")
+
+
+@dataclass
+class CompressedUpdate:
+    """CompressedUpdate (compress.hpp:49-55): ``selected`` ascending, the
+    payload packed in ``send`` (selected tensors at ``send_offsets``), step."""
+    selected: List[int]
+    step: int
+    send: object
+    send_offsets: List[int]
+    numels: List[int]
+    state: "CompressorState" = None
+
+    def payload_elements(self) -> int:
+        return sum(self.numels)
+
+    def payload(self) -> List[object]:
+        return [self.send[o:o + n] for o, n in zip(self.send_offsets, self.numels)]
+
+
+def covap_compress(gradients, state: CompressorState, config: Optional[CovapConfig] = None,
+                   stream=None) -> CompressedUpdate:
+    """covap_compress (compress.cpp:50-85) on the device: one K1 launch over
+    the whole flat gradient, then ++num_steps."""
+    plan = state.plan
+    if config is not None and (config.interval != plan.interval or config.rule != plan.rule):
+        raise InvalidState("config interval/rule differ from the plan the state was built on")
+    step = state.num_steps
+    state.filter_pack(gradients, stream=stream)
+    state.step_end()
+    sel = plan.selection(step)
+    offs, numels = [], []
+    for t in sel:
+        ts = plan.tensors[t]
+        br = plan.bucket_range(step, ts.bucket)
+        offs.append(br.send_offset + (ts.begin - br.sel_begin))
+        numels.append(ts.numel())
+    return CompressedUpdate(sel, step, state.send, offs, numels, state)
+
+
+def covap_decompress(update: CompressedUpdate, out=None, inv_world: float = 1.0,
+                     recv=None, stream=None):
+    """covap_decompress (compress.cpp:87-103) on the device (K2): payload at
+    the selected slots, zeros elsewhere; ``inv_world`` folds allreduce_mean's
+    scale (trainer.cpp:44-45) into the same pass."""
+    state = update.state
+    torch = _torch()
+    if out is None:
+        out = torch.empty(state.plan.total_numel(), dtype=state.dtype,
+                          device=torch.device("cuda", state.device))
+    saved = state.num_steps
+    state.num_steps = update.step
+    try:
+        state.unpack(out, inv_world, recv=recv, stream=stream)
+    finally:
+        state.num_steps = saved
+    return out
+
+
+# ------------------------------------------------------------ communicator
+
+class Communicator:
+    """One NCCL rank over NVLink/NVSwitch (C1).  Rendezvous of the unique id
+    rides on torch.distributed (plumbing); the data path is NCCL."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        h = ctypes.c_void_p()
+        L.lib().covap_comm_create(uid, int(nranks), int(rank), int(device), ctypes.byref(h))
+        self._h = h
+        self.nranks, self.rank, self.device = int(nranks), int(rank), int(device)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        L.lib().covap_comm_unique_id(buf)
+        return buf.raw
+
+    @staticmethod
+    def from_torch_distributed(device: int) -> "Communicator":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [Communicator.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return Communicator(obj[0], world, rank, device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def allreduce(self, buf, stream=None):
+        L.lib().covap_allreduce(self._h, _ptr(buf), buf.numel(), _dtype_code(buf.dtype),
+                                _stream_ptr(stream, self.device))
+
+    def profile_exchange(self, durations: Sequence[float], comp_ms: float):
+        n = len(durations)
+        d = (ctypes.c_double * max(n, 1))(*durations)
+        a = (ctypes.c_double * max(n, 1))()
+        c = ctypes.c_double()
+        L.lib().covap_comm_profile_exchange(self._h, d, n, float(comp_ms), a, ctypes.byref(c))
+        return list(a[:n]), c.value
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            L.lib().covap_comm_destroy(self._h)
+            self._h = None
+
+
+def allreduce_mean(buf, comm: Optional[Communicator], out=None, stream=None):
+    """allreduce_mean (trainer.cpp:35-47) of one device buffer: NCCL sum in
+    place, then (0 + sum) * 1/P via the K2 kernel with a single full run."""
+    torch = _torch()
+    P = comm.nranks if comm is not None else 1
+    if comm is not None:
+        comm.allreduce(buf, stream)
+    if out is None:
+        out = torch.empty_like(buf)
+    plan = BucketPlan(ModelSpec([LayerSpec("x", buf.numel(), 8 if buf.dtype == torch.float64 else 4)],
+                                bucket_cap_bytes=1 << 62))
+    st = CompressorState(plan, buf.dtype, buf.device.index or 0, EfSchedule(enabled=False))
+    # Phase 0 of a K=1 plan selects everything: one run [0, n) -> send[0, n);
+    # recv is the caller's buffer, so K2 computes (0 + buf) * 1/P.
+    st.unpack(out, 1.0 / P, recv=buf, stream=stream)
+    (stream or torch.cuda.current_stream(buf.device)).synchronize()  # st is freed on return
+    return out
+
+
+# ------------------------------------------------------------ the sync path
+
+class CovapSync:
+    """The per-step gradient synchronisation of one rank (trainer.cpp:365-386
+    restated for one process per GPU):
+
+    * ``sync(grad, out)`` — standalone: K1 -> NCCL allreduce(sum) of the
+      packed selected shards -> K2 (x 1/P, zero fill) -> ++step, on one stream;
+    * ``bucket_ready(b, grad, out)`` + ``finish()`` — the overlapped DDP-hook
+      schedule: K1(b) on the compute stream, allreduce(b's selected range) and
+      K2(b) on the side stream while later buckets are still being produced;
+    * ``dense_bucket_ready`` — the no-compression baseline (trainer.cpp:388).
+    """
+
+    def __init__(self, plan: BucketPlan, comm: Optional[Communicator] = None, dtype=None,
+                 device: int = 0, ef: Optional[EfSchedule] = None):
+        self.plan = plan
+        self.comm = comm
+        self.state = CompressorState(plan, dtype, device, ef)
+        self.device = device
+
+    @property
+    def world(self) -> int:
+        return self.comm.nranks if self.comm is not None else 1
+
+    def _c(self):
+        return None if self.comm is None else self.comm.handle
+
+    def sync(self, grad, out, stream=None):
+        self.state._check(grad)
+        self.state._check(out)
+        L.lib().covap_sync_step(self.state.handle, self._c(), _ptr(grad), _ptr(out),
+                                _stream_ptr(stream, self.device))
+
+    def bucket_ready(self, bucket: int, grad, out, stream=None):
+        L.lib().covap_bucket_ready(self.state.handle, self._c(), int(bucket), _ptr(grad), _ptr(out),
+                                   _stream_ptr(stream, self.device))
+
+    def dense_bucket_ready(self, bucket: int, grad, out, stream=None):
+        L.lib().covap_dense_bucket_ready(self.state.handle, self._c(), int(bucket), _ptr(grad),
+                                         _ptr(out), _stream_ptr(stream, self.device))
+
+    def finish(self, stream=None):
+        L.lib().covap_step_finish(self.state.handle, _stream_ptr(stream, self.device))
+
+    def last_comm_ms(self) -> List[float]:
+        n = len(self.plan.buckets)
+        d = (ctypes.c_double * n)()
+        L.lib().covap_state_last_comm_ms(self.state.handle, d, n)
+        return list(d)
+
+
+# ------------------------------------------------------------ harness
+
+def stream_key(seed: int, rank: int, step: int) -> int:
+    return L.lib().covap_stream_key(int(seed), int(rank), int(step))
+
+
+def generate(out, key: int, kind: int = 0, begin: int = 0, stream=None):
+    """K0: fill ``out`` with the synthetic gradient stream ``key``."""
+    L.lib().covap_generate(_ptr(out), out.numel(), _dtype_code(out.dtype), int(key), int(kind),
+                           int(begin), _stream_ptr(stream, out.device))
+
+
+def spin(us: float, blocks: int = 1, stream=None, device=None):
+    """K3: occupy `blocks` CTAs for `us` microseconds (backward emulator)."""
+    L.lib().covap_spin(float(us), int(blocks), _stream_ptr(stream, device))

@@ -1,0 +1,720 @@
+// covap_capi.cpp — the C-ABI (include/covap_c.h): planner handles, device
+// state, NCCL communicator and the per-step stream schedule.
+//
+// Reference map (paths under /root/reference/proj):
+//   covap_plan_*          model.cpp:36-143, compress.cpp:13-28
+//   covap_state_create    CompressorState::zeros, compress.cpp:37-42
+//   covap_filter_pack     covap_compress, compress.cpp:50-85 (K1)
+//   covap_unpack          covap_decompress + allreduce_mean's scale, compress.cpp:87-103,
+//                         trainer.cpp:41-45 (K2)
+//   covap_sync_step       the COVAP branch of train(), trainer.cpp:365-386
+//   covap_allreduce       allreduce_mean's sum, trainer.cpp:41-43 (C1, NCCL)
+//   covap_ccr / covap_choose_interval / covap_profile_ccr   perf.cpp:40-53, sim.cpp:164-216
+#include "covap_c.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "covap/errors.hpp"
+#include "covap_internal.h"
+#include "covap_plan.hpp"
+
+struct covap_plan {
+  covapb::Plan p;
+};
+
+struct covap_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1;
+  int rank = 0;
+  int device = 0;
+};
+
+struct covap_state {
+  covapb::Plan plan;
+  int dtype = COVAP_F32;
+  size_t esize = 4;
+  int device = 0;
+  covap_ef ef{1, 0.3, 100, 0.1};
+  uint64_t num_steps = 0;
+  void* residual = nullptr;
+  void* send = nullptr;
+  uint64_t send_cap = 0;
+  covapb::Run* d_runs = nullptr;  // all phases back to back, then one full run
+  std::vector<uint64_t> phase_off;
+  covapb::Run* d_full = nullptr;  // {[0, N), dst 0}: the dense (uncompressed) mean
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t done = nullptr;
+  std::vector<cudaEvent_t> ready, arrive, end;  // per bucket
+  std::vector<uint8_t> timed;                   // bucket had a collective in the last step
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+covap_status fail(covap_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+covap_status from_exception() {
+  try {
+    throw;
+  } catch (const covap::InvalidInput& e) {
+    return fail(COVAP_ERR_INVALID_INPUT, e.what());
+  } catch (const covap::InvalidState& e) {
+    return fail(COVAP_ERR_INVALID_STATE, e.what());
+  } catch (const covap::UndefinedRatio& e) {
+    return fail(COVAP_ERR_UNDEFINED_RATIO, e.what());
+  } catch (const covap::IncompleteProfile& e) {
+    return fail(COVAP_ERR_INCOMPLETE_PROFILE, e.what());
+  } catch (const covap::ConfigError& e) {
+    return fail(COVAP_ERR_CONFIG, e.what());
+  } catch (const covap::Error& e) {
+    return fail(COVAP_ERR_GENERIC, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(COVAP_ERR_GENERIC, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(COVAP_ERR_GENERIC, e.what());
+  } catch (...) {
+    return fail(COVAP_ERR_GENERIC, "unknown error");
+  }
+}
+
+struct CudaError {
+  cudaError_t e;
+  const char* where;
+};
+struct NcclError {
+  ncclResult_t r;
+  const char* where;
+};
+
+#define CK(x)                                            \
+  do {                                                   \
+    cudaError_t _e = (x);                                \
+    if (_e != cudaSuccess) throw CudaError{_e, #x};      \
+  } while (0)
+#define NK(x)                                            \
+  do {                                                   \
+    ncclResult_t _r = (x);                               \
+    if (_r != ncclSuccess) throw NcclError{_r, #x};      \
+  } while (0)
+
+// Runs body; maps every failure onto a status code + message.
+template <typename F>
+covap_status guarded(F&& body) {
+  try {
+    body();
+    return COVAP_OK;
+  } catch (const CudaError& ce) {
+    return fail(ce.e == cudaErrorNoDevice || ce.e == cudaErrorInsufficientDriver
+                    ? COVAP_ERR_NO_DEVICE
+                    : COVAP_ERR_CUDA,
+                std::string(ce.where) + ": " + cudaGetErrorString(ce.e));
+  } catch (const NcclError& ne) {
+    return fail(COVAP_ERR_NCCL, std::string(ne.where) + ": " + ncclGetErrorString(ne.r));
+  } catch (...) {
+    return from_exception();
+  }
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void need(bool cond, const char* msg) {
+  if (!cond) throw covap::InvalidInput(msg);
+}
+
+void need_aligned(const void* p, const char* what) {
+  if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+    throw covap::InvalidInput(std::string(what) + " must be 16-byte aligned");
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+const covapb::Phase& phase_of(const covapb::Plan& p, uint64_t step) {
+  return p.phases[step % p.interval];
+}
+
+double coeff_of(const covap_state* s) {
+  return s->ef.enabled ? covapb::ef_coefficient(s->num_steps, 1, s->ef.init_value,
+                                                s->ef.ascend_steps, s->ef.ascend_range)
+                       : 0.0;
+}
+
+ncclDataType_t nccl_type(int dtype) { return dtype == COVAP_F64 ? ncclFloat64 : ncclFloat32; }
+
+int world(const covap_comm* c) { return c ? c->nranks : 1; }
+
+void k1_range(covap_state* s, const void* grad, void* send, uint64_t a, uint64_t b,
+              cudaStream_t st) {
+  const size_t ph = s->num_steps % s->plan.interval;
+  const int nr = static_cast<int>(s->plan.phases[ph].runs.size());
+  CK(covapb::launch_filter_pack(s->dtype, grad, s->residual, send ? send : s->send,
+                                s->d_runs + s->phase_off[ph], nr, a, b, coeff_of(s),
+                                s->ef.enabled, st));
+}
+
+void k2_range(covap_state* s, const void* recv, void* out, double inv, uint64_t a, uint64_t b,
+              cudaStream_t st) {
+  const size_t ph = s->num_steps % s->plan.interval;
+  const int nr = static_cast<int>(s->plan.phases[ph].runs.size());
+  CK(covapb::launch_unpack(s->dtype, recv ? recv : s->send, out, s->d_runs + s->phase_off[ph], nr,
+                           a, b, inv, st));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* covap_last_error(void) { return g_last_error.c_str(); }
+
+int covap_version(void) { return 10000; }
+
+covap_status covap_device_count(int* count) {
+  return guarded([&] {
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (n == 0) throw CudaError{cudaErrorNoDevice, "cudaGetDeviceCount"};
+    *count = n;
+  });
+}
+
+// ---------------------------------------------------------------- planner
+
+covap_status covap_plan_create(const uint64_t* layer_numel, const uint32_t* bytes_per_param,
+                               size_t n_layers, uint64_t cap_bytes, uint32_t interval, int rule,
+                               int shard, covap_plan** out) {
+  return guarded([&] {
+    need(out != nullptr, "out must not be NULL");
+    need(n_layers == 0 || layer_numel != nullptr, "layer_numel must not be NULL");
+    auto* p = new covap_plan;
+    try {
+      p->p = covapb::build_plan(layer_numel, bytes_per_param, n_layers, cap_bytes, interval, rule,
+                                shard);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+void covap_plan_destroy(covap_plan* plan) { delete plan; }
+
+covap_status covap_plan_get_info(const covap_plan* plan, covap_plan_info* info) {
+  return guarded([&] {
+    need(plan && info, "NULL argument");
+    const auto& p = plan->p;
+    info->n_layers = p.n_layers;
+    info->n_buckets = p.buckets.size();
+    info->n_tensors = p.tensors.size();
+    info->total_numel = p.total;
+    info->twice_median = p.twice_median;
+    info->interval = p.interval;
+    info->rule = p.rule;
+    info->sharded = p.sharded ? 1 : 0;
+    info->align = static_cast<int32_t>(covapb::kSendAlign);
+    info->max_send_elems = p.max_send;
+  });
+}
+
+covap_status covap_plan_buckets(const covap_plan* plan, uint64_t* numel, uint64_t* begin,
+                                uint64_t* first_layer, uint64_t* n_layers) {
+  return guarded([&] {
+    need(plan != nullptr, "NULL plan");
+    const auto& bs = plan->p.buckets;
+    for (size_t b = 0; b < bs.size(); ++b) {
+      if (numel) numel[b] = bs[b].numel;
+      if (begin) begin[b] = bs[b].begin;
+      if (first_layer) first_layer[b] = bs[b].first_layer;
+      if (n_layers) n_layers[b] = bs[b].n_layers;
+    }
+  });
+}
+
+covap_status covap_plan_tensors(const covap_plan* plan, uint64_t* bucket, uint64_t* begin,
+                                uint64_t* end) {
+  return guarded([&] {
+    need(plan != nullptr, "NULL plan");
+    const auto& ts = plan->p.tensors;
+    for (size_t t = 0; t < ts.size(); ++t) {
+      if (bucket) bucket[t] = ts[t].bucket;
+      if (begin) begin[t] = ts[t].begin;
+      if (end) end[t] = ts[t].end;
+    }
+  });
+}
+
+covap_status covap_plan_selection(const covap_plan* plan, uint64_t num_steps, uint8_t* keep) {
+  return guarded([&] {
+    need(plan && keep, "NULL argument");
+    const auto& k = phase_of(plan->p, num_steps).keep;
+    std::memcpy(keep, k.data(), k.size());
+  });
+}
+
+covap_status covap_plan_bucket_range(const covap_plan* plan, uint64_t num_steps, size_t bucket,
+                                     covap_bucket_range* out) {
+  return guarded([&] {
+    need(plan && out, "NULL argument");
+    need(bucket < plan->p.buckets.size(), "bucket index out of range");
+    const auto& bk = plan->p.buckets[bucket];
+    const auto& sel = phase_of(plan->p, num_steps).per_bucket[bucket];
+    out->bucket_begin = bk.begin;
+    out->bucket_end = bk.begin + bk.numel;
+    out->sel_begin = sel.sel_begin;
+    out->sel_end = sel.sel_end;
+    out->send_offset = sel.send_offset;
+  });
+}
+
+covap_status covap_plan_send_elems(const covap_plan* plan, uint64_t num_steps,
+                                   uint64_t* send_elems, uint64_t* payload_elems) {
+  return guarded([&] {
+    need(plan != nullptr, "NULL plan");
+    const auto& ph = phase_of(plan->p, num_steps);
+    if (send_elems) *send_elems = ph.send_elems;
+    if (payload_elems) *payload_elems = ph.payload_elems;
+  });
+}
+
+covap_status covap_median_twice(const uint64_t* bucket_numel, size_t n, uint64_t* twice) {
+  return guarded([&] {
+    need(twice != nullptr, "NULL argument");
+    *twice = covapb::median_twice(std::vector<uint64_t>(bucket_numel, bucket_numel + n));
+  });
+}
+
+covap_status covap_select_tensors(uint64_t num_steps, uint32_t interval, size_t count, int rule,
+                                  uint8_t* keep) {
+  return guarded([&] {
+    const auto k = covapb::select(num_steps, interval, count, rule);
+    std::memcpy(keep, k.data(), k.size());
+  });
+}
+
+covap_status covap_ef_coefficient(uint64_t num_steps, const covap_ef* ef, double* coeff) {
+  return guarded([&] {
+    need(ef && coeff, "NULL argument");
+    *coeff = covapb::ef_coefficient(num_steps, ef->enabled, ef->init_value, ef->ascend_steps,
+                                    ef->ascend_range);
+  });
+}
+
+covap_status covap_ccr(double comm_ms, double comp_ms, double* out) {
+  return guarded([&] { *out = covapb::ccr(comm_ms, comp_ms); });
+}
+
+covap_status covap_choose_interval(double ccr_value, uint32_t* out) {
+  return guarded([&] { *out = covapb::choose_interval(ccr_value); });
+}
+
+covap_status covap_profile_ccr(const double* comm_start, const double* comm_end, size_t workers,
+                               size_t expected, size_t n_coll, double comp_ms,
+                               double* aligned_ms, double* naive_ms, double* ccr_out,
+                               uint32_t* interval_out) {
+  return guarded([&] {
+    // sim.cpp:166-201: every expected worker must be present.
+    if (workers != expected || expected == 0)
+      throw covap::IncompleteProfile("expected " + std::to_string(expected) +
+                                     " worker traces, got " + std::to_string(workers));
+    double aligned = 0.0;
+    for (size_t w = 0; w < workers; ++w) naive_ms[w] = 0.0;
+    for (size_t c = 0; c < n_coll; ++c) {
+      double last = comm_start[c];
+      for (size_t w = 1; w < workers; ++w) last = std::max(last, comm_start[w * n_coll + c]);
+      aligned += comm_end[c] - last;  // sim.cpp:202-203
+      for (size_t w = 0; w < workers; ++w) naive_ms[w] += comm_end[c] - comm_start[w * n_coll + c];
+    }
+    *aligned_ms = aligned;
+    *ccr_out = covapb::ccr(aligned, comp_ms);
+    *interval_out = covapb::choose_interval(*ccr_out);
+  });
+}
+
+// ---------------------------------------------------------------- state
+
+void covap_state_destroy(covap_state* s) {
+  if (!s) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s->device);
+  if (s->comm_stream) cudaStreamSynchronize(s->comm_stream);
+  cudaFree(s->residual);
+  cudaFree(s->send);
+  cudaFree(s->d_runs);
+  for (auto e : s->ready) cudaEventDestroy(e);
+  for (auto e : s->arrive) cudaEventDestroy(e);
+  for (auto e : s->end) cudaEventDestroy(e);
+  if (s->done) cudaEventDestroy(s->done);
+  if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete s;
+}
+
+covap_status covap_state_create(const covap_plan* plan, int dtype, int device,
+                                const covap_ef* ef, covap_state** out) {
+  covap_state* s = nullptr;
+  const covap_status st = guarded([&] {
+    need(plan && out, "NULL argument");
+    need(dtype == COVAP_F32 || dtype == COVAP_F64, "dtype must be COVAP_F32 or COVAP_F64");
+    if (ef && ef->enabled && ef->ascend_steps < 1)
+      throw covap::InvalidInput("ascend_steps must be >= 1");
+    DeviceGuard dg(device);
+    s = new covap_state;
+    s->plan = plan->p;
+    s->dtype = dtype;
+    s->esize = dtype == COVAP_F64 ? 8 : 4;
+    s->device = device;
+    if (ef) s->ef = *ef;
+    const uint64_t n = s->plan.total;
+    CK(cudaMalloc(&s->residual, std::max<uint64_t>(n, 1) * s->esize));
+    CK(cudaMemset(s->residual, 0, std::max<uint64_t>(n, 1) * s->esize));
+    s->send_cap = std::max<uint64_t>(s->plan.max_send, 1);
+    CK(cudaMalloc(&s->send, s->send_cap * s->esize));
+    CK(cudaMemset(s->send, 0, s->send_cap * s->esize));  // alignment gaps stay zero forever
+    std::vector<covapb::Run> all;
+    for (const auto& ph : s->plan.phases) {
+      s->phase_off.push_back(all.size());
+      all.insert(all.end(), ph.runs.begin(), ph.runs.end());
+    }
+    const size_t full_off = all.size();
+    all.push_back(covapb::Run{0, n, 0});
+    CK(cudaMalloc(&s->d_runs, all.size() * sizeof(covapb::Run)));
+    CK(cudaMemcpy(s->d_runs, all.data(), all.size() * sizeof(covapb::Run),
+                  cudaMemcpyHostToDevice));
+    s->d_full = s->d_runs + full_off;
+    CK(cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
+    const size_t nb = s->plan.buckets.size();
+    s->ready.resize(nb);
+    s->arrive.resize(nb);
+    s->end.resize(nb);
+    s->timed.assign(nb, 0);
+    for (size_t b = 0; b < nb; ++b) {
+      CK(cudaEventCreateWithFlags(&s->ready[b], cudaEventDisableTiming));
+      CK(cudaEventCreate(&s->arrive[b]));
+      CK(cudaEventCreate(&s->end[b]));
+    }
+    *out = s;
+  });
+  if (st != COVAP_OK && s) {
+    covap_state_destroy(s);
+  }
+  return st;
+}
+
+covap_status covap_state_residual(covap_state* s, void** dev_ptr, uint64_t* n) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    if (dev_ptr) *dev_ptr = s->residual;
+    if (n) *n = s->plan.total;
+  });
+}
+
+covap_status covap_state_send(covap_state* s, void** dev_ptr, uint64_t* capacity) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    if (dev_ptr) *dev_ptr = s->send;
+    if (capacity) *capacity = s->send_cap;
+  });
+}
+
+covap_status covap_state_get_step(const covap_state* s, uint64_t* num_steps) {
+  return guarded([&] {
+    need(s && num_steps, "NULL argument");
+    *num_steps = s->num_steps;
+  });
+}
+
+covap_status covap_state_set_step(covap_state* s, uint64_t num_steps) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    s->num_steps = num_steps;
+  });
+}
+
+covap_status covap_state_reset(covap_state* s, void* stream) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    DeviceGuard dg(s->device);
+    CK(cudaMemsetAsync(s->residual, 0, std::max<uint64_t>(s->plan.total, 1) * s->esize,
+                       as_stream(stream)));
+  });
+}
+
+// ---------------------------------------------------------------- K1 / K2
+
+covap_status covap_filter_pack(covap_state* s, const void* grad, void* send, size_t b0, size_t b1,
+                               void* stream) {
+  return guarded([&] {
+    need(s != nullptr && grad != nullptr, "NULL argument");
+    need(b0 <= b1 && b1 <= s->plan.buckets.size(), "bucket range out of bounds");
+    need_aligned(grad, "grad");
+    if (send) need_aligned(send, "send");
+    if (b0 == b1) return;
+    DeviceGuard dg(s->device);
+    const uint64_t a = s->plan.buckets[b0].begin;
+    const uint64_t b = s->plan.buckets[b1 - 1].begin + s->plan.buckets[b1 - 1].numel;
+    k1_range(s, grad, send, a, b, as_stream(stream));
+  });
+}
+
+covap_status covap_unpack(covap_state* s, const void* recv, void* out, double inv_world,
+                          size_t b0, size_t b1, void* stream) {
+  return guarded([&] {
+    need(s != nullptr && out != nullptr, "NULL argument");
+    need(b0 <= b1 && b1 <= s->plan.buckets.size(), "bucket range out of bounds");
+    need_aligned(out, "out");
+    if (recv) need_aligned(recv, "recv");
+    if (b0 == b1) return;
+    DeviceGuard dg(s->device);
+    const uint64_t a = s->plan.buckets[b0].begin;
+    const uint64_t b = s->plan.buckets[b1 - 1].begin + s->plan.buckets[b1 - 1].numel;
+    k2_range(s, recv, out, inv_world, a, b, as_stream(stream));
+  });
+}
+
+covap_status covap_step_end(covap_state* s) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    ++s->num_steps;
+  });
+}
+
+covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad, void* out,
+                             void* stream) {
+  return guarded([&] {
+    need(s && grad && out, "NULL argument");
+    need_aligned(grad, "grad");
+    need_aligned(out, "out");
+    if (comm) need(comm->device == s->device, "communicator and state are on different devices");
+    DeviceGuard dg(s->device);
+    cudaStream_t st = as_stream(stream);
+    const uint64_t n = s->plan.total;
+    const auto& ph = phase_of(s->plan, s->num_steps);
+    k1_range(s, grad, nullptr, 0, n, st);
+    const int P = world(comm);
+    if (P > 1 && ph.send_elems > 0)
+      NK(ncclAllReduce(s->send, s->send, ph.send_elems, nccl_type(s->dtype), ncclSum, comm->nccl,
+                       st));
+    k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 0, n, st);
+    ++s->num_steps;
+  });
+}
+
+covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket, const void* grad,
+                                void* out, void* stream) {
+  return guarded([&] {
+    need(s && grad && out, "NULL argument");
+    need(bucket < s->plan.buckets.size(), "bucket index out of range");
+    need_aligned(grad, "grad");
+    need_aligned(out, "out");
+    DeviceGuard dg(s->device);
+    cudaStream_t st = as_stream(stream);
+    const auto& bk = s->plan.buckets[bucket];
+    const auto& sel = phase_of(s->plan, s->num_steps).per_bucket[bucket];
+    const uint64_t a = bk.begin, b = bk.begin + bk.numel;
+    k1_range(s, grad, nullptr, a, b, st);
+    CK(cudaEventRecord(s->ready[bucket], st));
+    CK(cudaStreamWaitEvent(s->comm_stream, s->ready[bucket], 0));
+    const int P = world(comm);
+    const uint64_t len = sel.sel_end - sel.sel_begin;
+    s->timed[bucket] = len > 0 ? 1 : 0;
+    CK(cudaEventRecord(s->arrive[bucket], s->comm_stream));
+    if (P > 1 && len > 0)
+      NK(ncclAllReduce(static_cast<char*>(s->send) + sel.send_offset * s->esize,
+                       static_cast<char*>(s->send) + sel.send_offset * s->esize, len,
+                       nccl_type(s->dtype), ncclSum, comm->nccl, s->comm_stream));
+    CK(cudaEventRecord(s->end[bucket], s->comm_stream));
+    k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), a, b, s->comm_stream);
+  });
+}
+
+covap_status covap_dense_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket, void* grad,
+                                      void* out, void* stream) {
+  return guarded([&] {
+    need(s && grad && out, "NULL argument");
+    need(bucket < s->plan.buckets.size(), "bucket index out of range");
+    need_aligned(grad, "grad");
+    need_aligned(out, "out");
+    DeviceGuard dg(s->device);
+    cudaStream_t st = as_stream(stream);
+    const auto& bk = s->plan.buckets[bucket];
+    const uint64_t a = bk.begin, b = bk.begin + bk.numel;
+    CK(cudaEventRecord(s->ready[bucket], st));
+    CK(cudaStreamWaitEvent(s->comm_stream, s->ready[bucket], 0));
+    const int P = world(comm);
+    s->timed[bucket] = 1;
+    CK(cudaEventRecord(s->arrive[bucket], s->comm_stream));
+    if (P > 1)
+      NK(ncclAllReduce(static_cast<char*>(grad) + a * s->esize,
+                       static_cast<char*>(grad) + a * s->esize, bk.numel, nccl_type(s->dtype),
+                       ncclSum, comm->nccl, s->comm_stream));
+    CK(cudaEventRecord(s->end[bucket], s->comm_stream));
+    // allreduce_mean's "0 + sum, then x 1/P" (trainer.cpp:41-45) in place.
+    CK(covapb::launch_unpack(s->dtype, grad, out, s->d_full, 1, a, b,
+                             1.0 / static_cast<double>(P), s->comm_stream));
+  });
+}
+
+covap_status covap_step_finish(covap_state* s, void* stream) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    DeviceGuard dg(s->device);
+    CK(cudaEventRecord(s->done, s->comm_stream));
+    CK(cudaStreamWaitEvent(as_stream(stream), s->done, 0));
+    ++s->num_steps;
+  });
+}
+
+covap_status covap_state_last_comm_ms(covap_state* s, double* dur, size_t n) {
+  return guarded([&] {
+    need(s && dur, "NULL argument");
+    need(n <= s->plan.buckets.size(), "n exceeds bucket count");
+    DeviceGuard dg(s->device);
+    CK(cudaStreamSynchronize(s->comm_stream));
+    for (size_t b = 0; b < n; ++b) {
+      if (!s->timed[b]) {
+        dur[b] = -1.0;
+        continue;
+      }
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, s->arrive[b], s->end[b]));
+      dur[b] = ms;
+    }
+  });
+}
+
+// ---------------------------------------------------------------- comm
+
+covap_status covap_comm_unique_id(uint8_t id[128]) {
+  return guarded([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId uid;
+    NK(ncclGetUniqueId(&uid));
+    std::memcpy(id, &uid, 128);
+  });
+}
+
+covap_status covap_comm_create(const uint8_t id[128], int nranks, int rank, int device,
+                               covap_comm** out) {
+  return guarded([&] {
+    need(id && out, "NULL argument");
+    need(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / world size");
+    DeviceGuard dg(device);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    auto* c = new covap_comm;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    const ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      throw NcclError{r, "ncclCommInitRank"};
+    }
+    *out = c;
+  });
+}
+
+void covap_comm_destroy(covap_comm* c) {
+  if (!c) return;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+}
+
+covap_status covap_comm_size(const covap_comm* c, int* nranks, int* rank) {
+  return guarded([&] {
+    need(c != nullptr, "NULL comm");
+    if (nranks) *nranks = c->nranks;
+    if (rank) *rank = c->rank;
+  });
+}
+
+covap_status covap_allreduce(covap_comm* c, void* buf, uint64_t count, int dtype, void* stream) {
+  return guarded([&] {
+    need(c && buf, "NULL argument");
+    if (count == 0 || c->nranks == 1) return;
+    DeviceGuard dg(c->device);
+    NK(ncclAllReduce(buf, buf, count, nccl_type(dtype), ncclSum, c->nccl, as_stream(stream)));
+  });
+}
+
+covap_status covap_comm_profile_exchange(covap_comm* c, const double* dur, size_t n_coll,
+                                         double comp_ms, double* aligned_ms, double* comp_out) {
+  return guarded([&] {
+    need(dur && aligned_ms && comp_out, "NULL argument");
+    if (!c || c->nranks == 1) {
+      std::copy(dur, dur + n_coll, aligned_ms);
+      *comp_out = comp_ms;
+      return;
+    }
+    DeviceGuard dg(c->device);
+    std::vector<double> host(n_coll + 1);
+    std::copy(dur, dur + n_coll, host.begin());
+    host[n_coll] = comp_ms;
+    double* d = nullptr;
+    cudaStream_t st = nullptr;
+    CK(cudaMalloc(&d, host.size() * sizeof(double)));
+    try {
+      CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      CK(cudaMemcpyAsync(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      NK(ncclGroupStart());
+      if (n_coll) NK(ncclAllReduce(d, d, n_coll, ncclFloat64, ncclMin, c->nccl, st));
+      NK(ncclBroadcast(d + n_coll, d + n_coll, 1, ncclFloat64, 0, c->nccl, st));
+      NK(ncclGroupEnd());
+      CK(cudaMemcpyAsync(host.data(), d, host.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    } catch (...) {
+      if (st) cudaStreamDestroy(st);
+      cudaFree(d);
+      throw;
+    }
+    cudaStreamDestroy(st);
+    cudaFree(d);
+    std::copy(host.begin(), host.begin() + n_coll, aligned_ms);
+    *comp_out = host[n_coll];
+  });
+}
+
+// ---------------------------------------------------------------- harness
+
+uint64_t covap_stream_key(uint64_t seed, uint64_t rank, uint64_t step) {
+  return covapb::stream_key(seed, rank, step);
+}
+
+covap_status covap_generate(void* out, uint64_t n, int dtype, uint64_t key, int kind,
+                            uint64_t begin, void* stream) {
+  return guarded([&] {
+    need(out != nullptr, "NULL out");
+    need(dtype == COVAP_F32 || dtype == COVAP_F64, "bad dtype");
+    need_aligned(out, "out");
+    CK(covapb::launch_generate(dtype, out, n, key, kind, begin, as_stream(stream)));
+  });
+}
+
+covap_status covap_spin(double us, int blocks, void* stream) {
+  return guarded([&] { CK(covapb::launch_spin(us, blocks, as_stream(stream))); });
+}
+
+}  // extern "C"

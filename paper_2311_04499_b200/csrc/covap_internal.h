@@ -1,0 +1,39 @@
+// covap_internal.h — shared between the host planner / C-ABI (C++) and the
+// sm_100a kernels (CUDA).  Not installed; the public boundary is
+// include/covap_c.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace covapb {
+
+// One maximal contiguous run of selected elements at one phase: flat
+// [begin, end) goes to send[dst, dst + (end - begin)).  dst == begin (mod
+// kSendAlign) so that 16-byte vectors of the gradient map onto 16-byte
+// vectors of the send buffer.  Within a run, consecutive selected effective
+// tensors are contiguous both in the flat layout and in the send buffer.
+struct Run {
+  uint64_t begin;
+  uint64_t end;
+  uint64_t dst;
+};
+
+constexpr uint64_t kSendAlign = 32;  // elements (128 B fp32, 256 B fp64)
+
+// K1: c = g + coeff*r for flat [a, b); selected -> send, r = 0; else r = c.
+cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, const Run* runs,
+                               int nruns, uint64_t a, uint64_t b, double coeff, int ef,
+                               cudaStream_t s);
+// K2: out = in-run ? (0 + recv[dst + e - begin]) * inv : 0 for flat [a, b).
+cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
+                          uint64_t a, uint64_t b, double inv, cudaStream_t s);
+// K0: synthetic gradients.
+cudaError_t launch_generate(int dtype, void* out, uint64_t n, uint64_t key, int kind,
+                            uint64_t begin, cudaStream_t s);
+// K3: spin emulator.
+cudaError_t launch_spin(double us, int blocks, cudaStream_t s);
+
+uint64_t stream_key(uint64_t seed, uint64_t rank, uint64_t step);
+
+}  // namespace covapb

@@ -1,0 +1,164 @@
+// covap_plan.cpp — host planner (see covap_plan.hpp for the reference map).
+#include "covap_plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <string>
+
+#include "covap/errors.hpp"
+
+namespace covapb {
+
+uint64_t median_twice(std::vector<uint64_t> sizes) {
+  if (sizes.empty()) throw covap::InvalidInput("median_numel needs at least one bucket");
+  std::sort(sizes.begin(), sizes.end(), std::greater<>());
+  const size_t n = sizes.size(), mid = n / 2;
+  if (n % 2 == 1) return 2 * sizes[mid];
+  if (n == 2) return sizes[0] + sizes[1];
+  // Even n > 2: the reference averages the pair one rank below the
+  // conventional middle of the descending order (model.cpp:77-81).
+  return sizes[mid] + sizes[mid + 1];
+}
+
+std::vector<uint8_t> select(uint64_t step, uint32_t interval, size_t count, int rule) {
+  if (interval < 1) throw covap::InvalidInput("selection interval must be >= 1");
+  if (count < 1) throw covap::InvalidInput("selection needs at least one tensor");
+  const uint64_t phase = step % interval;
+  std::vector<uint8_t> keep(count);
+  for (size_t t = 0; t < count; ++t) {
+    const uint64_t r = t % interval;
+    keep[t] = rule == 0 ? (r == phase) : ((r + phase) % interval == 0);
+  }
+  return keep;
+}
+
+double ef_coefficient(uint64_t step, int /*enabled*/, double init, uint64_t ascend,
+                      double range) {
+  if (ascend < 1) throw covap::InvalidInput("ascend_steps must be >= 1");
+  const double raised = init + static_cast<double>(step / ascend) * range;
+  return std::min(raised, 1.0);
+}
+
+double ccr(double comm_ms, double comp_ms) {
+  if (comm_ms < 0.0 || comp_ms < 0.0) throw covap::InvalidInput("phase times must be non-negative");
+  if (comp_ms == 0.0) {
+    if (comm_ms == 0.0) return 0.0;
+    throw covap::UndefinedRatio("CCR is undefined for zero computation time");
+  }
+  return comm_ms / comp_ms;
+}
+
+uint32_t choose_interval(double ccr_value) {
+  if (ccr_value < 0.0) throw covap::InvalidInput("CCR must be non-negative");
+  const double up = std::ceil(ccr_value);
+  return up < 1.0 ? 1u : static_cast<uint32_t>(up);
+}
+
+Plan build_plan(const uint64_t* layer_numel, const uint32_t* bpp, size_t n_layers,
+                uint64_t cap_bytes, uint32_t interval, int rule, int shard) {
+  // ModelSpec::validate (model.cpp:24-34).
+  if (n_layers == 0) throw covap::InvalidInput("model has no layers");
+  for (size_t i = 0; i < n_layers; ++i) {
+    const std::string name = "l" + std::to_string(i);
+    if (layer_numel[i] < 1) throw covap::InvalidInput("layer '" + name + "' has param_count < 1");
+    const uint32_t w = bpp ? bpp[i] : 4u;
+    if (w != 2 && w != 4)
+      throw covap::InvalidInput("layer '" + name + "' has bytes_per_param outside {2, 4}");
+  }
+  if (cap_bytes < 1) throw covap::InvalidInput("bucket capacity must be at least one byte");
+  if (interval < 1) throw covap::InvalidInput("shard interval must be >= 1");
+  if (rule != 0 && rule != 1) throw covap::InvalidInput("unknown selection rule");
+
+  Plan plan;
+  plan.n_layers = n_layers;
+  plan.interval = interval;
+  plan.rule = rule;
+
+  // Greedy bucketing: a layer joins the open bucket unless that bucket is
+  // non-empty and would exceed the cap (model.cpp:53); an oversized layer
+  // therefore sits alone, unsplit.
+  PlanBucket cur;
+  bool open = false;
+  uint64_t flat = 0;
+  for (size_t i = 0; i < n_layers; ++i) {
+    const uint64_t bytes = layer_numel[i] * (bpp ? bpp[i] : 4u);
+    if (open && cur.bytes + bytes > cap_bytes) {
+      plan.buckets.push_back(cur);
+      cur = PlanBucket{};
+      open = false;
+    }
+    if (!open) {
+      cur.first_layer = i;
+      cur.begin = flat;
+      open = true;
+    }
+    cur.numel += layer_numel[i];
+    cur.bytes += bytes;
+    cur.n_layers += 1;
+    flat += layer_numel[i];
+  }
+  plan.buckets.push_back(cur);
+  plan.total = flat;
+
+  std::vector<uint64_t> sizes;
+  for (const auto& b : plan.buckets) sizes.push_back(b.numel);
+  plan.twice_median = median_twice(sizes);
+
+  // shard_plan runs only when K > 1 in train() (trainer.cpp:269-271).
+  plan.sharded = shard < 0 ? interval > 1 : shard != 0;
+  for (size_t b = 0; b < plan.buckets.size(); ++b) {
+    const auto& bk = plan.buckets[b];
+    uint64_t parts = 1;
+    if (plan.sharded) {
+      const uint64_t ratio = (2 * bk.numel) / plan.twice_median;  // model.hpp:56
+      if (ratio >= 2) parts = std::min<uint64_t>(ratio, interval);  // model.cpp:103-104
+    }
+    const uint64_t base = bk.numel / parts, extra = bk.numel % parts;
+    uint64_t off = 0;
+    for (uint64_t p = 0; p < parts; ++p) {
+      const uint64_t size = base + (p < extra ? 1 : 0);  // first numel%parts get +1
+      plan.tensors.push_back(PlanTensor{b, bk.begin + off, bk.begin + off + size});
+      off += size;
+    }
+  }
+
+  // Per-phase send layout.  Selection depends only on (step mod K, K,
+  // count), so K phase tables describe every step (compress.cpp:18-24).
+  plan.phases.resize(interval);
+  for (uint32_t p = 0; p < interval; ++p) {
+    Phase& ph = plan.phases[p];
+    ph.keep = select(p, interval, plan.tensors.size(), rule);
+    ph.per_bucket.assign(plan.buckets.size(), BucketSel{});
+    uint64_t cursor = 0;
+    for (size_t t = 0; t < plan.tensors.size(); ++t) {
+      if (!ph.keep[t]) continue;
+      const PlanTensor& ts = plan.tensors[t];
+      if (!ph.runs.empty() && ph.runs.back().end == ts.begin && t > 0 && ph.keep[t - 1]) {
+        ph.runs.back().end = ts.end;  // extend the run: contiguous in flat and in send
+      } else {
+        const uint64_t dst = cursor + ((ts.begin + kSendAlign - cursor % kSendAlign) % kSendAlign);
+        ph.runs.push_back(Run{ts.begin, ts.end, dst});
+      }
+      cursor = ph.runs.back().dst + (ph.runs.back().end - ph.runs.back().begin);
+      ph.payload_elems += ts.end - ts.begin;
+      BucketSel& bs = ph.per_bucket[ts.bucket];
+      const uint64_t off = ph.runs.back().dst + (ts.begin - ph.runs.back().begin);
+      if (bs.sel_end == bs.sel_begin) {
+        bs.sel_begin = ts.begin;
+        bs.sel_end = ts.end;
+        bs.send_offset = off;
+      } else {
+        // Shards of one bucket are <= K consecutive indices, so at most one
+        // is selected per phase; a second one would break the per-bucket
+        // single-range invariant the overlapped schedule relies on.
+        throw covap::Error("internal: two selected shards in one bucket");
+      }
+    }
+    ph.send_elems = cursor;
+    plan.max_send = std::max(plan.max_send, cursor);
+  }
+  return plan;
+}
+
+}  // namespace covapb
