@@ -149,11 +149,14 @@ covap_status covap_state_reset(covap_state* state, void* stream);
  * r = 0, unselected -> r = c.  send may be NULL (state scratch). */
 covap_status covap_filter_pack(covap_state* state, const void* grad, void* send, size_t b0,
                                size_t b1, void* stream);
-/* K2 (unpack_scale) over buckets [b0, b1): out[sel] = (0 + recv) * inv_world
- * (allreduce_mean's sum-then-scale, trainer.cpp:41-45), out[unsel] = 0
- * (covap_decompress's zero fill, compress.cpp:91-100).  recv may be NULL
- * (state scratch, i.e. the in-place allreduce result).  out may alias grad. */
-covap_status covap_unpack(covap_state* state, const void* recv, void* out, double inv_world,
+/* K2 (unpack_scale) over buckets [b0, b1): out[unsel] = 0 (covap_decompress's
+ * zero fill, compress.cpp:91-100) and out[sel] = f(recv) with
+ *   mean = 1: f(x) = (0 + x) * scale  -- allreduce_mean's sum-then-scale
+ *             (trainer.cpp:41-45) fused, scale = 1/P;
+ *   mean = 0: f(x) = x * scale        -- the plain embedding (compress.cpp:100).
+ * recv may be NULL (state scratch, i.e. the in-place allreduce result).
+ * out may alias the gradient passed to K1. */
+covap_status covap_unpack(covap_state* state, const void* recv, void* out, double scale, int mean,
                           size_t b0, size_t b1, void* stream);
 /* ++num_steps (compress.cpp:83). */
 covap_status covap_step_end(covap_state* state);

@@ -403,13 +403,16 @@ class CompressorState:
         L.lib().covap_filter_pack(self._h, _ptr(grad), None if send is None else _ptr(send),
                                   int(b0), int(b1), _stream_ptr(stream, self.device))
 
-    def unpack(self, out, inv_world: float = 1.0, b0: int = 0, b1: Optional[int] = None,
-               recv=None, stream=None):
-        """K2 over buckets [b0, b1) at the current step."""
+    def unpack(self, out, scale: float = 1.0, mean: bool = True, b0: int = 0,
+               b1: Optional[int] = None, recv=None, stream=None):
+        """K2 over buckets [b0, b1) at the current step: selected slots get
+        (0 + recv) * scale (mean=True, allreduce_mean's order) or recv * scale
+        (mean=False, covap_decompress); the rest is zero-filled."""
         self._check(out)
         b1 = len(self.plan.buckets) if b1 is None else b1
         L.lib().covap_unpack(self._h, None if recv is None else _ptr(recv), _ptr(out),
-                             float(inv_world), int(b0), int(b1), _stream_ptr(stream, self.device))
+                             float(scale), 1 if mean else 0, int(b0), int(b1),
+                             _stream_ptr(stream, self.device))
 
     def step_end(self):
         L.lib().covap_step_end(self._h)
@@ -459,11 +462,12 @@ def covap_compress(gradients, state: CompressorState, config: Optional[CovapConf
     return CompressedUpdate(sel, step, state.send, offs, numels, state)
 
 
-def covap_decompress(update: CompressedUpdate, out=None, inv_world: float = 1.0,
-                     recv=None, stream=None):
+def covap_decompress(update: CompressedUpdate, out=None, recv=None, world: int = 0,
+                     stream=None):
     """covap_decompress (compress.cpp:87-103) on the device (K2): payload at
-    the selected slots, zeros elsewhere; ``inv_world`` folds allreduce_mean's
-    scale (trainer.cpp:44-45) into the same pass."""
+    the selected slots, zeros elsewhere.  With ``world`` = P > 0 the pass also
+    applies allreduce_mean's (0 + sum) * 1/P (trainer.cpp:41-45) to a summed
+    ``recv`` — the fused unpack/scale of the sync path."""
     state = update.state
     torch = _torch()
     if out is None:
@@ -472,7 +476,10 @@ def covap_decompress(update: CompressedUpdate, out=None, inv_world: float = 1.0,
     saved = state.num_steps
     state.num_steps = update.step
     try:
-        state.unpack(out, inv_world, recv=recv, stream=stream)
+        if world > 0:
+            state.unpack(out, 1.0 / world, True, recv=recv, stream=stream)
+        else:
+            state.unpack(out, 1.0, False, recv=recv, stream=stream)
     finally:
         state.num_steps = saved
     return out
@@ -540,7 +547,7 @@ def allreduce_mean(buf, comm: Optional[Communicator], out=None, stream=None):
     st = CompressorState(plan, buf.dtype, buf.device.index or 0, EfSchedule(enabled=False))
     # Phase 0 of a K=1 plan selects everything: one run [0, n) -> send[0, n);
     # recv is the caller's buffer, so K2 computes (0 + buf) * 1/P.
-    st.unpack(out, 1.0 / P, recv=buf, stream=stream)
+    st.unpack(out, 1.0 / P, True, recv=buf, stream=stream)
     (stream or torch.cuda.current_stream(buf.device)).synchronize()  # st is freed on return
     return out
 

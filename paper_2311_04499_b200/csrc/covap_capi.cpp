@@ -173,12 +173,12 @@ void k1_range(covap_state* s, const void* grad, void* send, uint64_t a, uint64_t
                                 s->ef.enabled, st));
 }
 
-void k2_range(covap_state* s, const void* recv, void* out, double inv, uint64_t a, uint64_t b,
-              cudaStream_t st) {
+void k2_range(covap_state* s, const void* recv, void* out, double inv, int mean, uint64_t a,
+              uint64_t b, cudaStream_t st) {
   const size_t ph = s->num_steps % s->plan.interval;
   const int nr = static_cast<int>(s->plan.phases[ph].runs.size());
   CK(covapb::launch_unpack(s->dtype, recv ? recv : s->send, out, s->d_runs + s->phase_off[ph], nr,
-                           a, b, inv, st));
+                           a, b, inv, mean, st));
 }
 
 }  // namespace
@@ -479,7 +479,7 @@ covap_status covap_filter_pack(covap_state* s, const void* grad, void* send, siz
   });
 }
 
-covap_status covap_unpack(covap_state* s, const void* recv, void* out, double inv_world,
+covap_status covap_unpack(covap_state* s, const void* recv, void* out, double scale, int mean,
                           size_t b0, size_t b1, void* stream) {
   return guarded([&] {
     need(s != nullptr && out != nullptr, "NULL argument");
@@ -490,7 +490,7 @@ covap_status covap_unpack(covap_state* s, const void* recv, void* out, double in
     DeviceGuard dg(s->device);
     const uint64_t a = s->plan.buckets[b0].begin;
     const uint64_t b = s->plan.buckets[b1 - 1].begin + s->plan.buckets[b1 - 1].numel;
-    k2_range(s, recv, out, inv_world, a, b, as_stream(stream));
+    k2_range(s, recv, out, scale, mean, a, b, as_stream(stream));
   });
 }
 
@@ -517,7 +517,7 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
     if (P > 1 && ph.send_elems > 0)
       NK(ncclAllReduce(s->send, s->send, ph.send_elems, nccl_type(s->dtype), ncclSum, comm->nccl,
                        st));
-    k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 0, n, st);
+    k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, 0, n, st);
     ++s->num_steps;
   });
 }
@@ -546,7 +546,7 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
                        static_cast<char*>(s->send) + sel.send_offset * s->esize, len,
                        nccl_type(s->dtype), ncclSum, comm->nccl, s->comm_stream));
     CK(cudaEventRecord(s->end[bucket], s->comm_stream));
-    k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), a, b, s->comm_stream);
+    k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, a, b, s->comm_stream);
   });
 }
 
@@ -573,7 +573,7 @@ covap_status covap_dense_bucket_ready(covap_state* s, covap_comm* comm, size_t b
     CK(cudaEventRecord(s->end[bucket], s->comm_stream));
     // allreduce_mean's "0 + sum, then x 1/P" (trainer.cpp:41-45) in place.
     CK(covapb::launch_unpack(s->dtype, grad, out, s->d_full, 1, a, b,
-                             1.0 / static_cast<double>(P), s->comm_stream));
+                             1.0 / static_cast<double>(P), 1, s->comm_stream));
   });
 }
 

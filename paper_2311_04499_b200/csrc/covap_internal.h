@@ -25,9 +25,10 @@ constexpr uint64_t kSendAlign = 32;  // elements (128 B fp32, 256 B fp64)
 cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, const Run* runs,
                                int nruns, uint64_t a, uint64_t b, double coeff, int ef,
                                cudaStream_t s);
-// K2: out = in-run ? (0 + recv[dst + e - begin]) * inv : 0 for flat [a, b).
+// K2: out = in-run ? f(recv[dst + e - begin]) : 0 for flat [a, b), with
+// f(x) = (0 + x) * inv when mean (allreduce_mean), x * inv otherwise.
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
-                          uint64_t a, uint64_t b, double inv, cudaStream_t s);
+                          uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s);
 // K0: synthetic gradients.
 cudaError_t launch_generate(int dtype, void* out, uint64_t n, uint64_t key, int kind,
                             uint64_t begin, cudaStream_t s);

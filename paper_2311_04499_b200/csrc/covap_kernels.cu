@@ -182,31 +182,39 @@ __global__ void __launch_bounds__(kThreads)
 
 // ---------------------------------------------------------------- K2
 
+// mean: allreduce_mean's (0.0 + sum) * (1/P) (trainer.cpp:41-45) -- the
+// leading +0 turns a -0 sum into +0 exactly as the reference does; otherwise
+// the plain embedding of covap_decompress (compress.cpp:100) times `inv`.
+template <typename T>
+__device__ __forceinline__ T scale_of(T x, T inv, int mean) {
+  return mul_rn(mean ? add_rn(T(0), x) : x, inv);
+}
+
 template <typename T>
 __device__ __forceinline__ void unpack_scalar(const T* __restrict__ recv, T* __restrict__ out,
                                               const Run* __restrict__ runs, int nruns, uint64_t e,
-                                              T inv) {
+                                              T inv, int mean) {
   const int j = run_of(runs, nruns, first_run_after(runs, nruns, e), e);
-  out[e] = (j >= 0) ? mul_rn(add_rn(T(0), recv[runs[j].dst + (e - runs[j].begin)]), inv) : T(0);
+  out[e] = (j >= 0) ? scale_of(recv[runs[j].dst + (e - runs[j].begin)], inv, mean) : T(0);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
     unpack_kernel(const T* __restrict__ recv, T* __restrict__ out, const Run* __restrict__ runs,
-                  int nruns, uint64_t a, uint64_t b, T inv) {
+                  int nruns, uint64_t a, uint64_t b, T inv, int mean) {
   using V = typename V16<T>::type;
   constexpr int W = V16<T>::n;
   const uint64_t A = (a + W - 1) / W * W;
   if (A >= b) {
     if (blockIdx.x == 0)
       for (uint64_t e = a + threadIdx.x; e < b; e += blockDim.x)
-        unpack_scalar(recv, out, runs, nruns, e, inv);
+        unpack_scalar(recv, out, runs, nruns, e, inv, mean);
     return;
   }
   const uint64_t B = b / W * W;
   if (blockIdx.x == 0) {
-    if (threadIdx.x < A - a) unpack_scalar(recv, out, runs, nruns, a + threadIdx.x, inv);
-    if (threadIdx.x < b - B) unpack_scalar(recv, out, runs, nruns, B + threadIdx.x, inv);
+    if (threadIdx.x < A - a) unpack_scalar(recv, out, runs, nruns, a + threadIdx.x, inv, mean);
+    if (threadIdx.x < b - B) unpack_scalar(recv, out, runs, nruns, B + threadIdx.x, inv, mean);
   }
   const uint64_t nvec = (B - A) / W;
   const uint64_t v0 = nvec * blockIdx.x / gridDim.x;
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(kThreads)
         if (v >= v1) continue;
         V o;
 #pragma unroll
-        for (int k = 0; k < W; ++k) lane<V, T>(o, k) = mul_rn(add_rn(T(0), lane<V, T>(x[u], k)), inv);
+        for (int k = 0; k < W; ++k) lane<V, T>(o, k) = scale_of(lane<V, T>(x[u], k), inv, mean);
         __stcs(ov + v, o);
       }
     } else {
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(kThreads)
           const uint64_t ee = e + k;
           while (jj < nruns && runs[jj].end <= ee) ++jj;
           lane<V, T>(o, k) = (jj < nruns && runs[jj].begin <= ee)
-                                 ? mul_rn(add_rn(T(0), recv[runs[jj].dst + (ee - runs[jj].begin)]), inv)
+                                 ? scale_of(recv[runs[jj].dst + (ee - runs[jj].begin)], inv, mean)
                                  : T(0);
         }
         __stcs(ov + v, o);
@@ -378,19 +386,19 @@ cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, co
 }
 
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
-                          uint64_t a, uint64_t b, double inv, cudaStream_t s) {
+                          uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s) {
   if (b <= a) return cudaSuccess;
   DeviceShape& sh = shape_for_current_device();
   if (dtype == 0) {
     const unsigned grid = grid_for(b - a, 4, sh.sms, sh.k2_f32);
     unpack_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<const float*>(recv),
                                                    static_cast<float*>(out), runs, nruns, a, b,
-                                                   (float)inv);
+                                                   (float)inv, mean);
   } else {
     const unsigned grid = grid_for(b - a, 2, sh.sms, sh.k2_f64);
     unpack_kernel<double><<<grid, kThreads, 0, s>>>(static_cast<const double*>(recv),
                                                     static_cast<double*>(out), runs, nruns, a, b,
-                                                    inv);
+                                                    inv, mean);
   }
   return cudaGetLastError();
 }

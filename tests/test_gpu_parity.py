@@ -1,0 +1,307 @@
+"""GPU parity of the sm_100a path against the oracle and the reference.
+
+Bars (BASELINE.json north_star):
+  * shard boundaries, selection masks, K: bit-exact (test_planner.py);
+  * fp64 instantiation of K1/K2: bit-exact against the REFERENCE's own
+    covap_compress / covap_decompress / allreduce_mean (golden fixtures made
+    by oracle/_ref, and the live library when present);
+  * fp32 path: residuals, payload and synchronised gradients bit-exact against
+    the fp32 restatement at P = 1 (FMA contraction controlled by
+    __fmul_rn/__fadd_rn in the kernel and -ffp-contract=off in the oracle);
+  * at full BASELINE sizes: exact integer conservation and K-window coverage.
+Every call goes through the C-ABI (libcovap_b200.so) via the Python mirror.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda", 0)
+
+
+def manifest():
+    with open(os.path.join(GOLDEN, "manifest.json")) as f:
+        return json.load(f)
+
+
+def mk_model(c, sizes, cap):
+    return c.ModelSpec([c.LayerSpec(f"l{i}", int(n)) for i, n in enumerate(sizes)], cap)
+
+
+def dev_gen(c, key, n, kind, dtype):
+    t = torch.empty(n, dtype=dtype, device=DEV)
+    c.generate(t, key, kind)
+    return t
+
+
+def payload_of(plan, send, step):
+    """Concatenate the selected tensors out of the (gapped) send buffer."""
+    parts = []
+    for t in plan.selection(step):
+        ts = plan.tensors[t]
+        br = plan.bucket_range(step, ts.bucket)
+        off = br.send_offset + (ts.begin - br.sel_begin)
+        parts.append(send[off:off + ts.numel()])
+    if not parts:
+        return np.zeros(0, send.dtype)
+    return np.concatenate(parts)
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+# ------------------------------------------------------------------ K0
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_generator_bit_identical_to_host_twin(covap, orc, dtype, kind):
+    npd = np.float32 if dtype == torch.float32 else np.float64
+    for n in (1, 3, 5, 1000, 1 << 20, 12345677):
+        key = orc.stream_key(7, 3, n)
+        assert covap.stream_key(7, 3, n) == key
+        d = dev_gen(covap, key, n, kind, dtype).cpu().numpy()
+        assert np.array_equal(bits(d), bits(orc.generate(key, n, kind, 0, npd)))
+
+
+# ------------------------------------------------------------------ fp64 == reference
+
+@pytest.mark.parametrize("case", manifest()["compress"], ids=lambda c: c["name"])
+def test_fp64_kernels_bit_exact_vs_reference_fixtures(covap, orc, case):
+    fx = np.load(os.path.join(GOLDEN, f"compress_{case['name']}.npz"))
+    plan = covap.BucketPlan(mk_model(covap, case["sizes"], case["cap"]), interval=case["K"],
+                            rule=case["rule"])
+    assert [[t.bucket, t.begin, t.end] for t in plan.tensors] == fx["tensors"].tolist()
+    en, init, asc, rng = case["ef"]
+    st = covap.CompressorState(plan, torch.float64, 0, covap.EfSchedule(bool(en), init, asc, rng))
+    d = plan.total_numel()
+    out = torch.empty(d, dtype=torch.float64, device=DEV)
+    for s in range(case["steps"]):
+        g = dev_gen(covap, orc.stream_key(case["seed"], 0, s), d, case["kind"], torch.float64)
+        upd = covap.covap_compress(g, st)
+        assert upd.selected == fx[f"selected_{s}"].tolist() and upd.step == s
+        covap.covap_decompress(upd, out)
+        torch.cuda.synchronize()
+        send = st.send.cpu().numpy()
+        assert np.array_equal(bits(payload_of(plan, send, s)), bits(fx[f"payload_{s}"]))
+        assert np.array_equal(bits(st.residuals.cpu().numpy()), bits(fx[f"residual_{s}"]))
+        assert np.array_equal(bits(out.cpu().numpy()), bits(fx[f"dense_{s}"]))
+    assert st.num_steps == case["steps"]
+
+
+@pytest.mark.parametrize("case", manifest()["session"], ids=lambda c: c["name"])
+def test_fp64_sync_steps_bit_exact_vs_reference(covap, orc, case):
+    """The reference's whole P-worker step (trainer.cpp:365-386) vs P device
+    states on one GPU: K1 per worker, a fixed-order device sum of the packed
+    send buffers (the allreduce, rank order as trainer.cpp:41-43), K2 x 1/P."""
+    fx = np.load(os.path.join(GOLDEN, f"session_{case['name']}.npz"))
+    plan = covap.BucketPlan(mk_model(covap, case["sizes"], case["cap"]), interval=case["K"],
+                            rule=case["rule"])
+    en, init, asc, rng = case["ef"]
+    P = case["P"]
+    states = [covap.CompressorState(plan, torch.float64, 0,
+                                    covap.EfSchedule(bool(en), init, asc, rng)) for _ in range(P)]
+    d = plan.total_numel()
+    out = torch.empty(d, dtype=torch.float64, device=DEV)
+    for s in range(case["steps"]):
+        for w in range(P):
+            g = dev_gen(covap, orc.stream_key(case["seed"], w, s), d, case["kind"], torch.float64)
+            states[w].filter_pack(g)
+        total = torch.zeros_like(states[0].send)
+        for w in range(P):
+            total += states[w].send  # rank order 0..P-1 (trainer.cpp:41-43)
+        states[0].unpack(out, 1.0 / P, recv=total)
+        for w in range(P):
+            states[w].step_end()
+        torch.cuda.synchronize()
+        # (((0 + v0) + v1) + ...) * 1/P in rank order: bit-exact for every P
+        assert np.array_equal(bits(out.cpu().numpy()), bits(fx[f"update_{s}"]))
+        assert np.array_equal(bits(states[0].residuals.cpu().numpy()), bits(fx[f"residual0_{s}"]))
+
+
+def test_fp64_live_reference_random_layouts(covap, orc, ref):
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        n = int(rng.integers(1, 14))
+        sizes = [int(x) for x in rng.integers(1, 30000, n)]
+        cap = 4 * int(rng.integers(100, 40000))
+        K = int(rng.integers(1, 9))
+        rb, _, rts = ref.plan(sizes, cap, K)
+        plan = covap.BucketPlan(mk_model(covap, sizes, cap), interval=K)
+        assert [[t.bucket, t.begin, t.end] for t in plan.tensors] == [list(t) for t in rts]
+        numels = [t[2] - t[1] for t in rts]
+        d = sum(numels)
+        st = covap.CompressorState(plan, torch.float64, 0, covap.EfSchedule(True, 0.3, 2, 0.2))
+        r_ref = np.zeros(d)
+        ns = 0
+        out = torch.empty(d, dtype=torch.float64, device=DEV)
+        for s in range(2 * K + 1):
+            key = orc.stream_key(100 + trial, 0, s)
+            g = dev_gen(covap, key, d, 0, torch.float64)
+            p_ref, sel, ns = ref.compress(g.cpu().numpy(), numels, r_ref, ns, K, 0, (1, 0.3, 2, 0.2))
+            upd = covap.covap_compress(g, st)
+            covap.covap_decompress(upd, out)
+            torch.cuda.synchronize()
+            assert upd.selected == sel
+            assert np.array_equal(payload_of(plan, st.send.cpu().numpy(), s), p_ref)
+            assert np.array_equal(st.residuals.cpu().numpy(), r_ref)
+            assert np.array_equal(out.cpu().numpy(), ref.decompress(p_ref, sel, numels))
+
+
+# ------------------------------------------------------------------ fp32 == restatement
+
+F32_CASES = [("resnet50", 4, 0, (1, 0.3, 100, 0.1), 6), ("resnet50", 8, 0, (1, 0.4, 1, 0.2), 9),
+             ("vgg16", 4, 0, (1, 0.3, 1, 0.25), 5), ("vgg16", 3, 1, (0, 0.3, 100, 0.1), 4),
+             ("tablev", 19, 0, (1, 0.5, 2, 0.1), 3), ("bert_large", 4, 0, (1, 0.3, 1, 0.3), 2),
+             ("resnet50", 1, 0, (1, 0.3, 100, 0.1), 2)]
+
+
+@pytest.mark.parametrize("name,K,rule,ef,steps", F32_CASES,
+                         ids=[f"{c[0]}-K{c[1]}-r{c[2]}" for c in F32_CASES])
+def test_fp32_full_layouts_bit_exact_vs_oracle(covap, orc, name, K, rule, ef, steps):
+    """Full BASELINE layouts, fp32: send payload, residual arena and the
+    synchronised gradient (P = 1: (0 + x) * 1) bit-exact against the fp32
+    restatement, step after step (residual carried)."""
+    m = covap.load_layout(name)
+    plan = covap.plan_for(m, covap.CovapConfig(interval=K, rule=rule))
+    tensors = [(t.bucket, t.begin, t.end) for t in plan.tensors]
+    _, ots = orc.plan([l.param_count for l in m.layers], m.bucket_cap_bytes, K)
+    assert [tuple(t) for t in ots] == tensors
+    st = covap.CompressorState(plan, torch.float32, 0, covap.EfSchedule(bool(ef[0]), *ef[1:]))
+    sync = covap.CovapSync(plan, None, torch.float32, 0, covap.EfSchedule(bool(ef[0]), *ef[1:]))
+    d = plan.total_numel()
+    r = np.zeros(d, np.float32)
+    out = torch.empty(d, dtype=torch.float32, device=DEV)
+    out2 = torch.empty(d, dtype=torch.float32, device=DEV)
+    for s in range(steps):
+        key = orc.stream_key(5, 0, s)
+        g = dev_gen(covap, key, d, 0, torch.float32)
+        upd = covap.covap_compress(g, st)
+        covap.covap_decompress(upd, out)
+        sync.sync(g, out2)
+        keep = orc.select(s, K, len(tensors), rule)
+        coeff = np.float32(orc.ef_coefficient(s, *ef[1:]))
+        p = orc.compress(orc.generate(key, d, 0, 0, np.float32), r, tensors, keep, ef[0], coeff)
+        dense = orc.decompress(orc.allreduce_mean(p[None, :]) if len(p) else p, tensors, keep, d,
+                               np.float32)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(payload_of(plan, st.send.cpu().numpy(), s)), bits(p))
+        assert np.array_equal(bits(st.residuals.cpu().numpy()), bits(r))
+        assert np.array_equal(bits(out.cpu().numpy()), bits(orc.decompress(p, tensors, keep, d, np.float32)))
+        assert np.array_equal(bits(out2.cpu().numpy()), bits(dense))
+        assert np.array_equal(bits(sync.state.residuals.cpu().numpy()), bits(r))
+
+
+def test_overlapped_schedule_equals_standalone(covap):
+    """bucket_ready()/finish() on the side stream gives exactly sync()'s
+    results, and the dense path gives allreduce_mean at P = 1."""
+    for name, K in (("resnet50", 4), ("vgg16", 4), ("bert_large", 2)):
+        plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+        a = covap.CovapSync(plan, None, torch.float32, 0)
+        b = covap.CovapSync(plan, None, torch.float32, 0)
+        d = plan.total_numel()
+        oa = torch.empty(d, device=DEV)
+        ob = torch.empty(d, device=DEV)
+        for s in range(K + 1):
+            g = torch.empty(d, device=DEV)
+            covap.generate(g, covap.stream_key(9, 0, s))
+            a.sync(g, oa)
+            for bk in range(len(plan.buckets)):
+                b.bucket_ready(bk, g, ob)
+            b.finish()
+            torch.cuda.synchronize()
+            assert torch.equal(oa, ob)
+            assert torch.equal(a.state.residuals, b.state.residuals)
+        durs = b.last_comm_ms()
+        assert len(durs) == len(plan.buckets)
+        # dense baseline: out = (0 + g) * 1 at P = 1, in place
+        g = torch.randn(d, device=DEV)
+        g[::7] = -0.0
+        dense = g.clone()
+        for bk in range(len(plan.buckets)):
+            b.dense_bucket_ready(bk, dense, dense)
+        b.finish()
+        torch.cuda.synchronize()
+        assert torch.equal(dense, g + 0.0)
+        assert not torch.signbit(dense[::7]).any()
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_edge_cases_small_and_ragged(covap, orc):
+    """Unaligned bucket boundaries, 1-element layers, K > tensor count (empty
+    phases: no payload, residual still written, zero output), signed zeros."""
+    for sizes, cap, K in (([1], 4, 1), ([1, 2, 3], 4, 4), ([5, 1, 7, 3, 9], 12, 3),
+                          ([33, 1, 1, 65, 127, 4097], 132, 16), ([300, 300, 300], 1200, 8),
+                          ([4096, 3, 5, 4093], 16388, 2)):
+        plan = covap.BucketPlan(mk_model(covap, sizes, cap), interval=K)
+        tensors = [(t.bucket, t.begin, t.end) for t in plan.tensors]
+        _, ots = orc.plan(sizes, cap, K)
+        assert [tuple(t) for t in ots] == tensors
+        st = covap.CompressorState(plan, torch.float32, 0, covap.EfSchedule(True, 0.5, 1, 0.25))
+        d = plan.total_numel()
+        r = np.zeros(d, np.float32)
+        out = torch.empty(d, device=DEV)
+        for s in range(2 * K + 1):
+            key = orc.stream_key(31, 0, s)
+            gh = orc.generate(key, d, 0, 0, np.float32)
+            gh[::3] = -0.0
+            g = torch.from_numpy(gh.copy()).to(DEV)
+            upd = covap.covap_compress(g, st)
+            covap.covap_decompress(upd, out)
+            keep = orc.select(s, K, len(tensors))
+            p = orc.compress(gh, r, tensors, keep, 1, np.float32(orc.ef_coefficient(s, 0.5, 1, 0.25)))
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(payload_of(plan, st.send.cpu().numpy(), s)), bits(p))
+            assert np.array_equal(bits(st.residuals.cpu().numpy()), bits(r))
+            assert np.array_equal(bits(out.cpu().numpy()),
+                                  bits(orc.decompress(p, tensors, keep, d, np.float32)))
+
+
+def test_errors_on_device_calls(covap):
+    plan = covap.plan_for(covap.load_layout("resnet50"), covap.CovapConfig(interval=4))
+    st = covap.CompressorState(plan, torch.float32, 0)
+    d = plan.total_numel()
+    with pytest.raises(covap.InvalidState):
+        covap.covap_compress(torch.zeros(d - 1, device=DEV), st)
+    with pytest.raises(covap.InvalidInput):
+        covap.covap_compress(torch.zeros(d, dtype=torch.float64, device=DEV), st)
+    big = torch.zeros(d + 1, device=DEV)
+    with pytest.raises(covap.InvalidInput):  # 4-byte offset: not 16-byte aligned
+        st.filter_pack(big[1:])
+    with pytest.raises(covap.InvalidInput):
+        st.filter_pack(big[:d], b0=3, b1=2)
+    with pytest.raises(covap.InvalidState):
+        covap.covap_compress(big[:d], st, covap.CovapConfig(interval=2))
+
+
+# ------------------------------------------------------------------ full-size properties
+
+@pytest.mark.parametrize("name,K", [("bert_large", 4), ("vgg16", 8), ("resnet50", 16)])
+def test_full_size_integer_conservation(covap, name, K):
+    """Size-independent property at BASELINE sizes: with integer gradients and
+    coeff = 1 (test_compress.cpp:223-245, acceptance.cpp:273-327) the sum of
+    transmitted updates plus the residual store equals the sum of inputs
+    exactly (every element is transmitted once per K-window, so after K steps
+    the residual holds only what was accumulated since its tensor was sent)."""
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    sync = covap.CovapSync(plan, None, torch.float32, 0, covap.EfSchedule(True, 1.0, 1, 0.0))
+    d = plan.total_numel()
+    inp = torch.zeros(d, device=DEV)
+    sent = torch.zeros(d, device=DEV)
+    g = torch.empty(d, device=DEV)
+    out = torch.empty(d, device=DEV)
+    for s in range(K):
+        covap.generate(g, covap.stream_key(1, 0, s), 1)
+        inp += g
+        sync.sync(g, out)
+        sent += out
+    torch.cuda.synchronize()
+    assert torch.equal(sent + sync.state.residuals, inp)
