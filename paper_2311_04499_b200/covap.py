@@ -38,7 +38,7 @@ from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
 from . import _lib as L
-from .errors import InvalidInput, NoDeviceError
+from .errors import InvalidInput, InvalidState, NoDeviceError  # noqa: F401
 
 _LAYOUT_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "layouts")
 DEFAULT_BUCKET_CAP_BYTES = 25 * 1024 * 1024  # model.hpp:26
