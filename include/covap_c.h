@@ -158,20 +158,28 @@ covap_status covap_filter_pack(covap_state* state, const void* grad, void* send,
  * out may alias the gradient passed to K1. */
 covap_status covap_unpack(covap_state* state, const void* recv, void* out, double scale, int mean,
                           size_t b0, size_t b1, void* stream);
+/* K1F: K1 and K2 fused for a single rank over buckets [b0, b1): selected ->
+ * out = (0 + c) * scale and r = 0, unselected -> r = c and out = 0.  Equal to
+ * covap_filter_pack + covap_unpack(mean = 1) when the allreduce is the
+ * identity (P = 1); 16N instead of 24N bytes at K = 1.  out may alias grad. */
+covap_status covap_filter_unpack(covap_state* state, const void* grad, void* out, double scale,
+                                 size_t b0, size_t b1, void* stream);
 /* ++num_steps (compress.cpp:83). */
 covap_status covap_step_end(covap_state* state);
 
 /* The standalone sync step, trainer.cpp:365-386 for this rank: K1 over all
- * buckets -> ncclAllReduce(sum) of the packed send buffer (skipped when comm
- * is NULL or has one rank, or nothing is selected) -> K2 with 1/P -> ++step.
- * All on `stream`. */
+ * buckets -> ncclAllReduce(sum) of the packed send buffer (skipped when
+ * nothing is selected) -> K2 with 1/P -> ++step, all on `stream`.  With one
+ * rank (comm NULL or of size 1) the allreduce is the identity and the step is
+ * the single fused pass K1F. */
 covap_status covap_sync_step(covap_state* state, covap_comm* comm, const void* grad, void* out,
                              void* stream);
 
 /* Overlapped schedule (the DDP-hook shape): bucket b's gradient is ready on
  * `stream` -> K1(b) on `stream`, event -> on the state's comm stream:
- * allreduce of b's selected range, K2(b).  covap_step_finish makes `stream`
- * wait for the comm stream and advances the step. */
+ * allreduce of b's selected range, K2(b); with one rank K1F(b) on `stream`.
+ * covap_step_finish makes `stream` wait for the comm stream and advances the
+ * step. */
 covap_status covap_bucket_ready(covap_state* state, covap_comm* comm, size_t bucket,
                                 const void* grad, void* out, void* stream);
 covap_status covap_step_finish(covap_state* state, void* stream);

@@ -72,6 +72,7 @@ _SIGS = {
     "covap_state_reset": (None, [vp, vp]),
     "covap_filter_pack": (None, [vp, vp, vp, sz, sz, vp]),
     "covap_unpack": (None, [vp, vp, vp, f64, i32, sz, sz, vp]),
+    "covap_filter_unpack": (None, [vp, vp, vp, f64, sz, sz, vp]),
     "covap_step_end": (None, [vp]),
     "covap_sync_step": (None, [vp, vp, vp, vp, vp]),
     "covap_bucket_ready": (None, [vp, vp, sz, vp, vp, vp]),

@@ -414,6 +414,15 @@ class CompressorState:
                              float(scale), 1 if mean else 0, int(b0), int(b1),
                              _stream_ptr(stream, self.device))
 
+    def filter_unpack(self, grad, out, scale: float = 1.0, b0: int = 0,
+                      b1: Optional[int] = None, stream=None):
+        """K1F: K1 + K2 fused for a single rank (the allreduce is the identity)."""
+        self._check(grad)
+        self._check(out)
+        b1 = len(self.plan.buckets) if b1 is None else b1
+        L.lib().covap_filter_unpack(self._h, _ptr(grad), _ptr(out), float(scale), int(b0), int(b1),
+                                    _stream_ptr(stream, self.device))
+
     def step_end(self):
         L.lib().covap_step_end(self._h)
 
@@ -619,3 +628,57 @@ def generate(out, key: int, kind: int = 0, begin: int = 0, stream=None):
 def spin(us: float, blocks: int = 1, stream=None, device=None):
     """K3: occupy `blocks` CTAs for `us` microseconds (backward emulator)."""
     L.lib().covap_spin(float(us), int(blocks), _stream_ptr(stream, device))
+
+
+# ------------------------------------------------------------ CCR controller
+
+class NcclExchange:
+    """Rank-min of per-collective durations + rank 0's compute time over the
+    native NCCL communicator (covap_comm_profile_exchange)."""
+
+    def __init__(self, comm: Optional[Communicator]):
+        self.comm = comm
+
+    def __call__(self, durations, comp_ms):
+        if self.comm is None:
+            return list(durations), float(comp_ms)
+        return self.comm.profile_exchange(durations, comp_ms)
+
+
+class TorchDistExchange:
+    """The same exchange over an initialised torch.distributed group (any
+    backend; CPU tensors for gloo)."""
+
+    def __call__(self, durations, comp_ms):
+        torch = _torch()
+        import torch.distributed as dist
+        dev = torch.device("cuda", torch.cuda.current_device()) \
+            if dist.get_backend() == "nccl" else torch.device("cpu")
+        d = torch.tensor(list(durations), dtype=torch.float64, device=dev)
+        c = torch.tensor([float(comp_ms)], dtype=torch.float64, device=dev)
+        if d.numel():
+            dist.all_reduce(d, op=dist.ReduceOp.MIN)
+        dist.broadcast(c, src=0)
+        return d.cpu().tolist(), float(c.item())
+
+
+class CcrController:
+    """CCR-driven choice of K (PAPER §IV-B; perf.cpp:40-53, sim.cpp:164-216).
+
+    One dense iteration is profiled.  Each rank measures, per collective, the
+    time from its own arrival to the collective's completion; the collective
+    completes at the same instant everywhere, so the rank-minimum of those
+    durations is ``end - last arrival`` — the reference's rendezvous-aligned
+    communication time (sim.cpp:202-203) — without a global clock.  The
+    compute time is worker 0's (sim.cpp:208-211).  Every rank then derives the
+    same K = max(1, ceil(comm / comp))."""
+
+    def __init__(self, exchange):
+        self.exchange = exchange
+
+    def decide(self, own_comm_ms: Sequence[float], own_comp_ms: float) -> ProfileResult:
+        durs = [max(0.0, float(x)) for x in own_comm_ms]
+        aligned, comp0 = self.exchange(durs, own_comp_ms)
+        comm = float(sum(aligned))
+        c = ccr(comm, comp0)
+        return ProfileResult(c, comp0, comm, list(durs), choose_interval(c))

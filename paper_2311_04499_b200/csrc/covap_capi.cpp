@@ -173,6 +173,14 @@ void k1_range(covap_state* s, const void* grad, void* send, uint64_t a, uint64_t
                                 s->ef.enabled, st));
 }
 
+void k1f_range(covap_state* s, const void* grad, void* out, double inv, uint64_t a, uint64_t b,
+               cudaStream_t st) {
+  const size_t ph = s->num_steps % s->plan.interval;
+  const int nr = static_cast<int>(s->plan.phases[ph].runs.size());
+  CK(covapb::launch_filter_unpack(s->dtype, grad, s->residual, out, s->d_runs + s->phase_off[ph],
+                                  nr, a, b, coeff_of(s), s->ef.enabled, inv, st));
+}
+
 void k2_range(covap_state* s, const void* recv, void* out, double inv, int mean, uint64_t a,
               uint64_t b, cudaStream_t st) {
   const size_t ph = s->num_steps % s->plan.interval;
@@ -494,6 +502,21 @@ covap_status covap_unpack(covap_state* s, const void* recv, void* out, double sc
   });
 }
 
+covap_status covap_filter_unpack(covap_state* s, const void* grad, void* out, double scale,
+                                 size_t b0, size_t b1, void* stream) {
+  return guarded([&] {
+    need(s && grad && out, "NULL argument");
+    need(b0 <= b1 && b1 <= s->plan.buckets.size(), "bucket range out of bounds");
+    need_aligned(grad, "grad");
+    need_aligned(out, "out");
+    if (b0 == b1) return;
+    DeviceGuard dg(s->device);
+    const uint64_t a = s->plan.buckets[b0].begin;
+    const uint64_t b = s->plan.buckets[b1 - 1].begin + s->plan.buckets[b1 - 1].numel;
+    k1f_range(s, grad, out, scale, a, b, as_stream(stream));
+  });
+}
+
 covap_status covap_step_end(covap_state* s) {
   return guarded([&] {
     need(s != nullptr, "NULL state");
@@ -512,12 +535,18 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
     cudaStream_t st = as_stream(stream);
     const uint64_t n = s->plan.total;
     const auto& ph = phase_of(s->plan, s->num_steps);
-    k1_range(s, grad, nullptr, 0, n, st);
     const int P = world(comm);
-    if (P > 1 && ph.send_elems > 0)
-      NK(ncclAllReduce(s->send, s->send, ph.send_elems, nccl_type(s->dtype), ncclSum, comm->nccl,
-                       st));
-    k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, 0, n, st);
+    if (P == 1) {
+      // One rank: the allreduce is the identity, so K1 and K2 fuse into one
+      // pass (K1F) that writes (0 + c) * 1 straight to the selected slots.
+      k1f_range(s, grad, out, 1.0, 0, n, st);
+    } else {
+      k1_range(s, grad, nullptr, 0, n, st);
+      if (ph.send_elems > 0)
+        NK(ncclAllReduce(s->send, s->send, ph.send_elems, nccl_type(s->dtype), ncclSum,
+                         comm->nccl, st));
+      k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, 0, n, st);
+    }
     ++s->num_steps;
   });
 }
@@ -534,10 +563,15 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
     const auto& bk = s->plan.buckets[bucket];
     const auto& sel = phase_of(s->plan, s->num_steps).per_bucket[bucket];
     const uint64_t a = bk.begin, b = bk.begin + bk.numel;
+    const int P = world(comm);
+    if (P == 1) {  // no exchange: the fused pass on the producing stream
+      k1f_range(s, grad, out, 1.0, a, b, st);
+      s->timed[bucket] = 0;
+      return;
+    }
     k1_range(s, grad, nullptr, a, b, st);
     CK(cudaEventRecord(s->ready[bucket], st));
     CK(cudaStreamWaitEvent(s->comm_stream, s->ready[bucket], 0));
-    const int P = world(comm);
     const uint64_t len = sel.sel_end - sel.sel_begin;
     s->timed[bucket] = len > 0 ? 1 : 0;
     CK(cudaEventRecord(s->arrive[bucket], s->comm_stream));

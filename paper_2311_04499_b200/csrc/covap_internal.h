@@ -25,6 +25,12 @@ constexpr uint64_t kSendAlign = 32;  // elements (128 B fp32, 256 B fp64)
 cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, const Run* runs,
                                int nruns, uint64_t a, uint64_t b, double coeff, int ef,
                                cudaStream_t s);
+// K1F (one rank, fused K1 + K2): selected -> out = (0 + c) * inv, r = 0;
+// unselected -> r = c, out = 0.  No send buffer: the allreduce over one rank
+// is the identity.
+cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, const Run* runs,
+                                 int nruns, uint64_t a, uint64_t b, double coeff, int ef,
+                                 double inv, cudaStream_t s);
 // K2: out = in-run ? f(recv[dst + e - begin]) : 0 for flat [a, b), with
 // f(x) = (0 + x) * inv when mean (allreduce_mean), x * inv otherwise.
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,

@@ -1,24 +1,35 @@
 // covap_kernels.cu — the sm_100a kernels of the COVAP sync path.
 //
-//   K1 filter_pack   compress.cpp:59-81   (EF add, round-robin select, pack, residual write-back)
-//   K2 unpack        compress.cpp:87-103 + trainer.cpp:41-45 (embed, sum-then-scale, zero fill)
-//   K0 generate      synthetic gradients (rng.hpp:12-21 splitmix64 stream, counter-based)
-//   K3 spin          backward emulator for the overlap schedule
+//   K1  filter_pack    compress.cpp:59-81 (EF add, round-robin select, pack,
+//                      residual write-back)
+//   K1F filter_unpack  K1 + K2 fused for one rank: the allreduce over one
+//                      rank is the identity (trainer.cpp:41-45 with P = 1),
+//                      so c goes straight to its flat slot of the output
+//   K2  unpack         compress.cpp:87-103 + trainer.cpp:41-45 (embed,
+//                      sum-then-scale, zero fill)
+//   K0  generate       synthetic gradients (rng.hpp:12-21 splitmix64 stream)
+//   K3  spin           backward emulator for the overlap schedule
 //
-// K1/K2 are HBM-streaming kernels (≈0.2 flop/byte): no tensor cores, no shared
-// memory staging (no reuse).  Design:
-//   * every CTA owns one contiguous, equal share of the 16-byte vectors of the
-//     launch range (balanced to one vector, so no wave tail), walking it in
-//     tiles of kThreads x kUnroll vectors; all kUnroll loads of a tile are
-//     issued before any use (8 x 16 B in flight per thread for K1);
-//   * loads are ld.global.cs (evict-first) 128-bit; stores st.global.cs;
-//   * selection is positional: the phase's run table (a handful of entries)
-//     is binary-searched once per CTA and walked forward per tile, so a tile
-//     is "all selected", "none selected" (vector fast paths) or "mixed"
-//     (per-element path, only at run boundaries);
-//   * arithmetic uses __fmul_rn/__fadd_rn (__dmul_rn/__dadd_rn) so nvcc can
-//     never contract g + coeff*r into an FMA: the multiply and the add round
-//     separately exactly as compress.cpp:64 does on x86-64.
+// K1/K1F/K2 are HBM-streaming passes (~0.2 flop/byte): no tensor cores.
+// They are persistent TMA-bulk pipelines (design measured with
+// scripts/kbench.cu on B200: 0.89-0.98 of the copy peak for K1's 2-read /
+// 2-write shape vs 0.72-0.77 for a chunked LDG/STG version):
+//   * one CTA per SM (144 KB smem) walks 16 KB tiles of the launch range in
+//     interleaved order (tile = blockIdx + k * gridDim): all SMs stream
+//     through neighbouring DRAM pages at any instant;
+//   * thread 0 keeps kStages tiles of g and r in flight with
+//     cp.async.bulk (global -> smem, mbarrier complete_tx); results are
+//     staged in smem and written back with cp.async.bulk (smem -> global);
+//     a persistent zero tile in smem feeds the bulk stores that write zeros
+//     (residual reset of selected shards, zero fill of unselected ones), so
+//     zero streams cost no instructions;
+//   * selection is positional: each tile binary-searches the phase's run
+//     table (a few entries, L1-resident) and is "none selected" or "all
+//     selected" (bulk path) or "mixed" (element path; only the tiles that
+//     straddle a shard boundary);
+//   * arithmetic uses __fmul_rn/__fadd_rn (__dmul_rn/__dadd_rn): nvcc can
+//     never contract g + coeff*r into an FMA, so the multiply and the add
+//     round separately exactly as compress.cpp:64 does on x86-64.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,30 +42,95 @@ namespace covapb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
-
-template <typename T>
-struct V16;
-template <>
-struct V16<float> {
-  using type = float4;
-  static constexpr int n = 4;
-};
-template <>
-struct V16<double> {
-  using type = double2;
-  static constexpr int n = 2;
-};
+constexpr int kStages = 3;
+constexpr uint32_t kTileBytes = 16384;
+// K1/K1F: kStages x (g, r) input tiles + 2 staging tiles + 1 zero tile.
+constexpr uint32_t kSmemK1 = (2 * kStages + 3) * kTileBytes;
+// K2: kStagesK2 recv tiles + 2 staging tiles + 1 zero tile.
+constexpr int kStagesK2 = 4;
+constexpr uint32_t kSmemK2 = (kStagesK2 + 3) * kTileBytes;
 
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 
-template <typename V, typename T>
-__device__ __forceinline__ T& lane(V& v, int k) {
-  return reinterpret_cast<T*>(&v)[k];
+// allreduce_mean's (0.0 + sum) * (1/P) (trainer.cpp:41-45) when mean — the
+// leading +0 turns a -0 sum into +0 exactly as the reference does — else the
+// plain embedding of covap_decompress (compress.cpp:100) times `inv`.
+template <typename T>
+__device__ __forceinline__ T scale_of(T x, T inv, int mean) {
+  return mul_rn(mean ? add_rn(T(0), x) : x, inv);
 }
+
+// 16-byte vector of T and lane access.
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using type = float4;
+};
+template <>
+struct Vec16<double> {
+  using type = double2;
+};
+__device__ __forceinline__ float& lane(float4& v, int q) { return reinterpret_cast<float*>(&v)[q]; }
+__device__ __forceinline__ float lane(const float4& v, int q) {
+  return reinterpret_cast<const float*>(&v)[q];
+}
+__device__ __forceinline__ double& lane(double2& v, int q) { return reinterpret_cast<double*>(&v)[q]; }
+__device__ __forceinline__ double lane(const double2& v, int q) {
+  return reinterpret_cast<const double*>(&v)[q];
+}
+
+// ------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "COVAP_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      " @!p bra COVAP_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Wait until at most N committed bulk groups still read shared memory.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// Wait until every committed bulk group has fully completed (writes visible).
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------ selection
 
 // Smallest j with runs[j].end > x (runs sorted, disjoint).
 __device__ __forceinline__ int first_run_after(const Run* __restrict__ runs, int n, uint64_t x) {
@@ -69,218 +145,284 @@ __device__ __forceinline__ int first_run_after(const Run* __restrict__ runs, int
   return lo;
 }
 
-// The selected-run index holding element e, or -1; j is a forward cursor.
-__device__ __forceinline__ int run_of(const Run* __restrict__ runs, int n, int j, uint64_t e) {
+enum TileClass { kNone = 0, kFull = 1, kMixed = 2 };
+
+struct TileSel {
+  int cls;
+  int j;        // first run ending after the tile start
+  uint64_t rb;  // run begin / dst (kFull)
+  uint64_t rd;
+};
+
+__device__ __forceinline__ TileSel classify(const Run* __restrict__ runs, int n, uint64_t e0,
+                                            uint64_t e1) {
+  TileSel s;
+  s.j = first_run_after(runs, n, e0);
+  s.rb = s.rd = 0;
+  if (s.j >= n || runs[s.j].begin >= e1) {
+    s.cls = kNone;
+  } else if (runs[s.j].begin <= e0 && e1 <= runs[s.j].end) {
+    s.cls = kFull;
+    s.rb = runs[s.j].begin;
+    s.rd = runs[s.j].dst;
+  } else {
+    s.cls = kMixed;
+  }
+  return s;
+}
+
+// Selected run holding e (cursor j moves forward), or -1.
+__device__ __forceinline__ int run_at(const Run* __restrict__ runs, int n, int& j, uint64_t e) {
   while (j < n && runs[j].end <= e) ++j;
   return (j < n && runs[j].begin <= e) ? j : -1;
 }
 
-// ---------------------------------------------------------------- K1
+// ------------------------------------------------------------ kernel args
 
 template <typename T>
-__device__ __forceinline__ void filter_scalar(const T* __restrict__ g, T* __restrict__ r,
-                                              T* __restrict__ send, const Run* __restrict__ runs,
-                                              int nruns, uint64_t e, T coeff, int ef) {
-  T c = g[e];
-  if (ef) c = add_rn(c, mul_rn(coeff, r[e]));
-  const int j = run_of(runs, nruns, first_run_after(runs, nruns, e), e);
-  if (j >= 0) {
-    send[runs[j].dst + (e - runs[j].begin)] = c;
-    r[e] = T(0);
+struct Args {
+  const T* g;      // K1/K1F: fresh gradient
+  T* r;            // K1/K1F: residual store (in/out)
+  T* send;         // K1: packed send buffer
+  T* out;          // K1F/K2: synchronised gradient (flat layout)
+  const T* recv;   // K2: allreduced send buffer
+  const Run* runs;
+  int nruns;
+  uint64_t a, b;   // flat element range of the launch
+  T coeff;         // EF coefficient (K1/K1F)
+  int ef;          // EF enabled: read r
+  T inv;           // K1F/K2 scale (1/P)
+  int mean;        // K2: allreduce_mean semantics
+};
+
+// Element path (scalar head/tail and mixed tiles).
+template <typename T, int OP>
+__device__ __forceinline__ void element(const Args<T>& A, int& j, uint64_t e, T gv, T rv) {
+  const int k = run_at(A.runs, A.nruns, j, e);
+  if (OP == 2) {
+    A.out[e] = k >= 0 ? scale_of(A.recv[A.runs[k].dst + (e - A.runs[k].begin)], A.inv, A.mean)
+                      : T(0);
+    return;
+  }
+  const T c = A.ef ? add_rn(gv, mul_rn(A.coeff, rv)) : gv;
+  if (k >= 0) {
+    if (OP == 0)
+      A.send[A.runs[k].dst + (e - A.runs[k].begin)] = c;
+    else
+      A.out[e] = scale_of(c, A.inv, 1);
+    A.r[e] = T(0);
   } else {
-    r[e] = c;
+    A.r[e] = c;
+    if (OP == 1) A.out[e] = T(0);
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads)
-    filter_pack_kernel(const T* __restrict__ g, T* __restrict__ r, T* __restrict__ send,
-                       const Run* __restrict__ runs, int nruns, uint64_t a, uint64_t b, T coeff,
-                       int ef) {
-  using V = typename V16<T>::type;
-  constexpr int W = V16<T>::n;
-  const uint64_t A = (a + W - 1) / W * W;
-  uint64_t B;
-  if (A >= b) {  // the whole range sits inside one vector: scalar only
-    if (blockIdx.x == 0)
-      for (uint64_t e = a + threadIdx.x; e < b; e += blockDim.x)
-        filter_scalar(g, r, send, runs, nruns, e, coeff, ef);
+// Elements [a, a16) and [b16, b) that do not fill a 16-byte vector.
+template <typename T, int OP>
+__device__ void edges(const Args<T>& A, uint64_t a16, uint64_t b16) {
+  for (uint64_t e = A.a + threadIdx.x; e < a16; e += blockDim.x) {
+    int j = first_run_after(A.runs, A.nruns, e);
+    element<T, OP>(A, j, e, OP == 2 ? T(0) : A.g[e], (OP != 2 && A.ef) ? A.r[e] : T(0));
+  }
+  for (uint64_t e = b16 + threadIdx.x; e < A.b; e += blockDim.x) {
+    int j = first_run_after(A.runs, A.nruns, e);
+    element<T, OP>(A, j, e, OP == 2 ? T(0) : A.g[e], (OP != 2 && A.ef) ? A.r[e] : T(0));
+  }
+}
+
+// ------------------------------------------------------------ K1 / K1F
+
+// OP 0 = K1 filter_pack (selected -> send), OP 1 = K1F (selected -> out).
+template <typename T, int OP>
+__global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
+  constexpr uint32_t TE = kTileBytes / sizeof(T);  // elements per tile
+  using V = typename Vec16<T>::type;
+  constexpr uint32_t W = 16 / sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* gin = reinterpret_cast<T*>(smem);  // kStages tiles
+  T* rin = gin + kStages * TE;          // kStages tiles
+  T* stage = rin + kStages * TE;        // 2 tiles
+  T* zero = stage + 2 * TE;             // 1 tile
+  __shared__ __align__(8) uint64_t bar[kStages];
+
+  const uint64_t a16 = (A.a + 16 / sizeof(T) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
+  const uint64_t b16 = A.b / (16 / sizeof(T)) * (16 / sizeof(T));
+  if (a16 >= b16) {  // nothing vector-sized: element path only
+    if (blockIdx.x == 0) {
+      for (uint64_t e = A.a + threadIdx.x; e < A.b; e += blockDim.x) {
+        int j = first_run_after(A.runs, A.nruns, e);
+        element<T, OP>(A, j, e, A.g[e], A.ef ? A.r[e] : T(0));
+      }
+    }
     return;
   }
-  B = b / W * W;
-  if (blockIdx.x == 0) {  // unaligned head [a, A) and tail [B, b)
-    if (threadIdx.x < A - a) filter_scalar(g, r, send, runs, nruns, a + threadIdx.x, coeff, ef);
-    if (threadIdx.x < b - B) filter_scalar(g, r, send, runs, nruns, B + threadIdx.x, coeff, ef);
+  if (blockIdx.x == 0) edges<T, OP>(A, a16, b16);
+
+  const uint64_t ntiles = (b16 - a16 + TE - 1) / TE;
+  const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) mbar_init(&bar[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint64_t nvec = (B - A) / W;
-  const uint64_t v0 = nvec * blockIdx.x / gridDim.x;
-  const uint64_t v1 = nvec * (blockIdx.x + 1) / gridDim.x;
-  if (v0 >= v1) return;
-  const V* __restrict__ gv = reinterpret_cast<const V*>(g + A);
-  V* __restrict__ rv = reinterpret_cast<V*>(r + A);
+  fence_async_smem();  // zero tile visible to the bulk-copy (async) proxy
+  __syncthreads();
 
-  int j = first_run_after(runs, nruns, A + v0 * W);
-  constexpr uint64_t kTile = (uint64_t)kThreads * kUnroll;
-  for (uint64_t t = v0; t < v1; t += kTile) {
-    const uint64_t te0 = A + t * W;
-    const uint64_t te1 = A + min(t + kTile, v1) * W;
-    while (j < nruns && runs[j].end <= te0) ++j;
-    uint64_t rb = 0, re = 0, rd = 0;
-    if (j < nruns) {
-      rb = runs[j].begin;
-      re = runs[j].end;
-      rd = runs[j].dst;
-    }
-    const bool none = (j >= nruns) || rb >= te1;
-    const bool full = !none && rb <= te0 && te1 <= re;
+  auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * TE; };
+  auto issue = [&](uint64_t k) {  // thread 0 only
+    const int s = static_cast<int>(k % kStages);
+    const uint64_t e0 = tile_lo(k);
+    const uint32_t bytes = static_cast<uint32_t>((min(e0 + TE, b16) - e0) * sizeof(T));
+    mbar_arrive_tx(&bar[s], A.ef ? 2 * bytes : bytes);
+    bulk_load(gin + s * TE, A.g + e0, bytes, &bar[s]);
+    if (A.ef) bulk_load(rin + s * TE, A.r + e0, bytes, &bar[s]);
+  };
+  if (threadIdx.x == 0)
+    for (uint64_t k = 0; k < my && k < kStages; ++k) issue(k);
 
-    V x[kUnroll], y[kUnroll];
+  for (uint64_t k = 0; k < my; ++k) {
+    const int s = static_cast<int>(k % kStages);
+    const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
+    const uint32_t n = static_cast<uint32_t>(e1 - e0);
+    T* st = stage + (k & 1) * TE;
+    const TileSel sel = classify(A.runs, A.nruns, e0, e1);
+    mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
+    if (threadIdx.x == 0) bulk_wait_read<1>();  // staging tile (k & 1) free again
+    __syncthreads();
+
+    const T* gs = gin + s * TE;
+    const T* rs = rin + s * TE;
+    if (sel.cls != kMixed) {
+      // 16-byte vectors: a warp touches 512 contiguous bytes, no bank conflicts
+      const bool full = sel.cls == kFull;
+      const V* gv = reinterpret_cast<const V*>(gs);
+      const V* rv = reinterpret_cast<const V*>(rs);
+      V* sv = reinterpret_cast<V*>(st);
+      for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
+        V x = gv[v];
+        if (A.ef) {
+          const V y = rv[v];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t v = t + (uint64_t)u * kThreads + threadIdx.x;
-      if (v < v1) {
-        x[u] = __ldcs(gv + v);
-        if (ef) y[u] = __ldcs(rv + v);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t v = t + (uint64_t)u * kThreads + threadIdx.x;
-      if (v >= v1) continue;
-      V c = x[u];
-      if (ef) {
-#pragma unroll
-        for (int k = 0; k < W; ++k)
-          lane<V, T>(c, k) = add_rn(lane<V, T>(x[u], k), mul_rn(coeff, lane<V, T>(y[u], k)));
-      }
-      const uint64_t e = A + v * W;
-      if (full) {
-        __stcs(reinterpret_cast<V*>(send + rd + (e - rb)), c);
-        V z;
-#pragma unroll
-        for (int k = 0; k < W; ++k) lane<V, T>(z, k) = T(0);
-        __stcs(rv + v, z);
-      } else if (none) {
-        __stcs(rv + v, c);
-      } else {
-        int jj = j;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-          const uint64_t ee = e + k;
-          while (jj < nruns && runs[jj].end <= ee) ++jj;
-          if (jj < nruns && runs[jj].begin <= ee) {
-            send[runs[jj].dst + (ee - runs[jj].begin)] = lane<V, T>(c, k);
-            r[ee] = T(0);
-          } else {
-            r[ee] = lane<V, T>(c, k);
-          }
+          for (int q = 0; q < W; ++q) lane(x, q) = add_rn(lane(x, q), mul_rn(A.coeff, lane(y, q)));
         }
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------- K2
-
-// mean: allreduce_mean's (0.0 + sum) * (1/P) (trainer.cpp:41-45) -- the
-// leading +0 turns a -0 sum into +0 exactly as the reference does; otherwise
-// the plain embedding of covap_decompress (compress.cpp:100) times `inv`.
-template <typename T>
-__device__ __forceinline__ T scale_of(T x, T inv, int mean) {
-  return mul_rn(mean ? add_rn(T(0), x) : x, inv);
-}
-
-template <typename T>
-__device__ __forceinline__ void unpack_scalar(const T* __restrict__ recv, T* __restrict__ out,
-                                              const Run* __restrict__ runs, int nruns, uint64_t e,
-                                              T inv, int mean) {
-  const int j = run_of(runs, nruns, first_run_after(runs, nruns, e), e);
-  out[e] = (j >= 0) ? scale_of(recv[runs[j].dst + (e - runs[j].begin)], inv, mean) : T(0);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads)
-    unpack_kernel(const T* __restrict__ recv, T* __restrict__ out, const Run* __restrict__ runs,
-                  int nruns, uint64_t a, uint64_t b, T inv, int mean) {
-  using V = typename V16<T>::type;
-  constexpr int W = V16<T>::n;
-  const uint64_t A = (a + W - 1) / W * W;
-  if (A >= b) {
-    if (blockIdx.x == 0)
-      for (uint64_t e = a + threadIdx.x; e < b; e += blockDim.x)
-        unpack_scalar(recv, out, runs, nruns, e, inv, mean);
-    return;
-  }
-  const uint64_t B = b / W * W;
-  if (blockIdx.x == 0) {
-    if (threadIdx.x < A - a) unpack_scalar(recv, out, runs, nruns, a + threadIdx.x, inv, mean);
-    if (threadIdx.x < b - B) unpack_scalar(recv, out, runs, nruns, B + threadIdx.x, inv, mean);
-  }
-  const uint64_t nvec = (B - A) / W;
-  const uint64_t v0 = nvec * blockIdx.x / gridDim.x;
-  const uint64_t v1 = nvec * (blockIdx.x + 1) / gridDim.x;
-  if (v0 >= v1) return;
-  V* __restrict__ ov = reinterpret_cast<V*>(out + A);
-
-  int j = first_run_after(runs, nruns, A + v0 * W);
-  constexpr uint64_t kTile = (uint64_t)kThreads * kUnroll;
-  for (uint64_t t = v0; t < v1; t += kTile) {
-    const uint64_t te0 = A + t * W;
-    const uint64_t te1 = A + min(t + kTile, v1) * W;
-    while (j < nruns && runs[j].end <= te0) ++j;
-    uint64_t rb = 0, re = 0, rd = 0;
-    if (j < nruns) {
-      rb = runs[j].begin;
-      re = runs[j].end;
-      rd = runs[j].dst;
-    }
-    const bool none = (j >= nruns) || rb >= te1;
-    const bool full = !none && rb <= te0 && te1 <= re;
-    if (none) {
-      V z;
+        if (OP == 1 && full) {
 #pragma unroll
-      for (int k = 0; k < W; ++k) lane<V, T>(z, k) = T(0);
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t v = t + (uint64_t)u * kThreads + threadIdx.x;
-        if (v < v1) __stcs(ov + v, z);
-      }
-    } else if (full) {
-      V x[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t v = t + (uint64_t)u * kThreads + threadIdx.x;
-        if (v < v1) x[u] = __ldcs(reinterpret_cast<const V*>(recv + rd + (A + v * W - rb)));
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t v = t + (uint64_t)u * kThreads + threadIdx.x;
-        if (v >= v1) continue;
-        V o;
-#pragma unroll
-        for (int k = 0; k < W; ++k) lane<V, T>(o, k) = scale_of(lane<V, T>(x[u], k), inv, mean);
-        __stcs(ov + v, o);
+          for (int q = 0; q < W; ++q) lane(x, q) = scale_of(lane(x, q), A.inv, 1);
+        }
+        sv[v] = x;
       }
     } else {
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t v = t + (uint64_t)u * kThreads + threadIdx.x;
-        if (v >= v1) continue;
-        const uint64_t e = A + v * W;
-        int jj = j;
-        V o;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-          const uint64_t ee = e + k;
-          while (jj < nruns && runs[jj].end <= ee) ++jj;
-          lane<V, T>(o, k) = (jj < nruns && runs[jj].begin <= ee)
-                                 ? scale_of(recv[runs[jj].dst + (ee - runs[jj].begin)], inv, mean)
-                                 : T(0);
-        }
-        __stcs(ov + v, o);
+      int j = sel.j;
+      for (uint32_t i = threadIdx.x; i < n; i += kThreads)
+        element<T, OP>(A, j, e0 + i, gs[i], A.ef ? rs[i] : T(0));
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = n * sizeof(T);
+      if (sel.cls == kFull) {
+        if (OP == 0)
+          bulk_store(A.send + sel.rd + (e0 - sel.rb), st, bytes);
+        else
+          bulk_store(A.out + e0, st, bytes);
+        bulk_store(A.r + e0, zero, bytes);  // residual reset (compress.cpp:77)
+      } else if (sel.cls == kNone) {
+        bulk_store(A.r + e0, st, bytes);    // r = compensated (compress.cpp:79)
+        if (OP == 1) bulk_store(A.out + e0, zero, bytes);
       }
+      bulk_commit();  // one group per tile, possibly empty, keeps the count exact
+      if (k + kStages < my) issue(k + kStages);
     }
   }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+// ------------------------------------------------------------ K2
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
+  constexpr uint32_t TE = kTileBytes / sizeof(T);
+  using V = typename Vec16<T>::type;
+  constexpr uint32_t W = 16 / sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* in = reinterpret_cast<T*>(smem);  // kStagesK2 tiles
+  T* stage = in + kStagesK2 * TE;      // 2 tiles
+  T* zero = stage + 2 * TE;            // 1 tile
+  __shared__ __align__(8) uint64_t bar[kStagesK2];
+
+  const uint64_t a16 = (A.a + 16 / sizeof(T) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
+  const uint64_t b16 = A.b / (16 / sizeof(T)) * (16 / sizeof(T));
+  if (a16 >= b16) {
+    if (blockIdx.x == 0)
+      for (uint64_t e = A.a + threadIdx.x; e < A.b; e += blockDim.x) {
+        int j = first_run_after(A.runs, A.nruns, e);
+        element<T, 2>(A, j, e, T(0), T(0));
+      }
+    return;
+  }
+  if (blockIdx.x == 0) edges<T, 2>(A, a16, b16);
+
+  const uint64_t ntiles = (b16 - a16 + TE - 1) / TE;
+  const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStagesK2; ++i) mbar_init(&bar[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_async_smem();
+  __syncthreads();
+
+  auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * TE; };
+  auto issue = [&](uint64_t k) {  // only "all selected" tiles need their recv slice
+    const int s = static_cast<int>(k % kStagesK2);
+    const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
+    const TileSel sel = classify(A.runs, A.nruns, e0, e1);
+    if (sel.cls == kFull) {
+      const uint32_t bytes = static_cast<uint32_t>((e1 - e0) * sizeof(T));
+      mbar_arrive_tx(&bar[s], bytes);
+      bulk_load(in + s * TE, A.recv + sel.rd + (e0 - sel.rb), bytes, &bar[s]);
+    } else {
+      mbar_arrive_tx(&bar[s], 0);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (uint64_t k = 0; k < my && k < kStagesK2; ++k) issue(k);
+
+  for (uint64_t k = 0; k < my; ++k) {
+    const int s = static_cast<int>(k % kStagesK2);
+    const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
+    const uint32_t n = static_cast<uint32_t>(e1 - e0);
+    T* st = stage + (k & 1) * TE;
+    const TileSel sel = classify(A.runs, A.nruns, e0, e1);
+    mbar_wait(&bar[s], static_cast<uint32_t>((k / kStagesK2) & 1));
+    if (threadIdx.x == 0) bulk_wait_read<1>();
+    __syncthreads();
+    if (sel.cls == kFull) {
+      const V* xv = reinterpret_cast<const V*>(in + s * TE);
+      V* sv = reinterpret_cast<V*>(st);
+      for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
+        V x = xv[v];
+#pragma unroll
+        for (int q = 0; q < W; ++q) lane(x, q) = scale_of(lane(x, q), A.inv, A.mean);
+        sv[v] = x;
+      }
+    } else if (sel.cls == kMixed) {
+      int j = sel.j;
+      for (uint32_t i = threadIdx.x; i < n; i += kThreads) element<T, 2>(A, j, e0 + i, T(0), T(0));
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = n * sizeof(T);
+      if (sel.cls == kFull)
+        bulk_store(A.out + e0, st, bytes);
+      else if (sel.cls == kNone)
+        bulk_store(A.out + e0, zero, bytes);  // zero fill (compress.cpp:91)
+      bulk_commit();
+      if (k + kStagesK2 < my) issue(k + kStagesK2);
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------- K0
@@ -295,26 +437,29 @@ template <typename T>
 __device__ __forceinline__ T gen_value(uint64_t key, uint64_t i, int kind) {
   const uint64_t x = splitmix_out(key + (i + 1) * 0x9e3779b97f4a7c15ULL);
   if (kind == 0) {
-    const int32_t s = (int32_t)((x & 0xffff) + ((x >> 16) & 0xffff) + ((x >> 32) & 0xffff) +
-                                (x >> 48)) -
+    const int32_t s = static_cast<int32_t>((x & 0xffff) + ((x >> 16) & 0xffff) +
+                                           ((x >> 32) & 0xffff) + (x >> 48)) -
                       131070;
-    return mul_rn((T)s, (T)(1.0 / 32768.0));
+    return mul_rn(static_cast<T>(s), static_cast<T>(1.0 / 32768.0));
   }
-  return (T)((int64_t)(x % 2001) - 1000);
+  return static_cast<T>(static_cast<int64_t>(x % 2001) - 1000);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
     generate_kernel(T* __restrict__ out, uint64_t n, uint64_t key, int kind, uint64_t begin) {
-  using V = typename V16<T>::type;
-  constexpr int W = V16<T>::n;
+  constexpr int W = 16 / sizeof(T);
   const uint64_t nvec = n / W;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
-    V o;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec;
+       v += stride) {
+    T o[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) lane<V, T>(o, k) = gen_value<T>(key, begin + v * W + k, kind);
-    reinterpret_cast<V*>(out)[v] = o;
+    for (int k = 0; k < W; ++k) o[k] = gen_value<T>(key, begin + v * W + k, kind);
+    if (W == 4)
+      reinterpret_cast<float4*>(out)[v] = *reinterpret_cast<float4*>(o);
+    else
+      reinterpret_cast<double2*>(out)[v] = *reinterpret_cast<double2*>(o);
   }
   if (blockIdx.x == 0)
     for (uint64_t e = nvec * W + threadIdx.x; e < n; e += blockDim.x)
@@ -335,33 +480,68 @@ __global__ void spin_kernel(uint64_t ns) {
 
 struct DeviceShape {
   int sms = 0;
-  int k1_f32 = 0, k1_f64 = 0, k2_f32 = 0, k2_f64 = 0;
+  bool ready = false;
 };
 
-DeviceShape& shape_for_current_device() {
+// One-time per-device setup: SM count and the >48 KB dynamic-smem opt-in of
+// every instantiation.
+cudaError_t shape(DeviceShape** out) {
   static std::mutex mu;
   static DeviceShape shapes[64];
   int dev = 0;
-  cudaGetDevice(&dev);
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lock(mu);
   DeviceShape& s = shapes[dev & 63];
-  if (s.sms == 0) {
-    cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.k1_f32, filter_pack_kernel<float>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.k1_f64, filter_pack_kernel<double>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.k2_f32, unpack_kernel<float>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.k2_f64, unpack_kernel<double>, kThreads, 0);
+  if (!s.ready) {
+    if ((e = cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+    const int k1 = static_cast<int>(kSmemK1), k2 = static_cast<int>(kSmemK2);
+    if ((e = cudaFuncSetAttribute(filter_kernel<float, 0>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k1)) ||
+        (e = cudaFuncSetAttribute(filter_kernel<float, 1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k1)) ||
+        (e = cudaFuncSetAttribute(filter_kernel<double, 0>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k1)) ||
+        (e = cudaFuncSetAttribute(filter_kernel<double, 1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k1)) ||
+        (e = cudaFuncSetAttribute(unpack_kernel<float>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k2)) ||
+        (e = cudaFuncSetAttribute(unpack_kernel<double>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k2)))
+      return e;
+    s.ready = true;
   }
-  return s;
+  *out = &s;
+  return cudaSuccess;
 }
 
-// One resident wave (SMs x CTAs/SM), fewer when the range is small: each CTA
-// then gets at least one full tile.
-unsigned grid_for(uint64_t n_elems, int width, int sms, int per_sm) {
-  const uint64_t nvec = n_elems / width;
-  const uint64_t tiles = (nvec + (uint64_t)kThreads * kUnroll - 1) / ((uint64_t)kThreads * kUnroll);
-  const uint64_t wave = (uint64_t)sms * (uint64_t)std::max(per_sm, 1);
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(wave, tiles));
+// Persistent grid: one CTA per SM (the smem footprint allows one), fewer
+// when the range has fewer 16 KB tiles than SMs.
+unsigned grid_for(uint64_t n_elems, size_t esize, int sms) {
+  const uint64_t te = kTileBytes / esize;
+  const uint64_t tiles = (n_elems + te - 1) / te;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(sms, tiles)));
+}
+
+template <typename T>
+Args<T> make_args(const void* g, void* r, void* send, void* out, const void* recv,
+                  const Run* runs, int nruns, uint64_t a, uint64_t b, double coeff, int ef,
+                  double inv, int mean) {
+  Args<T> A;
+  A.g = static_cast<const T*>(g);
+  A.r = static_cast<T*>(r);
+  A.send = static_cast<T*>(send);
+  A.out = static_cast<T*>(out);
+  A.recv = static_cast<const T*>(recv);
+  A.runs = runs;
+  A.nruns = nruns;
+  A.a = a;
+  A.b = b;
+  A.coeff = static_cast<T>(coeff);
+  A.ef = ef;
+  A.inv = static_cast<T>(inv);
+  A.mean = mean;
+  return A;
 }
 
 }  // namespace
@@ -370,45 +550,59 @@ cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, co
                                int nruns, uint64_t a, uint64_t b, double coeff, int ef,
                                cudaStream_t s) {
   if (b <= a) return cudaSuccess;
-  DeviceShape& sh = shape_for_current_device();
-  if (dtype == 0) {
-    const unsigned grid = grid_for(b - a, 4, sh.sms, sh.k1_f32);
-    filter_pack_kernel<float><<<grid, kThreads, 0, s>>>(
-        static_cast<const float*>(g), static_cast<float*>(r), static_cast<float*>(send), runs,
-        nruns, a, b, (float)coeff, ef);
-  } else {
-    const unsigned grid = grid_for(b - a, 2, sh.sms, sh.k1_f64);
-    filter_pack_kernel<double><<<grid, kThreads, 0, s>>>(
-        static_cast<const double*>(g), static_cast<double*>(r), static_cast<double*>(send), runs,
-        nruns, a, b, coeff, ef);
-  }
+  DeviceShape* sh;
+  cudaError_t e = shape(&sh);
+  if (e) return e;
+  if (dtype == 0)
+    filter_kernel<float, 0><<<grid_for(b - a, 4, sh->sms), kThreads, kSmemK1, s>>>(
+        make_args<float>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
+  else
+    filter_kernel<double, 0><<<grid_for(b - a, 8, sh->sms), kThreads, kSmemK1, s>>>(
+        make_args<double>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, const Run* runs,
+                                 int nruns, uint64_t a, uint64_t b, double coeff, int ef,
+                                 double inv, cudaStream_t s) {
+  if (b <= a) return cudaSuccess;
+  DeviceShape* sh;
+  cudaError_t e = shape(&sh);
+  if (e) return e;
+  if (dtype == 0)
+    filter_kernel<float, 1><<<grid_for(b - a, 4, sh->sms), kThreads, kSmemK1, s>>>(
+        make_args<float>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
+  else
+    filter_kernel<double, 1><<<grid_for(b - a, 8, sh->sms), kThreads, kSmemK1, s>>>(
+        make_args<double>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
   return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
                           uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s) {
   if (b <= a) return cudaSuccess;
-  DeviceShape& sh = shape_for_current_device();
-  if (dtype == 0) {
-    const unsigned grid = grid_for(b - a, 4, sh.sms, sh.k2_f32);
-    unpack_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<const float*>(recv),
-                                                   static_cast<float*>(out), runs, nruns, a, b,
-                                                   (float)inv, mean);
-  } else {
-    const unsigned grid = grid_for(b - a, 2, sh.sms, sh.k2_f64);
-    unpack_kernel<double><<<grid, kThreads, 0, s>>>(static_cast<const double*>(recv),
-                                                    static_cast<double*>(out), runs, nruns, a, b,
-                                                    inv, mean);
-  }
+  DeviceShape* sh;
+  cudaError_t e = shape(&sh);
+  if (e) return e;
+  if (dtype == 0)
+    unpack_kernel<float><<<grid_for(b - a, 4, sh->sms), kThreads, kSmemK2, s>>>(
+        make_args<float>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
+                         mean));
+  else
+    unpack_kernel<double><<<grid_for(b - a, 8, sh->sms), kThreads, kSmemK2, s>>>(
+        make_args<double>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
+                          mean));
   return cudaGetLastError();
 }
 
 cudaError_t launch_generate(int dtype, void* out, uint64_t n, uint64_t key, int kind,
                             uint64_t begin, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  DeviceShape& sh = shape_for_current_device();
-  const unsigned grid = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>((uint64_t)sh.sms * 8, (n / 4 + kThreads - 1) / kThreads));
+  DeviceShape* sh;
+  cudaError_t e = shape(&sh);
+  if (e) return e;
+  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(
+      1, std::min<uint64_t>(static_cast<uint64_t>(sh->sms) * 8, (n / 4 + kThreads - 1) / kThreads)));
   if (dtype == 0)
     generate_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<float*>(out), n, key, kind, begin);
   else
@@ -418,7 +612,7 @@ cudaError_t launch_generate(int dtype, void* out, uint64_t n, uint64_t key, int 
 
 cudaError_t launch_spin(double us, int blocks, cudaStream_t s) {
   if (us <= 0) return cudaSuccess;
-  spin_kernel<<<std::max(blocks, 1), 32, 0, s>>>((uint64_t)(us * 1000.0));
+  spin_kernel<<<std::max(blocks, 1), 32, 0, s>>>(static_cast<uint64_t>(us * 1000.0));
   return cudaGetLastError();
 }
 

@@ -305,3 +305,30 @@ def test_full_size_integer_conservation(covap, name, K):
         sent += out
     torch.cuda.synchronize()
     assert torch.equal(sent + sync.state.residuals, inp)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 3), ("tablev", 19), ("resnet50", 1)])
+def test_fused_single_rank_pass_equals_k1_k2(covap, dtype, name, K):
+    """K1F (the one-rank sync pass) is bit-identical to K1 -> K2(mean, 1/1),
+    also when the output overwrites the gradient in place."""
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    ef = covap.EfSchedule(True, 0.3, 1, 0.2)
+    a = covap.CompressorState(plan, dtype, 0, ef)
+    b = covap.CompressorState(plan, dtype, 0, ef)
+    d = plan.total_numel()
+    oa = torch.empty(d, dtype=dtype, device=DEV)
+    for s in range(K + 2):
+        g = torch.empty(d, dtype=dtype, device=DEV)
+        covap.generate(g, covap.stream_key(3, 0, s))
+        g[::11] = -0.0
+        a.filter_pack(g)
+        a.unpack(oa, 1.0, True)
+        a.step_end()
+        gb = g.clone()
+        b.filter_unpack(gb, gb)  # in place: out aliases grad
+        b.step_end()
+        torch.cuda.synchronize()
+        assert torch.equal(oa.view(torch.int32 if dtype == torch.float32 else torch.int64),
+                           gb.view(torch.int32 if dtype == torch.float32 else torch.int64))
+        assert torch.equal(a.residuals, b.residuals)
