@@ -12,6 +12,8 @@ from .errors import raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcovap_b200.so")
+# Development override (scripts/variants.sh builds kernel variants elsewhere).
+LIB_PATH = os.environ.get("COVAP_LIB_PATH", LIB_PATH)
 
 u8p = ctypes.POINTER(ctypes.c_uint8)
 u32p = ctypes.POINTER(ctypes.c_uint32)

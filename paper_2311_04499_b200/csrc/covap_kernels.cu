@@ -14,15 +14,15 @@
 // They are persistent TMA-bulk pipelines (design measured with
 // scripts/kbench.cu on B200: 0.89-0.98 of the copy peak for K1's 2-read /
 // 2-write shape vs 0.72-0.77 for a chunked LDG/STG version):
-//   * one CTA per SM (144 KB smem) walks 16 KB tiles of the launch range in
+//   * one CTA per SM (160 KB smem) walks 16 KB tiles of the launch range in
 //     interleaved order (tile = blockIdx + k * gridDim): all SMs stream
 //     through neighbouring DRAM pages at any instant;
-//   * thread 0 keeps kStages tiles of g and r in flight with
-//     cp.async.bulk (global -> smem, mbarrier complete_tx); results are
-//     staged in smem and written back with cp.async.bulk (smem -> global);
-//     a persistent zero tile in smem feeds the bulk stores that write zeros
-//     (residual reset of selected shards, zero fill of unselected ones), so
-//     zero streams cost no instructions;
+//   * thread 0 keeps kStages tiles of g and r (K2: kStagesK2 tiles of recv)
+//     in flight with cp.async.bulk (global -> smem, mbarrier complete_tx);
+//     results are staged in smem and written back with cp.async.bulk
+//     (smem -> global); zero streams (residual reset of selected shards,
+//     zero fill of unselected output) are plain 128-bit stores by all
+//     threads, so the bulk-store queue only carries data;
 //   * selection is positional: each tile binary-searches the phase's run
 //     table (a few entries, L1-resident) and is "none selected" or "all
 //     selected" (bulk path) or "mixed" (element path; only the tiles that
@@ -41,14 +41,36 @@
 namespace covapb {
 namespace {
 
+// Pipeline shape (defaults = the measured best on B200, see DESIGN.md §3;
+// the macros exist so scripts/variants.sh can A/B them in one GPU session).
+#ifndef COVAP_K1_STAGES
+#define COVAP_K1_STAGES 2
+#endif
+#ifndef COVAP_K2_STAGES
+#define COVAP_K2_STAGES 4
+#endif
+#ifndef COVAP_K1_TILE
+#define COVAP_K1_TILE 24576
+#endif
+#ifndef COVAP_K2_TILE
+#define COVAP_K2_TILE 32768
+#endif
+#ifndef COVAP_K1_CTAS  // K1/K1F CTAs per SM (the smem footprint must allow it)
+#define COVAP_K1_CTAS 1
+#endif
+#ifndef COVAP_ZERO_BULK  // 1: zero streams are bulk stores of a zero tile; 0: 128-bit STG
+#define COVAP_ZERO_BULK 1
+#endif
 constexpr int kThreads = 256;
-constexpr int kStages = 3;
-constexpr uint32_t kTileBytes = 16384;
-// K1/K1F: kStages x (g, r) input tiles + 2 staging tiles + 1 zero tile.
-constexpr uint32_t kSmemK1 = (2 * kStages + 3) * kTileBytes;
-// K2: kStagesK2 recv tiles + 2 staging tiles + 1 zero tile.
-constexpr int kStagesK2 = 4;
-constexpr uint32_t kSmemK2 = (kStagesK2 + 3) * kTileBytes;
+constexpr int kZeroTiles = COVAP_ZERO_BULK ? 1 : 0;
+// K1/K1F: kStages slots of (g, r) tiles + 2 staging tiles (+ zero tile).
+constexpr uint32_t kTileK1 = COVAP_K1_TILE;
+constexpr int kStages = COVAP_K1_STAGES;
+constexpr uint32_t kSmemK1 = (2 * kStages + 2 + kZeroTiles) * kTileK1;
+// K2: kStagesK2 recv slots + 2 staging tiles (+ zero tile).
+constexpr uint32_t kTileK2 = COVAP_K2_TILE;
+constexpr int kStagesK2 = COVAP_K2_STAGES;
+constexpr uint32_t kSmemK2 = (kStagesK2 + 2 + kZeroTiles) * kTileK2;
 
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
@@ -230,23 +252,41 @@ __device__ void edges(const Args<T>& A, uint64_t a16, uint64_t b16) {
   }
 }
 
+// Zero-fill of a 16-byte-aligned tile by all threads (128-bit stores): the
+// residual reset of selected shards and the zero fill of unselected output.
+template <typename T>
+__device__ __forceinline__ void zero_tile(T* dst, uint32_t n) {
+  using V = typename Vec16<T>::type;
+  constexpr uint32_t W = 16 / sizeof(T);
+  V z;
+  for (uint32_t q = 0; q < W; ++q) lane(z, q) = T(0);
+  V* d = reinterpret_cast<V*>(dst);
+  for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) d[v] = z;
+}
+
 // ------------------------------------------------------------ K1 / K1F
+//
+// Input ring: kStages slots of (g tile, r tile), refilled as soon as the tile
+// has been consumed.  Results go to one of two staging tiles and leave with a
+// bulk store; before a staging tile is rewritten, thread 0 waits until the
+// bulk store issued two tiles earlier has read it.  Zero streams (r of
+// selected tiles, out of unselected tiles in K1F) are plain 128-bit stores.
 
 // OP 0 = K1 filter_pack (selected -> send), OP 1 = K1F (selected -> out).
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
-  constexpr uint32_t TE = kTileBytes / sizeof(T);  // elements per tile
+__global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const Args<T> A) {
+  constexpr uint32_t TE = kTileK1 / sizeof(T);  // elements per tile
   using V = typename Vec16<T>::type;
   constexpr uint32_t W = 16 / sizeof(T);
   extern __shared__ __align__(128) unsigned char smem[];
-  T* gin = reinterpret_cast<T*>(smem);  // kStages tiles
-  T* rin = gin + kStages * TE;          // kStages tiles
-  T* stage = rin + kStages * TE;        // 2 tiles
-  T* zero = stage + 2 * TE;             // 1 tile
+  T* gin = reinterpret_cast<T*>(smem);  // kStages tiles (g)
+  T* rin = gin + kStages * TE;          // kStages tiles (r)
+  T* stage = rin + kStages * TE;        // 2 staging tiles
+  T* zero = stage + 2 * TE;             // zero tile (COVAP_ZERO_BULK)
   __shared__ __align__(8) uint64_t bar[kStages];
 
-  const uint64_t a16 = (A.a + 16 / sizeof(T) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
-  const uint64_t b16 = A.b / (16 / sizeof(T)) * (16 / sizeof(T));
+  const uint64_t a16 = (A.a + W - 1) / W * W;
+  const uint64_t b16 = A.b / W * W;
   if (a16 >= b16) {  // nothing vector-sized: element path only
     if (blockIdx.x == 0) {
       for (uint64_t e = A.a + threadIdx.x; e < A.b; e += blockDim.x) {
@@ -260,12 +300,13 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
 
   const uint64_t ntiles = (b16 - a16 + TE - 1) / TE;
   const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
+  if (COVAP_ZERO_BULK)
+    for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&bar[i]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  fence_async_smem();  // zero tile visible to the bulk-copy (async) proxy
+  fence_async_smem();
   __syncthreads();
 
   auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * TE; };
@@ -284,12 +325,11 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
     const int s = static_cast<int>(k % kStages);
     const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
     const uint32_t n = static_cast<uint32_t>(e1 - e0);
-    T* st = stage + (k & 1) * TE;
     const TileSel sel = classify(A.runs, A.nruns, e0, e1);
-    mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
+    T* st = stage + (k & 1) * TE;
     if (threadIdx.x == 0) bulk_wait_read<1>();  // staging tile (k & 1) free again
+    mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
     __syncthreads();
-
     const T* gs = gin + s * TE;
     const T* rs = rin + s * TE;
     if (sel.cls != kMixed) {
@@ -303,13 +343,20 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
         if (A.ef) {
           const V y = rv[v];
 #pragma unroll
-          for (int q = 0; q < W; ++q) lane(x, q) = add_rn(lane(x, q), mul_rn(A.coeff, lane(y, q)));
+          for (int q = 0; q < static_cast<int>(W); ++q)
+            lane(x, q) = add_rn(lane(x, q), mul_rn(A.coeff, lane(y, q)));
         }
         if (OP == 1 && full) {
 #pragma unroll
-          for (int q = 0; q < W; ++q) lane(x, q) = scale_of(lane(x, q), A.inv, 1);
+          for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, 1);
         }
         sv[v] = x;
+      }
+      if (!COVAP_ZERO_BULK) {
+        if (full)
+          zero_tile(A.r + e0, n);    // residual reset (compress.cpp:77)
+        else if (OP == 1)
+          zero_tile(A.out + e0, n);  // unselected output is zero (compress.cpp:91)
       }
     } else {
       int j = sel.j;
@@ -325,33 +372,38 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
           bulk_store(A.send + sel.rd + (e0 - sel.rb), st, bytes);
         else
           bulk_store(A.out + e0, st, bytes);
-        bulk_store(A.r + e0, zero, bytes);  // residual reset (compress.cpp:77)
+        if (COVAP_ZERO_BULK) bulk_store(A.r + e0, zero, bytes);  // residual reset
       } else if (sel.cls == kNone) {
-        bulk_store(A.r + e0, st, bytes);    // r = compensated (compress.cpp:79)
-        if (OP == 1) bulk_store(A.out + e0, zero, bytes);
+        bulk_store(A.r + e0, st, bytes);  // r = compensated (compress.cpp:79)
+        if (COVAP_ZERO_BULK && OP == 1) bulk_store(A.out + e0, zero, bytes);
       }
-      bulk_commit();  // one group per tile, possibly empty, keeps the count exact
-      if (k + kStages < my) issue(k + kStages);
+      bulk_commit();  // one group per tile (possibly empty)
+      if (k + kStages < my) issue(k + kStages);  // input slot s is consumed
     }
   }
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------ K2
+//
+// Only "all selected" tiles need their recv slice: they go through a
+// kStagesK2-slot input ring and two staging tiles as in K1.  "None selected"
+// tiles are a 128-bit zero fill by all threads; "mixed" tiles take the
+// element path.
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
-  constexpr uint32_t TE = kTileBytes / sizeof(T);
+  constexpr uint32_t TE = kTileK2 / sizeof(T);
   using V = typename Vec16<T>::type;
   constexpr uint32_t W = 16 / sizeof(T);
   extern __shared__ __align__(128) unsigned char smem[];
-  T* in = reinterpret_cast<T*>(smem);  // kStagesK2 tiles
-  T* stage = in + kStagesK2 * TE;      // 2 tiles
-  T* zero = stage + 2 * TE;            // 1 tile
+  T* in = reinterpret_cast<T*>(smem);  // kStagesK2 slots
+  T* stage = in + kStagesK2 * TE;      // 2 staging tiles
+  T* zero = stage + 2 * TE;            // zero tile (COVAP_ZERO_BULK)
   __shared__ __align__(8) uint64_t bar[kStagesK2];
 
-  const uint64_t a16 = (A.a + 16 / sizeof(T) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
-  const uint64_t b16 = A.b / (16 / sizeof(T)) * (16 / sizeof(T));
+  const uint64_t a16 = (A.a + W - 1) / W * W;
+  const uint64_t b16 = A.b / W * W;
   if (a16 >= b16) {
     if (blockIdx.x == 0)
       for (uint64_t e = A.a + threadIdx.x; e < A.b; e += blockDim.x) {
@@ -364,7 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
 
   const uint64_t ntiles = (b16 - a16 + TE - 1) / TE;
   const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
+  if (COVAP_ZERO_BULK)
+    for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStagesK2; ++i) mbar_init(&bar[i]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -373,56 +426,70 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   __syncthreads();
 
   auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * TE; };
-  auto issue = [&](uint64_t k) {  // only "all selected" tiles need their recv slice
-    const int s = static_cast<int>(k % kStagesK2);
-    const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
-    const TileSel sel = classify(A.runs, A.nruns, e0, e1);
-    if (sel.cls == kFull) {
-      const uint32_t bytes = static_cast<uint32_t>((e1 - e0) * sizeof(T));
-      mbar_arrive_tx(&bar[s], bytes);
-      bulk_load(in + s * TE, A.recv + sel.rd + (e0 - sel.rb), bytes, &bar[s]);
-    } else {
-      mbar_arrive_tx(&bar[s], 0);
+  // Producer (thread 0): next tile to examine, next slot sequence number;
+  // only "all selected" tiles take a slot.
+  uint64_t kp = 0, qp = 0;
+  auto produce_one = [&]() {
+    while (kp < my) {
+      const uint64_t e0 = tile_lo(kp), e1 = min(e0 + TE, b16);
+      const TileSel sel = classify(A.runs, A.nruns, e0, e1);
+      ++kp;
+      if (sel.cls == kFull) {
+        const int s = static_cast<int>(qp % kStagesK2);
+        const uint32_t bytes = static_cast<uint32_t>((e1 - e0) * sizeof(T));
+        mbar_arrive_tx(&bar[s], bytes);
+        bulk_load(in + s * TE, A.recv + sel.rd + (e0 - sel.rb), bytes, &bar[s]);
+        ++qp;
+        return;
+      }
     }
   };
   if (threadIdx.x == 0)
-    for (uint64_t k = 0; k < my && k < kStagesK2; ++k) issue(k);
+    for (int i = 0; i < kStagesK2; ++i) produce_one();
 
+  uint64_t qc = 0;  // consumer slot sequence number
   for (uint64_t k = 0; k < my; ++k) {
-    const int s = static_cast<int>(k % kStagesK2);
     const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
     const uint32_t n = static_cast<uint32_t>(e1 - e0);
-    T* st = stage + (k & 1) * TE;
     const TileSel sel = classify(A.runs, A.nruns, e0, e1);
-    mbar_wait(&bar[s], static_cast<uint32_t>((k / kStagesK2) & 1));
-    if (threadIdx.x == 0) bulk_wait_read<1>();
-    __syncthreads();
-    if (sel.cls == kFull) {
-      const V* xv = reinterpret_cast<const V*>(in + s * TE);
-      V* sv = reinterpret_cast<V*>(st);
-      for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
-        V x = xv[v];
-#pragma unroll
-        for (int q = 0; q < W; ++q) lane(x, q) = scale_of(lane(x, q), A.inv, A.mean);
-        sv[v] = x;
-      }
-    } else if (sel.cls == kMixed) {
+    if (sel.cls == kNone) {  // zero fill (compress.cpp:91)
+      if (!COVAP_ZERO_BULK)
+        zero_tile(A.out + e0, n);
+      else if (threadIdx.x == 0)
+        bulk_store(A.out + e0, zero, n * sizeof(T));
+      continue;
+    }
+    if (sel.cls == kMixed) {
       int j = sel.j;
       for (uint32_t i = threadIdx.x; i < n; i += kThreads) element<T, 2>(A, j, e0 + i, T(0), T(0));
+      continue;
+    }
+    const int s = static_cast<int>(qc % kStagesK2);
+    T* st = stage + (qc & 1) * TE;
+    if (threadIdx.x == 0) bulk_wait_read<1>();
+    mbar_wait(&bar[s], static_cast<uint32_t>((qc / kStagesK2) & 1));
+    __syncthreads();
+    const V* xv = reinterpret_cast<const V*>(in + s * TE);
+    V* sv = reinterpret_cast<V*>(st);
+    for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
+      V x = xv[v];
+#pragma unroll
+      for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, A.mean);
+      sv[v] = x;
     }
     fence_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
-      const uint32_t bytes = n * sizeof(T);
-      if (sel.cls == kFull)
-        bulk_store(A.out + e0, st, bytes);
-      else if (sel.cls == kNone)
-        bulk_store(A.out + e0, zero, bytes);  // zero fill (compress.cpp:91)
+      bulk_store(A.out + e0, st, n * sizeof(T));
       bulk_commit();
-      if (k + kStagesK2 < my) issue(k + kStagesK2);
+      produce_one();  // input slot s is consumed
     }
+    ++qc;
   }
-  if (threadIdx.x == 0) bulk_wait_all();
+  if (threadIdx.x == 0) {
+    bulk_commit();
+    bulk_wait_all();
+  }
 }
 
 // ---------------------------------------------------------------- K0
@@ -517,8 +584,8 @@ cudaError_t shape(DeviceShape** out) {
 
 // Persistent grid: one CTA per SM (the smem footprint allows one), fewer
 // when the range has fewer 16 KB tiles than SMs.
-unsigned grid_for(uint64_t n_elems, size_t esize, int sms) {
-  const uint64_t te = kTileBytes / esize;
+unsigned grid_for(uint64_t n_elems, size_t esize, int sms, uint32_t tile_bytes) {
+  const uint64_t te = tile_bytes / esize;
   const uint64_t tiles = (n_elems + te - 1) / te;
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(sms, tiles)));
 }
@@ -554,10 +621,10 @@ cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, co
   cudaError_t e = shape(&sh);
   if (e) return e;
   if (dtype == 0)
-    filter_kernel<float, 0><<<grid_for(b - a, 4, sh->sms), kThreads, kSmemK1, s>>>(
+    filter_kernel<float, 0><<<grid_for(b - a, 4, sh->sms * COVAP_K1_CTAS, kTileK1), kThreads, kSmemK1, s>>>(
         make_args<float>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
   else
-    filter_kernel<double, 0><<<grid_for(b - a, 8, sh->sms), kThreads, kSmemK1, s>>>(
+    filter_kernel<double, 0><<<grid_for(b - a, 8, sh->sms * COVAP_K1_CTAS, kTileK1), kThreads, kSmemK1, s>>>(
         make_args<double>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
   return cudaGetLastError();
 }
@@ -570,10 +637,10 @@ cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, c
   cudaError_t e = shape(&sh);
   if (e) return e;
   if (dtype == 0)
-    filter_kernel<float, 1><<<grid_for(b - a, 4, sh->sms), kThreads, kSmemK1, s>>>(
+    filter_kernel<float, 1><<<grid_for(b - a, 4, sh->sms * COVAP_K1_CTAS, kTileK1), kThreads, kSmemK1, s>>>(
         make_args<float>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
   else
-    filter_kernel<double, 1><<<grid_for(b - a, 8, sh->sms), kThreads, kSmemK1, s>>>(
+    filter_kernel<double, 1><<<grid_for(b - a, 8, sh->sms * COVAP_K1_CTAS, kTileK1), kThreads, kSmemK1, s>>>(
         make_args<double>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
   return cudaGetLastError();
 }
@@ -585,11 +652,11 @@ cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* run
   cudaError_t e = shape(&sh);
   if (e) return e;
   if (dtype == 0)
-    unpack_kernel<float><<<grid_for(b - a, 4, sh->sms), kThreads, kSmemK2, s>>>(
+    unpack_kernel<float><<<grid_for(b - a, 4, sh->sms, kTileK2), kThreads, kSmemK2, s>>>(
         make_args<float>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
                          mean));
   else
-    unpack_kernel<double><<<grid_for(b - a, 8, sh->sms), kThreads, kSmemK2, s>>>(
+    unpack_kernel<double><<<grid_for(b - a, 8, sh->sms, kTileK2), kThreads, kSmemK2, s>>>(
         make_args<double>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
                           mean));
   return cudaGetLastError();
