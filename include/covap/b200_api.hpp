@@ -1,0 +1,237 @@
+#pragma once
+// The C++ face of the B200 COVAP path: the hot-path subset of the reference
+// library's public API (proj/include/covap/{compress,model,perf,sim,trainer,
+// rng}.hpp), re-implemented over the C-ABI of libcovap_b200.so
+// (include/covap_c.h).  Same names, argument meaning, value semantics and
+// exception classes, so reference callers — and the reference's own unit
+// tests — compile against it unchanged; the arithmetic runs in the sm_100a
+// kernels (fp64 instantiation, bit-exact with the reference's double code).
+//
+// The value-semantics functions copy host data to the device per call; the
+// device-resident classes at the end (covap::b200::Plan/State/Comm/Sync) are
+// the production interface.  Built into libcovap_cxx.so
+// (paper_2311_04499_b200/csrc/covap_cxx.cpp).
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "covap/errors.hpp"
+#include "covap_c.h"
+
+namespace covap {
+
+// ------------------------------------------------------------------ rng
+// splitmix64 stream (the reference's generator, rng.hpp:12-66 — same
+// algorithm, so seeds give the same streams).
+class SplitMix64 {
+ public:
+  explicit SplitMix64(std::uint64_t seed) : s_(seed) {}
+  std::uint64_t next();
+  double next_unit();                        // [0, 1), 53 random bits
+  std::uint64_t next_below(std::uint64_t n); // unbiased, rejection sampling
+  double next_normal();                      // Box-Muller, pairs cached
+
+ private:
+  std::uint64_t s_;
+  bool spare_ok_ = false;
+  double spare_ = 0.0;
+};
+std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t tag);
+
+// ------------------------------------------------------------------ model
+struct LayerSpec {
+  std::string name;
+  std::uint64_t param_count = 0;
+  std::uint32_t bytes_per_param = 4;
+  double backward_ms = 0.0;
+  std::uint64_t bytes() const { return param_count * bytes_per_param; }
+};
+
+struct ModelSpec {
+  static constexpr std::uint64_t kDefaultBucketCapBytes = 25ULL << 20;
+  std::vector<LayerSpec> layers;  // backward completion order
+  std::uint64_t bucket_cap_bytes = kDefaultBucketCapBytes;
+  std::uint64_t total_params() const;
+  double total_backward_ms() const;
+  void validate() const;  // InvalidInput
+};
+
+struct Bucket {
+  std::size_t index = 0;
+  std::vector<std::size_t> layer_refs;
+  std::uint64_t numel = 0;
+  std::uint64_t bytes = 0;
+};
+
+struct Shard {
+  std::size_t parent_bucket = 0;
+  std::uint64_t begin_elem = 0, end_elem = 0;
+  std::uint64_t numel() const { return end_elem - begin_elem; }
+};
+
+struct MedianNumel {
+  std::uint64_t twice = 0;  // exact: twice the median is an integer
+  double value() const { return static_cast<double>(twice) / 2.0; }
+  std::uint64_t floor_ratio(std::uint64_t numel) const { return (2 * numel) / twice; }
+};
+
+struct BucketPlan {
+  std::vector<Bucket> buckets;
+  std::uint64_t cap_bytes = ModelSpec::kDefaultBucketCapBytes;
+  std::vector<Shard> shards;
+  bool bucket_is_sharded(std::size_t bucket_index) const;
+  std::uint64_t total_numel() const;
+};
+
+struct EffectiveTensor {
+  std::size_t bucket = 0;
+  std::uint64_t begin = 0, end = 0;  // global flat offsets
+  std::uint64_t numel() const { return end - begin; }
+};
+
+BucketPlan allocate_buckets(const ModelSpec& model, std::uint64_t cap_bytes);
+BucketPlan allocate_buckets(const ModelSpec& model);
+MedianNumel median_numel(const BucketPlan& plan);
+BucketPlan shard_plan(const BucketPlan& plan, std::uint32_t interval);
+std::vector<EffectiveTensor> effective_tensors(const BucketPlan& plan);
+std::vector<std::uint64_t> effective_numels(const BucketPlan& plan);
+
+// ------------------------------------------------------------------ compress
+using TensorVec = std::vector<double>;
+using GradientSet = std::vector<TensorVec>;  // one vector per effective tensor
+
+enum class SelectionRule { kMatchStep, kPlusStep };
+
+std::vector<std::size_t> select_tensors(std::uint64_t num_steps, std::uint32_t interval,
+                                        std::size_t tensor_count,
+                                        SelectionRule rule = SelectionRule::kMatchStep);
+
+struct EfSchedule {
+  bool enabled = true;
+  double init_value = 0.3;
+  std::uint64_t ascend_steps = 100;
+  double ascend_range = 0.1;
+};
+double ef_coefficient(std::uint64_t num_steps, const EfSchedule& schedule);
+
+struct CovapConfig {
+  std::uint32_t interval = 1;
+  SelectionRule rule = SelectionRule::kMatchStep;
+  EfSchedule ef;
+};
+
+struct CompressorState {
+  GradientSet residuals;
+  std::uint64_t num_steps = 0;
+  static CompressorState zeros(const std::vector<std::uint64_t>& numels);
+};
+
+struct CompressedUpdate {
+  std::vector<std::size_t> selected;  // ascending
+  GradientSet payload;                // payload[i] <-> selected[i]
+  std::uint64_t step = 0;
+  std::uint64_t payload_elements() const;
+};
+
+// K1 on the GPU (fp64): fold scheduled residuals in, pack the selected
+// tensors, write the rest back as residuals, advance the step.
+CompressedUpdate covap_compress(const GradientSet& gradients, CompressorState& state,
+                                const CovapConfig& config);
+// K2 on the GPU (fp64): payload at its tensor slots, zeros elsewhere.
+GradientSet covap_decompress(const CompressedUpdate& update,
+                             const std::vector<std::uint64_t>& numels);
+
+// ------------------------------------------------------------------ trainer
+// (0 + v_0 + ... + v_{P-1}) * (1/P) in worker order, on the GPU.
+std::vector<double> allreduce_mean(const std::vector<std::vector<double>>& per_worker);
+
+// ------------------------------------------------------------------ perf / sim
+double ccr(double comm_ms, double comp_ms);
+std::uint32_t choose_interval(double ccr_value);
+
+enum class EventKind { kComputeStart, kComputeEnd, kCompressStart, kCompressEnd, kCommStart, kCommEnd };
+struct Event {
+  EventKind kind;
+  std::int64_t tensor;
+  std::uint32_t worker;
+  double time_ms;
+};
+struct IterationTimeline {
+  std::vector<Event> events;
+  double t_total_ms = 0.0;
+};
+struct ProfileResult {
+  double ccr = 0.0;
+  double comp_ms = 0.0;
+  double comm_aligned_ms = 0.0;
+  std::vector<double> naive_comm_ms;
+  std::uint32_t recommended_interval = 1;
+};
+ProfileResult profile_ccr(std::span<const IterationTimeline> per_worker,
+                          std::uint32_t expected_workers);
+
+// ------------------------------------------------------------------ device-resident API
+namespace b200 {
+
+namespace detail {
+[[noreturn]] void raise(covap_status st);
+inline void check(covap_status st) {
+  if (st != COVAP_OK) raise(st);
+}
+}  // namespace detail
+
+class Comm;
+
+// BucketPlan + effective tensors + per-phase send layout for one K.
+class Plan {
+ public:
+  Plan(const ModelSpec& model, std::uint32_t interval,
+       SelectionRule rule = SelectionRule::kMatchStep, int shard = -1);
+  const covap_plan* get() const { return p_.get(); }
+  covap_plan_info info() const;
+
+ private:
+  std::shared_ptr<covap_plan> p_;
+};
+
+// CompressorState resident on one GPU (fp32 or fp64 arena).
+class State {
+ public:
+  State(const Plan& plan, int dtype, int device, const EfSchedule& ef);
+  covap_state* get() const { return s_.get(); }
+  std::uint64_t num_steps() const;
+
+ private:
+  std::shared_ptr<covap_state> s_;
+};
+
+class Comm {
+ public:
+  static std::vector<std::uint8_t> unique_id();
+  Comm(const std::vector<std::uint8_t>& id, int nranks, int rank, int device);
+  covap_comm* get() const { return c_.get(); }
+
+ private:
+  std::shared_ptr<covap_comm> c_;
+};
+
+// One rank's gradient synchronisation (trainer.cpp:365-386 per rank).
+class Sync {
+ public:
+  Sync(const Plan& plan, const Comm* comm, int dtype, int device, const EfSchedule& ef);
+  void step(const void* grad, void* out, void* stream);                   // covap_sync_step
+  void bucket_ready(std::size_t bucket, const void* grad, void* out, void* stream);
+  void finish(void* stream);
+  State& state() { return state_; }
+
+ private:
+  State state_;
+  covap_comm* comm_;
+};
+
+}  // namespace b200
+}  // namespace covap

@@ -175,6 +175,15 @@ covap_status covap_step_end(covap_state* state);
 covap_status covap_sync_step(covap_state* state, covap_comm* comm, const void* grad, void* out,
                              void* stream);
 
+/* The same step on HOST buffers (pinned for overlap): the flat range is cut
+ * into chunks (chunk_elems, 0 = 4 Mi elements); chunk c's H2D copy, its
+ * kernels (+ the allreduce of its slice of the send buffer) and its D2H copy
+ * run on three streams, so PCIe traffic in both directions overlaps.
+ * dev_grad / dev_out are device staging buffers of N elements (may alias). */
+covap_status covap_sync_step_host(covap_state* state, covap_comm* comm, const void* host_grad,
+                                  void* host_out, void* dev_grad, void* dev_out,
+                                  uint64_t chunk_elems, void* stream);
+
 /* Overlapped schedule (the DDP-hook shape): bucket b's gradient is ready on
  * `stream` -> K1(b) on `stream`, event -> on the state's comm stream:
  * allreduce of b's selected range, K2(b); with one rank K1F(b) on `stream`.
@@ -207,6 +216,26 @@ covap_status covap_allreduce(covap_comm* comm, void* buf, uint64_t count, int dt
  * (sim.cpp:208-211).  Blocking.  comm NULL -> single rank. */
 covap_status covap_comm_profile_exchange(covap_comm* comm, const double* dur, size_t n_coll,
                                          double comp_ms, double* aligned_ms, double* comp_out);
+
+/* ------------------------------------------- memory and generic kernels -- */
+/* Used by the C++ value-semantics layer (include/covap/b200_api.hpp) so it
+ * needs no CUDA headers.  kind: 0 = host->device, 1 = device->host,
+ * 2 = device->device. */
+covap_status covap_device_alloc(int device, uint64_t bytes, void** out);
+covap_status covap_device_free(int device, void* ptr);
+covap_status covap_memcpy(void* dst, const void* src, uint64_t bytes, int kind, void* stream);
+covap_status covap_stream_synchronize(void* stream);
+/* covap_decompress for an arbitrary selection (compress.cpp:87-103): K2 over
+ * [0, total) with the caller's ascending ranges; range i's values come from
+ * payload[payload_off[i] ...].  mean / scale as covap_unpack.  Blocking. */
+covap_status covap_embed(int device, int dtype, const void* payload, void* out, uint64_t total,
+                         const uint64_t* sel_begin, const uint64_t* sel_end,
+                         const uint64_t* payload_off, size_t nsel, double scale, int mean,
+                         void* stream);
+/* allreduce_mean of P in-process workers (trainer.cpp:35-47): rows is P x n
+ * (worker-major), out = (0 + x_0 + ... + x_{P-1}) * (1/P) in worker order. */
+covap_status covap_mean_rows(int device, int dtype, const void* rows, void* out, uint64_t P,
+                             uint64_t n, void* stream);
 
 /* ------------------------------------------------------ harness kernels -- */
 

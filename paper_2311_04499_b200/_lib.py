@@ -77,6 +77,7 @@ _SIGS = {
     "covap_filter_unpack": (None, [vp, vp, vp, f64, sz, sz, vp]),
     "covap_step_end": (None, [vp]),
     "covap_sync_step": (None, [vp, vp, vp, vp, vp]),
+    "covap_sync_step_host": (None, [vp, vp, vp, vp, vp, vp, u64, vp]),
     "covap_bucket_ready": (None, [vp, vp, sz, vp, vp, vp]),
     "covap_step_finish": (None, [vp, vp]),
     "covap_dense_bucket_ready": (None, [vp, vp, sz, vp, vp, vp]),
@@ -87,6 +88,12 @@ _SIGS = {
     "covap_comm_size": (None, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
     "covap_allreduce": (None, [vp, vp, u64, i32, vp]),
     "covap_comm_profile_exchange": (None, [vp, f64p, sz, f64, f64p, f64p]),
+    "covap_device_alloc": (None, [i32, u64, ctypes.POINTER(vp)]),
+    "covap_device_free": (None, [i32, vp]),
+    "covap_memcpy": (None, [vp, vp, u64, i32, vp]),
+    "covap_stream_synchronize": (None, [vp]),
+    "covap_embed": (None, [i32, i32, vp, vp, u64, u64p, u64p, u64p, sz, f64, i32, vp]),
+    "covap_mean_rows": (None, [i32, i32, vp, vp, u64, u64, vp]),
     "covap_stream_key": (u64, [u64, u64, u64]),
     "covap_generate": (None, [vp, u64, i32, u64, i32, u64, vp]),
     "covap_spin": (None, [f64, i32, vp]),

@@ -595,6 +595,28 @@ class CovapSync:
         L.lib().covap_sync_step(self.state.handle, self._c(), _ptr(grad), _ptr(out),
                                 _stream_ptr(stream, self.device))
 
+    def sync_host(self, host_grad, host_out, dev_grad=None, dev_out=None,
+                  chunk_elems: int = 0, stream=None):
+        """The sync step on host (pinned) buffers: chunked H2D -> kernels (+
+        allreduce) -> D2H on three streams (covap_sync_step_host)."""
+        torch = _torch()
+        n = self.plan.total_numel()
+        if host_grad.numel() != n or host_out.numel() != n:
+            raise InvalidState("host buffer length does not match the plan")
+        if host_grad.dtype != self.state.dtype or host_out.dtype != self.state.dtype:
+            raise InvalidInput("host buffers must have the state's dtype")
+        dev = torch.device("cuda", self.device)
+        if dev_grad is None:
+            if getattr(self, "_stage", None) is None:
+                self._stage = torch.empty(n, dtype=self.state.dtype, device=dev)
+            dev_grad = self._stage
+        dev_out = dev_grad if dev_out is None else dev_out
+        L.lib().covap_sync_step_host(self.state.handle, self._c(),
+                                     ctypes.c_void_p(host_grad.data_ptr()),
+                                     ctypes.c_void_p(host_out.data_ptr()), _ptr(dev_grad),
+                                     _ptr(dev_out), int(chunk_elems),
+                                     _stream_ptr(stream, self.device))
+
     def bucket_ready(self, bucket: int, grad, out, stream=None):
         L.lib().covap_bucket_ready(self.state.handle, self._c(), int(bucket), _ptr(grad), _ptr(out),
                                    _stream_ptr(stream, self.device))

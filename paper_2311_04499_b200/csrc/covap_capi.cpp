@@ -51,6 +51,9 @@ struct covap_state {
   std::vector<uint64_t> phase_off;
   covapb::Run* d_full = nullptr;  // {[0, N), dst 0}: the dense (uncompressed) mean
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t h2d_stream = nullptr;  // host-buffer pipeline (covap_sync_step_host)
+  cudaStream_t d2h_stream = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_k;  // per-chunk event pools (reused cyclically)
   cudaEvent_t done = nullptr;
   std::vector<cudaEvent_t> ready, arrive, end;  // per bucket
   std::vector<uint8_t> timed;                   // bucket had a collective in the last step
@@ -59,6 +62,7 @@ struct covap_state {
 namespace {
 
 thread_local std::string g_last_error;
+constexpr int kChunkEvents = 64;
 
 covap_status fail(covap_status code, const std::string& msg) {
   g_last_error = msg;
@@ -374,6 +378,10 @@ void covap_state_destroy(covap_state* s) {
   for (auto e : s->arrive) cudaEventDestroy(e);
   for (auto e : s->end) cudaEventDestroy(e);
   if (s->done) cudaEventDestroy(s->done);
+  for (auto e : s->ev_in) cudaEventDestroy(e);
+  for (auto e : s->ev_k) cudaEventDestroy(e);
+  if (s->h2d_stream) cudaStreamDestroy(s->h2d_stream);
+  if (s->d2h_stream) cudaStreamDestroy(s->d2h_stream);
   if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
   if (prev >= 0) cudaSetDevice(prev);
   delete s;
@@ -412,6 +420,14 @@ covap_status covap_state_create(const covap_plan* plan, int dtype, int device,
                   cudaMemcpyHostToDevice));
     s->d_full = s->d_runs + full_off;
     CK(cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->h2d_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking));
+    s->ev_in.resize(kChunkEvents);
+    s->ev_k.resize(kChunkEvents);
+    for (int i = 0; i < kChunkEvents; ++i) {
+      CK(cudaEventCreateWithFlags(&s->ev_in[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&s->ev_k[i], cudaEventDisableTiming));
+    }
     CK(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
     const size_t nb = s->plan.buckets.size();
     s->ready.resize(nb);
@@ -547,6 +563,68 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
                          comm->nccl, st));
       k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, 0, n, st);
     }
+    ++s->num_steps;
+  });
+}
+
+covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* host_grad,
+                                  void* host_out, void* dev_grad, void* dev_out,
+                                  uint64_t chunk_elems, void* stream) {
+  return guarded([&] {
+    need(s && host_grad && host_out && dev_grad && dev_out, "NULL argument");
+    need_aligned(dev_grad, "dev_grad");
+    need_aligned(dev_out, "dev_out");
+    if (comm) need(comm->device == s->device, "communicator and state are on different devices");
+    DeviceGuard dg(s->device);
+    cudaStream_t st = as_stream(stream);
+    const uint64_t n = s->plan.total;
+    const size_t es = s->esize;
+    // Chunks of a multiple of 8192 elements (32 KB fp32), at least 1 Mi.
+    uint64_t chunk = std::max<uint64_t>(chunk_elems ? chunk_elems : (4u << 20), 1u << 20);
+    chunk = (chunk + 8191) / 8192 * 8192;
+    const int P = world(comm);
+    const auto& ph = phase_of(s->plan, s->num_steps);
+    const double inv = 1.0 / static_cast<double>(P);
+    // Step boundary: the copy streams start after everything already on `stream`.
+    CK(cudaEventRecord(s->done, st));
+    CK(cudaStreamWaitEvent(s->h2d_stream, s->done, 0));
+    uint64_t c = 0;
+    for (uint64_t a = 0; a < n; a += chunk, ++c) {
+      const uint64_t b = std::min(n, a + chunk);
+      cudaEvent_t ein = s->ev_in[c % kChunkEvents], ek = s->ev_k[c % kChunkEvents];
+      CK(cudaMemcpyAsync(static_cast<char*>(dev_grad) + a * es,
+                         static_cast<const char*>(host_grad) + a * es, (b - a) * es,
+                         cudaMemcpyHostToDevice, s->h2d_stream));
+      CK(cudaEventRecord(ein, s->h2d_stream));
+      CK(cudaStreamWaitEvent(st, ein, 0));
+      if (P == 1) {
+        k1f_range(s, dev_grad, dev_out, 1.0, a, b, st);
+      } else {
+        k1_range(s, dev_grad, nullptr, a, b, st);
+        // The chunk's selected elements occupy one contiguous envelope of the
+        // send buffer (runs map monotonically); every rank derives the same
+        // envelopes from the plan, so the collectives match.
+        uint64_t lo = UINT64_MAX, hi = 0;
+        for (const auto& r : ph.runs) {
+          const uint64_t x0 = std::max(a, r.begin), x1 = std::min(b, r.end);
+          if (x0 >= x1) continue;
+          lo = std::min(lo, r.dst + (x0 - r.begin));
+          hi = std::max(hi, r.dst + (x1 - r.begin));
+        }
+        if (hi > lo)
+          NK(ncclAllReduce(static_cast<char*>(s->send) + lo * es,
+                           static_cast<char*>(s->send) + lo * es, hi - lo, nccl_type(s->dtype),
+                           ncclSum, comm->nccl, st));
+        k2_range(s, nullptr, dev_out, inv, 1, a, b, st);
+      }
+      CK(cudaEventRecord(ek, st));
+      CK(cudaStreamWaitEvent(s->d2h_stream, ek, 0));
+      CK(cudaMemcpyAsync(static_cast<char*>(host_out) + a * es,
+                         static_cast<const char*>(dev_out) + a * es, (b - a) * es,
+                         cudaMemcpyDeviceToHost, s->d2h_stream));
+    }
+    CK(cudaEventRecord(s->done, s->d2h_stream));
+    CK(cudaStreamWaitEvent(st, s->done, 0));
     ++s->num_steps;
   });
 }
@@ -728,6 +806,79 @@ covap_status covap_comm_profile_exchange(covap_comm* c, const double* dur, size_
     cudaFree(d);
     std::copy(host.begin(), host.begin() + n_coll, aligned_ms);
     *comp_out = host[n_coll];
+  });
+}
+
+// ---------------------------------------------------------------- memory / generic kernels
+
+covap_status covap_device_alloc(int device, uint64_t bytes, void** out) {
+  return guarded([&] {
+    need(out != nullptr, "NULL out");
+    DeviceGuard dg(device);
+    *out = nullptr;
+    CK(cudaMalloc(out, std::max<uint64_t>(bytes, 16)));
+  });
+}
+
+covap_status covap_device_free(int device, void* p) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    CK(cudaFree(p));
+  });
+}
+
+covap_status covap_memcpy(void* dst, const void* src, uint64_t bytes, int kind, void* stream) {
+  return guarded([&] {
+    need(kind >= 0 && kind <= 2, "kind must be 0 (H2D), 1 (D2H) or 2 (D2D)");
+    if (bytes == 0) return;
+    need(dst && src, "NULL argument");
+    const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                             : kind == 1 ? cudaMemcpyDeviceToHost
+                                         : cudaMemcpyDeviceToDevice;
+    CK(cudaMemcpyAsync(dst, src, bytes, k, as_stream(stream)));
+  });
+}
+
+covap_status covap_stream_synchronize(void* stream) {
+  return guarded([&] { CK(cudaStreamSynchronize(as_stream(stream))); });
+}
+
+covap_status covap_embed(int device, int dtype, const void* payload, void* out, uint64_t total,
+                         const uint64_t* sel_begin, const uint64_t* sel_end,
+                         const uint64_t* payload_off, size_t nsel, double scale, int mean,
+                         void* stream) {
+  return guarded([&] {
+    need(out != nullptr && (nsel == 0 || (payload && sel_begin && sel_end && payload_off)),
+         "NULL argument");
+    need(dtype == COVAP_F32 || dtype == COVAP_F64, "bad dtype");
+    need_aligned(out, "out");
+    std::vector<covapb::Run> runs(nsel);
+    for (size_t i = 0; i < nsel; ++i) {
+      need(sel_begin[i] <= sel_end[i] && sel_end[i] <= total, "selection range out of bounds");
+      need(i == 0 || sel_begin[i] >= sel_end[i - 1], "selection ranges must ascend");
+      runs[i] = covapb::Run{sel_begin[i], sel_end[i], payload_off[i]};
+    }
+    DeviceGuard dg(device);
+    cudaStream_t st = as_stream(stream);
+    covapb::Run* d_runs = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&d_runs), std::max<size_t>(nsel, 1) * sizeof(covapb::Run), st));
+    if (nsel)
+      CK(cudaMemcpyAsync(d_runs, runs.data(), nsel * sizeof(covapb::Run), cudaMemcpyHostToDevice, st));
+    const cudaError_t e = covapb::launch_unpack(dtype, payload, out, d_runs, static_cast<int>(nsel),
+                                                0, total, scale, mean, st);
+    cudaFreeAsync(d_runs, st);
+    CK(e);
+    CK(cudaStreamSynchronize(st));  // the host run table above is stack memory
+  });
+}
+
+covap_status covap_mean_rows(int device, int dtype, const void* rows, void* out, uint64_t P,
+                             uint64_t n, void* stream) {
+  return guarded([&] {
+    need(rows && out, "NULL argument");
+    need(P >= 1, "allreduce needs at least one worker vector");
+    DeviceGuard dg(device);
+    CK(covapb::launch_mean_rows(dtype, rows, out, P, n, as_stream(stream)));
   });
 }
 

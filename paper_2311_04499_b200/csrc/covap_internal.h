@@ -35,6 +35,9 @@ cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, c
 // f(x) = (0 + x) * inv when mean (allreduce_mean), x * inv otherwise.
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
                           uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s);
+// allreduce_mean over P rows (P x n, worker-major) in worker order.
+cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,
+                             cudaStream_t s);
 // K0: synthetic gradients.
 cudaError_t launch_generate(int dtype, void* out, uint64_t n, uint64_t key, int kind,
                             uint64_t begin, cudaStream_t s);

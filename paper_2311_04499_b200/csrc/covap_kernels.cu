@@ -176,6 +176,7 @@ struct TileSel {
   uint64_t rd;
 };
 
+template <typename T>
 __device__ __forceinline__ TileSel classify(const Run* __restrict__ runs, int n, uint64_t e0,
                                             uint64_t e1) {
   TileSel s;
@@ -183,7 +184,10 @@ __device__ __forceinline__ TileSel classify(const Run* __restrict__ runs, int n,
   s.rb = s.rd = 0;
   if (s.j >= n || runs[s.j].begin >= e1) {
     s.cls = kNone;
-  } else if (runs[s.j].begin <= e0 && e1 <= runs[s.j].end) {
+  } else if (runs[s.j].begin <= e0 && e1 <= runs[s.j].end &&
+             (runs[s.j].dst - runs[s.j].begin) % (16 / sizeof(T)) == 0) {
+    // (the planner always aligns dst; caller-built tables may not, and a
+    // misaligned run takes the element path)
     s.cls = kFull;
     s.rb = runs[s.j].begin;
     s.rd = runs[s.j].dst;
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
     const int s = static_cast<int>(k % kStages);
     const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
     const uint32_t n = static_cast<uint32_t>(e1 - e0);
-    const TileSel sel = classify(A.runs, A.nruns, e0, e1);
+    const TileSel sel = classify<T>(A.runs, A.nruns, e0, e1);
     T* st = stage + (k & 1) * TE;
     if (threadIdx.x == 0) bulk_wait_read<1>();  // staging tile (k & 1) free again
     mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   auto produce_one = [&]() {
     while (kp < my) {
       const uint64_t e0 = tile_lo(kp), e1 = min(e0 + TE, b16);
-      const TileSel sel = classify(A.runs, A.nruns, e0, e1);
+      const TileSel sel = classify<T>(A.runs, A.nruns, e0, e1);
       ++kp;
       if (sel.cls == kFull) {
         const int s = static_cast<int>(qp % kStagesK2);
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   for (uint64_t k = 0; k < my; ++k) {
     const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
     const uint32_t n = static_cast<uint32_t>(e1 - e0);
-    const TileSel sel = classify(A.runs, A.nruns, e0, e1);
+    const TileSel sel = classify<T>(A.runs, A.nruns, e0, e1);
     if (sel.cls == kNone) {  // zero fill (compress.cpp:91)
       if (!COVAP_ZERO_BULK)
         zero_tile(A.out + e0, n);
@@ -460,8 +464,18 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
       continue;
     }
     if (sel.cls == kMixed) {
-      int j = sel.j;
-      for (uint32_t i = threadIdx.x; i < n; i += kThreads) element<T, 2>(A, j, e0 + i, T(0), T(0));
+      // Tiles that straddle a shard boundary: per element, but with no
+      // loop-carried state so the recv loads of consecutive iterations
+      // overlap (the runs table is L1-resident).
+#pragma unroll 4
+      for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+        const uint64_t e = e0 + i;
+        int j = sel.j;
+        while (j < A.nruns && A.runs[j].end <= e) ++j;
+        const bool in = j < A.nruns && A.runs[j].begin <= e;
+        const uint64_t src = in ? A.runs[j].dst + (e - A.runs[j].begin) : 0;
+        A.out[e] = in ? scale_of(A.recv[src], A.inv, A.mean) : T(0);
+      }
       continue;
     }
     const int s = static_cast<int>(qc % kStagesK2);
@@ -489,6 +503,20 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   if (threadIdx.x == 0) {
     bulk_commit();
     bulk_wait_all();
+  }
+}
+
+// ---------------------------------------------------------------- mean of rows
+// allreduce_mean for P in-process workers (trainer.cpp:41-45): out[i] =
+// ((0 + x_0[i]) + x_1[i] + ... + x_{P-1}[i]) * inv, in worker order.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    mean_rows_kernel(const T* __restrict__ rows, T* __restrict__ out, uint64_t P, uint64_t n, T inv) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    T acc = T(0);
+    for (uint64_t w = 0; w < P; ++w) acc = add_rn(acc, rows[w * n + i]);
+    out[i] = mul_rn(acc, inv);
   }
 }
 
@@ -659,6 +687,25 @@ cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* run
     unpack_kernel<double><<<grid_for(b - a, 8, sh->sms, kTileK2), kThreads, kSmemK2, s>>>(
         make_args<double>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
                           mean));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,
+                             cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  DeviceShape* sh;
+  cudaError_t e = shape(&sh);
+  if (e) return e;
+  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(
+      1, std::min<uint64_t>(static_cast<uint64_t>(sh->sms) * 8, (n + kThreads - 1) / kThreads)));
+  const double inv = 1.0 / static_cast<double>(P);
+  if (dtype == 0)
+    mean_rows_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<const float*>(rows),
+                                                      static_cast<float*>(out), P, n,
+                                                      static_cast<float>(inv));
+  else
+    mean_rows_kernel<double><<<grid, kThreads, 0, s>>>(static_cast<const double*>(rows),
+                                                       static_cast<double*>(out), P, n, inv);
   return cudaGetLastError();
 }
 

@@ -332,3 +332,26 @@ def test_fused_single_rank_pass_equals_k1_k2(covap, dtype, name, K):
         assert torch.equal(oa.view(torch.int32 if dtype == torch.float32 else torch.int64),
                            gb.view(torch.int32 if dtype == torch.float32 else torch.int64))
         assert torch.equal(a.residuals, b.residuals)
+
+
+@pytest.mark.parametrize("name,K,chunk", [("resnet50", 1, 0), ("resnet50", 4, 1 << 20),
+                                          ("vgg16", 4, 3 << 20), ("tablev", 19, 1 << 21)])
+def test_host_pipeline_equals_device_sync(covap, name, K, chunk):
+    """covap_sync_step_host (chunked H2D / kernels / D2H on three streams)
+    gives exactly the device-resident step's output and residuals."""
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    a = covap.CovapSync(plan, None, torch.float32, 0)
+    b = covap.CovapSync(plan, None, torch.float32, 0)
+    d = plan.total_numel()
+    g = torch.empty(d, device=DEV)
+    out = torch.empty(d, device=DEV)
+    hin = torch.empty(d, pin_memory=True)
+    hout = torch.empty(d, pin_memory=True)
+    for s in range(K + 1):
+        covap.generate(g, covap.stream_key(21, 0, s))
+        hin.copy_(g)
+        a.sync(g, out)
+        b.sync_host(hin, hout, chunk_elems=chunk)
+        torch.cuda.synchronize()
+        assert torch.equal(out.cpu(), hout)
+        assert torch.equal(a.state.residuals, b.state.residuals)
