@@ -61,6 +61,12 @@ namespace {
 #ifndef COVAP_ZERO_BULK  // 1: zero streams are bulk stores of a zero tile; 0: 128-bit STG
 #define COVAP_ZERO_BULK 1
 #endif
+#ifndef COVAP_K1_STG  // 1: K1 results leave by 128-bit STG from registers (no staging tiles)
+#define COVAP_K1_STG 0
+#endif
+#ifndef COVAP_K2_STG  // 1: K2 results leave by 128-bit STG from registers (no staging tiles)
+#define COVAP_K2_STG 0
+#endif
 constexpr int kThreads = 256;
 constexpr int kZeroTiles = COVAP_ZERO_BULK ? 1 : 0;
 // K1/K1F: kStages slots of (g, r) tiles + 2 staging tiles (+ zero tile).
@@ -331,11 +337,50 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
     const uint32_t n = static_cast<uint32_t>(e1 - e0);
     const TileSel sel = classify<T>(A.runs, A.nruns, e0, e1);
     T* st = stage + (k & 1) * TE;
+    const T* gs = gin + s * TE;
+    const T* rs = rin + s * TE;
+    if constexpr (COVAP_K1_STG != 0) {
+      // Results go straight from registers to global memory; the slot is
+      // free once every thread has read it.
+      mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
+      if (sel.cls != kMixed) {
+        const bool full = sel.cls == kFull;
+        const V* gv = reinterpret_cast<const V*>(gs);
+        const V* rv = reinterpret_cast<const V*>(rs);
+        V z;
+#pragma unroll
+        for (int q = 0; q < static_cast<int>(W); ++q) lane(z, q) = T(0);
+        V* dst = full ? reinterpret_cast<V*>(OP == 0 ? A.send + sel.rd + (e0 - sel.rb) : A.out + e0)
+                      : reinterpret_cast<V*>(A.r + e0);
+        V* zdst = full ? reinterpret_cast<V*>(A.r + e0)
+                       : (OP == 1 ? reinterpret_cast<V*>(A.out + e0) : nullptr);
+        for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
+          V x = gv[v];
+          if (A.ef) {
+            const V y = rv[v];
+#pragma unroll
+            for (int q = 0; q < static_cast<int>(W); ++q)
+              lane(x, q) = add_rn(lane(x, q), mul_rn(A.coeff, lane(y, q)));
+          }
+          if (OP == 1 && full) {
+#pragma unroll
+            for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, 1);
+          }
+          dst[v] = x;
+          if (zdst) zdst[v] = z;
+        }
+      } else {
+        int j = sel.j;
+        for (uint32_t i = threadIdx.x; i < n; i += kThreads)
+          element<T, OP>(A, j, e0 + i, gs[i], A.ef ? rs[i] : T(0));
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && k + kStages < my) issue(k + kStages);
+      continue;
+    }
     if (threadIdx.x == 0) bulk_wait_read<1>();  // staging tile (k & 1) free again
     mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
     __syncthreads();
-    const T* gs = gin + s * TE;
-    const T* rs = rin + s * TE;
     if (sel.cls != kMixed) {
       // 16-byte vectors: a warp touches 512 contiguous bytes, no bank conflicts
       const bool full = sel.cls == kFull;
@@ -464,22 +509,52 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
       continue;
     }
     if (sel.cls == kMixed) {
-      // Tiles that straddle a shard boundary: per element, but with no
-      // loop-carried state so the recv loads of consecutive iterations
-      // overlap (the runs table is L1-resident).
-#pragma unroll 4
-      for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
-        const uint64_t e = e0 + i;
-        int j = sel.j;
-        while (j < A.nruns && A.runs[j].end <= e) ++j;
-        const bool in = j < A.nruns && A.runs[j].begin <= e;
-        const uint64_t src = in ? A.runs[j].dst + (e - A.runs[j].begin) : 0;
-        A.out[e] = in ? scale_of(A.recv[src], A.inv, A.mean) : T(0);
+      // Tiles that straddle a shard boundary: per element, all of a
+      // thread's recv loads issued before any use (coalesced across the
+      // warp), so the tile costs about one memory latency, not one per
+      // element.  The runs table is L1-resident.
+      constexpr int kPer = TE / kThreads;
+      static_assert(kPer <= 32, "selection mask is 32 bits");
+      T vals[kPer];
+      uint32_t hit = 0;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const uint32_t i = threadIdx.x + q * kThreads;
+        vals[q] = T(0);
+        if (i < n) {
+          const uint64_t e = e0 + i;
+          int j = sel.j;
+          while (j < A.nruns && A.runs[j].end <= e) ++j;
+          if (j < A.nruns && A.runs[j].begin <= e) {
+            vals[q] = A.recv[A.runs[j].dst + (e - A.runs[j].begin)];
+            hit |= 1u << q;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const uint32_t i = threadIdx.x + q * kThreads;
+        if (i < n) A.out[e0 + i] = ((hit >> q) & 1u) ? scale_of(vals[q], A.inv, A.mean) : T(0);
       }
       continue;
     }
     const int s = static_cast<int>(qc % kStagesK2);
     T* st = stage + (qc & 1) * TE;
+    if constexpr (COVAP_K2_STG != 0) {
+      mbar_wait(&bar[s], static_cast<uint32_t>((qc / kStagesK2) & 1));
+      const V* xv = reinterpret_cast<const V*>(in + s * TE);
+      V* ov = reinterpret_cast<V*>(A.out + e0);
+      for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
+        V x = xv[v];
+#pragma unroll
+        for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, A.mean);
+        ov[v] = x;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) produce_one();
+      ++qc;
+      continue;
+    }
     if (threadIdx.x == 0) bulk_wait_read<1>();
     mbar_wait(&bar[s], static_cast<uint32_t>((qc / kStagesK2) & 1));
     __syncthreads();

@@ -6,9 +6,10 @@ set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 declare -A V=(
   [g]=""
-  [h]="-DCOVAP_K1_TILE=16384 -DCOVAP_K1_CTAS=2"
-  [j]="-DCOVAP_K1_STAGES=3"
-  [k]="-DCOVAP_K1_TILE=12288 -DCOVAP_K1_STAGES=3 -DCOVAP_K1_CTAS=2"
+  [k1stg]="-DCOVAP_K1_STG=1 -DCOVAP_ZERO_BULK=0"
+  [k2stg]="-DCOVAP_K2_STG=1 -DCOVAP_ZERO_BULK=0"
+  [k2stg_zb]="-DCOVAP_K2_STG=1"
+  [bothstg3]="-DCOVAP_K1_STG=1 -DCOVAP_K2_STG=1 -DCOVAP_ZERO_BULK=0 -DCOVAP_K1_STAGES=3 -DCOVAP_K2_STAGES=6"
 )
 if [ "$1" = "build" ]; then
   for name in "${!V[@]}"; do
@@ -18,7 +19,7 @@ if [ "$1" = "build" ]; then
   done
   exit 0
 fi
-for name in ${NAMES:-g h j k}; do
+for name in ${NAMES:-g k1stg k2stg k2stg_zb bothstg3}; do
   lib=$ROOT/paper_2311_04499_b200/_variants/$name/libcovap_b200.so
   for cfg in "--layout resnet50 --interval 1" "--layout resnet50 --interval 4" "--layout vgg16 --interval 4" "--layout bert_large --interval 1" "--layout bert_large --interval 4"; do
     COVAP_LIB_PATH=$lib timeout 300 python $ROOT/bench.py $cfg --no-cpu-baseline --no-overhead --steps 30 --warmup 5 2>/dev/null | \
