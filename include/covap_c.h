@@ -140,6 +140,11 @@ covap_status covap_state_residual(covap_state* state, void** dev_ptr, uint64_t* 
 covap_status covap_state_send(covap_state* state, void** dev_ptr, uint64_t* capacity);
 covap_status covap_state_get_step(const covap_state* state, uint64_t* num_steps);
 covap_status covap_state_set_step(covap_state* state, uint64_t num_steps);
+/* With one rank (comm NULL or of size 1) the sync entry points run the fused
+ * K1F pass by default; fuse_single_rank = 0 makes them run K1 -> allreduce
+ * (NCCL over the 1-rank communicator when one is given) -> K2 instead, the
+ * exact multi-rank code path — used to test that path on one GPU. */
+covap_status covap_state_set_fused(covap_state* state, int fuse_single_rank);
 /* Zero the residual arena (stream-ordered). */
 covap_status covap_state_reset(covap_state* state, void* stream);
 

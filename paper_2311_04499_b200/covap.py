@@ -392,6 +392,10 @@ class CompressorState:
     def num_steps(self, v: int):
         L.lib().covap_state_set_step(self._h, int(v))
 
+    def set_fused(self, fuse_single_rank: bool):
+        """One rank: fused K1F pass (default) or the multi-rank K1 -> C1 -> K2 path."""
+        L.lib().covap_state_set_fused(self._h, 1 if fuse_single_rank else 0)
+
     def reset(self, stream=None):
         L.lib().covap_state_reset(self._h, _stream_ptr(stream, self.device))
 
@@ -576,11 +580,14 @@ class CovapSync:
     """
 
     def __init__(self, plan: BucketPlan, comm: Optional[Communicator] = None, dtype=None,
-                 device: int = 0, ef: Optional[EfSchedule] = None):
+                 device: int = 0, ef: Optional[EfSchedule] = None,
+                 fuse_single_rank: bool = True):
         self.plan = plan
         self.comm = comm
         self.state = CompressorState(plan, dtype, device, ef)
         self.device = device
+        if not fuse_single_rank:
+            self.state.set_fused(False)
 
     @property
     def world(self) -> int:

@@ -57,6 +57,7 @@ struct covap_state {
   cudaEvent_t done = nullptr;
   std::vector<cudaEvent_t> ready, arrive, end;  // per bucket
   std::vector<uint8_t> timed;                   // bucket had a collective in the last step
+  bool fuse_single_rank = true;                 // P = 1: run K1F instead of K1 -> C1 -> K2
 };
 
 namespace {
@@ -477,6 +478,13 @@ covap_status covap_state_set_step(covap_state* s, uint64_t num_steps) {
   });
 }
 
+covap_status covap_state_set_fused(covap_state* s, int fuse_single_rank) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    s->fuse_single_rank = fuse_single_rank != 0;
+  });
+}
+
 covap_status covap_state_reset(covap_state* s, void* stream) {
   return guarded([&] {
     need(s != nullptr, "NULL state");
@@ -552,13 +560,13 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
     const uint64_t n = s->plan.total;
     const auto& ph = phase_of(s->plan, s->num_steps);
     const int P = world(comm);
-    if (P == 1) {
+    if (P == 1 && s->fuse_single_rank) {
       // One rank: the allreduce is the identity, so K1 and K2 fuse into one
       // pass (K1F) that writes (0 + c) * 1 straight to the selected slots.
       k1f_range(s, grad, out, 1.0, 0, n, st);
     } else {
       k1_range(s, grad, nullptr, 0, n, st);
-      if (ph.send_elems > 0)
+      if (comm && ph.send_elems > 0)
         NK(ncclAllReduce(s->send, s->send, ph.send_elems, nccl_type(s->dtype), ncclSum,
                          comm->nccl, st));
       k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, 0, n, st);
@@ -597,7 +605,7 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
                          cudaMemcpyHostToDevice, s->h2d_stream));
       CK(cudaEventRecord(ein, s->h2d_stream));
       CK(cudaStreamWaitEvent(st, ein, 0));
-      if (P == 1) {
+      if (P == 1 && s->fuse_single_rank) {
         k1f_range(s, dev_grad, dev_out, 1.0, a, b, st);
       } else {
         k1_range(s, dev_grad, nullptr, a, b, st);
@@ -611,7 +619,7 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
           lo = std::min(lo, r.dst + (x0 - r.begin));
           hi = std::max(hi, r.dst + (x1 - r.begin));
         }
-        if (hi > lo)
+        if (comm && hi > lo)
           NK(ncclAllReduce(static_cast<char*>(s->send) + lo * es,
                            static_cast<char*>(s->send) + lo * es, hi - lo, nccl_type(s->dtype),
                            ncclSum, comm->nccl, st));
@@ -642,7 +650,7 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
     const auto& sel = phase_of(s->plan, s->num_steps).per_bucket[bucket];
     const uint64_t a = bk.begin, b = bk.begin + bk.numel;
     const int P = world(comm);
-    if (P == 1) {  // no exchange: the fused pass on the producing stream
+    if (P == 1 && s->fuse_single_rank) {  // no exchange: the fused pass on the producing stream
       k1f_range(s, grad, out, 1.0, a, b, st);
       s->timed[bucket] = 0;
       return;
@@ -653,7 +661,7 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
     const uint64_t len = sel.sel_end - sel.sel_begin;
     s->timed[bucket] = len > 0 ? 1 : 0;
     CK(cudaEventRecord(s->arrive[bucket], s->comm_stream));
-    if (P > 1 && len > 0)
+    if (comm && len > 0)
       NK(ncclAllReduce(static_cast<char*>(s->send) + sel.send_offset * s->esize,
                        static_cast<char*>(s->send) + sel.send_offset * s->esize, len,
                        nccl_type(s->dtype), ncclSum, comm->nccl, s->comm_stream));
@@ -678,7 +686,7 @@ covap_status covap_dense_bucket_ready(covap_state* s, covap_comm* comm, size_t b
     const int P = world(comm);
     s->timed[bucket] = 1;
     CK(cudaEventRecord(s->arrive[bucket], s->comm_stream));
-    if (P > 1)
+    if (comm)
       NK(ncclAllReduce(static_cast<char*>(grad) + a * s->esize,
                        static_cast<char*>(grad) + a * s->esize, bk.numel, nccl_type(s->dtype),
                        ncclSum, comm->nccl, s->comm_stream));
@@ -776,7 +784,7 @@ covap_status covap_comm_profile_exchange(covap_comm* c, const double* dur, size_
                                          double comp_ms, double* aligned_ms, double* comp_out) {
   return guarded([&] {
     need(dur && aligned_ms && comp_out, "NULL argument");
-    if (!c || c->nranks == 1) {
+    if (!c) {
       std::copy(dur, dur + n_coll, aligned_ms);
       *comp_out = comp_ms;
       return;

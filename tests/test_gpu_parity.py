@@ -355,3 +355,50 @@ def test_host_pipeline_equals_device_sync(covap, name, K, chunk):
         torch.cuda.synchronize()
         assert torch.equal(out.cpu(), hout)
         assert torch.equal(a.state.residuals, b.state.residuals)
+
+
+@pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 4), ("tablev", 19), ("bert_large", 2)])
+def test_multi_rank_code_path_on_one_gpu(covap, name, K):
+    """The K1 -> NCCL allreduce -> K2 path every P > 1 rank runs, exercised on
+    one GPU through a 1-rank NCCL communicator (fusion switched off): sync(),
+    the per-bucket overlapped schedule, the chunked host pipeline and the
+    dense path give exactly the fused single-rank results; the per-bucket
+    collective timings and the CCR exchange go through NCCL."""
+    comm = covap.Communicator(covap.Communicator.unique_id(), 1, 0, 0)
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    ref = covap.CovapSync(plan, None, torch.float32, 0)
+    a = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
+    b = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
+    c = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
+    d = plan.total_numel()
+    g = torch.empty(d, device=DEV)
+    o_ref, o_a, o_b = (torch.empty(d, device=DEV) for _ in range(3))
+    hin = torch.empty(d, pin_memory=True)
+    hout = torch.empty(d, pin_memory=True)
+    for s in range(K + 1):
+        covap.generate(g, covap.stream_key(33, 0, s))
+        hin.copy_(g)
+        ref.sync(g, o_ref)
+        a.sync(g, o_a)
+        for bk in range(len(plan.buckets)):
+            b.bucket_ready(bk, g, o_b)
+        b.finish()
+        c.sync_host(hin, hout, chunk_elems=1 << 20)
+        torch.cuda.synchronize()
+        for o in (o_a, o_b, hout.to(DEV)):
+            assert torch.equal(o, o_ref)
+        for st in (a, b, c):
+            assert torch.equal(st.state.residuals, ref.state.residuals)
+        durs = b.last_comm_ms()
+        for bk in range(len(plan.buckets)):
+            sel = plan.bucket_range(s, bk)
+            assert (durs[bk] >= 0) == (sel.sel_end > sel.sel_begin)
+    aligned, comp = comm.profile_exchange([1.5, 0.25, 3.0], 7.0)
+    assert aligned == [1.5, 0.25, 3.0] and comp == 7.0
+    dense = g.clone()
+    for bk in range(len(plan.buckets)):
+        a.dense_bucket_ready(bk, dense, dense)
+    a.finish()
+    torch.cuda.synchronize()
+    assert torch.equal(dense, g + 0.0)
+    comm.close()
