@@ -181,7 +181,8 @@ covap_status covap_sync_step(covap_state* state, covap_comm* comm, const void* g
                              void* stream);
 
 /* The same step on HOST buffers (pinned for overlap): the flat range is cut
- * into chunks (chunk_elems, 0 = 4 Mi elements); chunk c's H2D copy, its
+ * into chunks (chunk_elems; 0 = max(4 Mi, N/32) elements, ramped down to a
+ * quarter at both ends); chunk c's H2D copy, its
  * kernels (+ the allreduce of its slice of the send buffer) and its D2H copy
  * run on three streams, so PCIe traffic in both directions overlaps.
  * dev_grad / dev_out are device staging buffers of N elements (may alias). */

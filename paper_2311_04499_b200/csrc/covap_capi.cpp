@@ -587,18 +587,38 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
     cudaStream_t st = as_stream(stream);
     const uint64_t n = s->plan.total;
     const size_t es = s->esize;
-    // Chunks of a multiple of 8192 elements (32 KB fp32), at least 1 Mi.
-    uint64_t chunk = std::max<uint64_t>(chunk_elems ? chunk_elems : (4u << 20), 1u << 20);
+    // Chunk boundaries (multiples of 8192 elements): C-sized chunks in the
+    // middle, ramping C/4, C/2 at both ends so the first H2D and the last
+    // D2H — the parts no other copy overlaps — are short.
+    // Default C = max(4 Mi, N / 32): measured best for ResNet-50 (4 Mi) and
+    // BERT-large (~10 Mi) on B200 PCIe (profiles/r1_design_study.md).
+    uint64_t chunk = std::max<uint64_t>(
+        chunk_elems ? chunk_elems : std::max<uint64_t>(4u << 20, n / 32), 1u << 20);
     chunk = (chunk + 8191) / 8192 * 8192;
+    std::vector<uint64_t> cuts{0};
+    if (n >= 3 * chunk) {
+      const uint64_t q = chunk / 4 / 8192 * 8192, h = chunk / 2 / 8192 * 8192;
+      cuts.push_back(q);
+      cuts.push_back(q + h);
+      const uint64_t mid_end = n - q - h;
+      const uint64_t m = (mid_end - (q + h) + chunk - 1) / chunk;
+      for (uint64_t i = 1; i < m; ++i)
+        cuts.push_back((q + h) + ((mid_end - (q + h)) * i / m) / 8192 * 8192);
+      cuts.push_back(mid_end);
+      cuts.push_back(n - q);
+    } else {
+      for (uint64_t a = chunk; a < n; a += chunk) cuts.push_back(a);
+    }
+    cuts.push_back(n);
     const int P = world(comm);
     const auto& ph = phase_of(s->plan, s->num_steps);
     const double inv = 1.0 / static_cast<double>(P);
     // Step boundary: the copy streams start after everything already on `stream`.
     CK(cudaEventRecord(s->done, st));
     CK(cudaStreamWaitEvent(s->h2d_stream, s->done, 0));
-    uint64_t c = 0;
-    for (uint64_t a = 0; a < n; a += chunk, ++c) {
-      const uint64_t b = std::min(n, a + chunk);
+    for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+      const uint64_t a = cuts[c], b = cuts[c + 1];
+      if (b <= a) continue;
       cudaEvent_t ein = s->ev_in[c % kChunkEvents], ek = s->ev_k[c % kChunkEvents];
       CK(cudaMemcpyAsync(static_cast<char*>(dev_grad) + a * es,
                          static_cast<const char*>(host_grad) + a * es, (b - a) * es,
