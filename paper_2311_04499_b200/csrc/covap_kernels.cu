@@ -61,6 +61,9 @@ namespace {
 #ifndef COVAP_ZERO_BULK  // 1: zero streams are bulk stores of a zero tile; 0: 128-bit STG
 #define COVAP_ZERO_BULK 1
 #endif
+#ifndef COVAP_PDL  // programmatic dependent launch between consecutive sync kernels
+#define COVAP_PDL 1
+#endif
 #ifndef COVAP_K1_STG  // 1: K1 results leave by 128-bit STG from registers (no staging tiles)
 #define COVAP_K1_STG 0
 #endif
@@ -156,6 +159,15 @@ __device__ __forceinline__ void bulk_wait_all() {
 }
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Programmatic dependent launch: let the next kernel in the stream be
+// scheduled now (its CTAs take SMs as ours exit), and wait for the previous
+// kernel's memory before touching global data.  No-ops without PDL.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  if (COVAP_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() {
+  if (COVAP_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ------------------------------------------------------------ selection
@@ -295,9 +307,11 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
   T* zero = stage + 2 * TE;             // zero tile (COVAP_ZERO_BULK)
   __shared__ __align__(8) uint64_t bar[kStages];
 
+  pdl_launch_dependents();
   const uint64_t a16 = (A.a + W - 1) / W * W;
   const uint64_t b16 = A.b / W * W;
   if (a16 >= b16) {  // nothing vector-sized: element path only
+    pdl_wait();
     if (blockIdx.x == 0) {
       for (uint64_t e = A.a + threadIdx.x; e < A.b; e += blockDim.x) {
         int j = first_run_after(A.runs, A.nruns, e);
@@ -306,8 +320,6 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
     }
     return;
   }
-  if (blockIdx.x == 0) edges<T, OP>(A, a16, b16);
-
   const uint64_t ntiles = (b16 - a16 + TE - 1) / TE;
   const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (COVAP_ZERO_BULK)
@@ -318,6 +330,8 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
   }
   fence_async_smem();
   __syncthreads();
+  pdl_wait();  // the previous kernel's writes (r, out, ...) are visible from here
+  if (blockIdx.x == 0) edges<T, OP>(A, a16, b16);
 
   auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * TE; };
   auto issue = [&](uint64_t k) {  // thread 0 only
@@ -451,9 +465,11 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   T* zero = stage + 2 * TE;            // zero tile (COVAP_ZERO_BULK)
   __shared__ __align__(8) uint64_t bar[kStagesK2];
 
+  pdl_launch_dependents();
   const uint64_t a16 = (A.a + W - 1) / W * W;
   const uint64_t b16 = A.b / W * W;
   if (a16 >= b16) {
+    pdl_wait();
     if (blockIdx.x == 0)
       for (uint64_t e = A.a + threadIdx.x; e < A.b; e += blockDim.x) {
         int j = first_run_after(A.runs, A.nruns, e);
@@ -461,8 +477,6 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
       }
     return;
   }
-  if (blockIdx.x == 0) edges<T, 2>(A, a16, b16);
-
   const uint64_t ntiles = (b16 - a16 + TE - 1) / TE;
   const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (COVAP_ZERO_BULK)
@@ -473,6 +487,8 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   }
   fence_async_smem();
   __syncthreads();
+  pdl_wait();
+  if (blockIdx.x == 0) edges<T, 2>(A, a16, b16);
 
   auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * TE; };
   // Producer (thread 0): next tile to examine, next slot sequence number;
@@ -714,6 +730,24 @@ Args<T> make_args(const void* g, void* r, void* send, void* out, const void* rec
   return A;
 }
 
+// Launch with the programmatic-stream-serialization attribute (PDL) so the
+// kernel may start while the previous kernel in the stream drains.
+template <typename... KArgs, typename... Args2>
+cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, unsigned smem, cudaStream_t s,
+                   Args2&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = COVAP_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args2>(args)...);
+}
+
 }  // namespace
 
 cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, const Run* runs,
@@ -724,12 +758,12 @@ cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, co
   cudaError_t e = shape(&sh);
   if (e) return e;
   if (dtype == 0)
-    filter_kernel<float, 0><<<grid_for(b - a, 4, sh->sms * COVAP_K1_CTAS, kTileK1), kThreads, kSmemK1, s>>>(
-        make_args<float>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
+    e = launch(filter_kernel<float, 0>, grid_for(b - a, 4, sh->sms * COVAP_K1_CTAS, kTileK1), kSmemK1, s,
+               make_args<float>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
   else
-    filter_kernel<double, 0><<<grid_for(b - a, 8, sh->sms * COVAP_K1_CTAS, kTileK1), kThreads, kSmemK1, s>>>(
-        make_args<double>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
-  return cudaGetLastError();
+    e = launch(filter_kernel<double, 0>, grid_for(b - a, 8, sh->sms * COVAP_K1_CTAS, kTileK1), kSmemK1, s,
+               make_args<double>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, const Run* runs,
@@ -740,12 +774,12 @@ cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, c
   cudaError_t e = shape(&sh);
   if (e) return e;
   if (dtype == 0)
-    filter_kernel<float, 1><<<grid_for(b - a, 4, sh->sms * COVAP_K1_CTAS, kTileK1), kThreads, kSmemK1, s>>>(
-        make_args<float>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
+    e = launch(filter_kernel<float, 1>, grid_for(b - a, 4, sh->sms * COVAP_K1_CTAS, kTileK1), kSmemK1, s,
+               make_args<float>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
   else
-    filter_kernel<double, 1><<<grid_for(b - a, 8, sh->sms * COVAP_K1_CTAS, kTileK1), kThreads, kSmemK1, s>>>(
-        make_args<double>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
-  return cudaGetLastError();
+    e = launch(filter_kernel<double, 1>, grid_for(b - a, 8, sh->sms * COVAP_K1_CTAS, kTileK1), kSmemK1, s,
+               make_args<double>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
@@ -755,14 +789,14 @@ cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* run
   cudaError_t e = shape(&sh);
   if (e) return e;
   if (dtype == 0)
-    unpack_kernel<float><<<grid_for(b - a, 4, sh->sms, kTileK2), kThreads, kSmemK2, s>>>(
-        make_args<float>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
-                         mean));
+    e = launch(unpack_kernel<float>, grid_for(b - a, 4, sh->sms, kTileK2), kSmemK2, s,
+               make_args<float>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
+                                mean));
   else
-    unpack_kernel<double><<<grid_for(b - a, 8, sh->sms, kTileK2), kThreads, kSmemK2, s>>>(
-        make_args<double>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
-                          mean));
-  return cudaGetLastError();
+    e = launch(unpack_kernel<double>, grid_for(b - a, 8, sh->sms, kTileK2), kSmemK2, s,
+               make_args<double>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
+                                 mean));
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,

@@ -5,11 +5,8 @@
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 declare -A V=(
-  [g]=""
-  [k1stg]="-DCOVAP_K1_STG=1 -DCOVAP_ZERO_BULK=0"
-  [k2stg]="-DCOVAP_K2_STG=1 -DCOVAP_ZERO_BULK=0"
-  [k2stg_zb]="-DCOVAP_K2_STG=1"
-  [bothstg3]="-DCOVAP_K1_STG=1 -DCOVAP_K2_STG=1 -DCOVAP_ZERO_BULK=0 -DCOVAP_K1_STAGES=3 -DCOVAP_K2_STAGES=6"
+  [pdl]=""
+  [nopdl]="-DCOVAP_PDL=0"
 )
 if [ "$1" = "build" ]; then
   for name in "${!V[@]}"; do
@@ -19,7 +16,7 @@ if [ "$1" = "build" ]; then
   done
   exit 0
 fi
-for name in ${NAMES:-g k1stg k2stg k2stg_zb bothstg3}; do
+for name in ${NAMES:-pdl nopdl}; do
   lib=$ROOT/paper_2311_04499_b200/_variants/$name/libcovap_b200.so
   for cfg in "--layout resnet50 --interval 1" "--layout resnet50 --interval 4" "--layout vgg16 --interval 4" "--layout bert_large --interval 1" "--layout bert_large --interval 4"; do
     COVAP_LIB_PATH=$lib timeout 300 python $ROOT/bench.py $cfg --no-cpu-baseline --no-overhead --steps 30 --warmup 5 2>/dev/null | \
