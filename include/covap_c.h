@@ -70,13 +70,23 @@ typedef struct covap_plan_info {
   int32_t sharded;        /* shard_plan was applied (only when K > 1) */
   int32_t align;          /* send-buffer alignment quantum, elements */
   uint64_t max_send_elems;/* send-buffer capacity over all phases (with alignment gaps) */
+  uint64_t device_numel;  /* length of device-side arenas: N, or N + bucket padding */
+  int32_t padded;         /* COVAP_PLAN_PAD_BUCKETS was given */
 } covap_plan_info;
 
 typedef struct covap_bucket_range {
   uint64_t bucket_begin, bucket_end; /* flat [begin,end) of the bucket */
-  uint64_t sel_begin, sel_end;       /* selected sub-range this phase (empty: begin == end) */
+  uint64_t sel_begin, sel_end;       /* selected sub-range this phase, flat (empty: begin == end) */
   uint64_t send_offset;              /* element offset of sel_begin in the send buffer */
+  uint64_t device_begin;             /* offset of the bucket in device arenas */
 } covap_bucket_range;
+
+/* Plan flags.  COVAP_PLAN_PAD_BUCKETS: device-side arenas (gradient, residual,
+ * output) start every bucket on a 32-element boundary — the "device layout"
+ * — so a bucket held in its own 16-byte-aligned buffer (a DDP GradBucket)
+ * can be passed to the *_local entry points.  Flat coordinates (tensors,
+ * selection) are unchanged; device_numel gives the padded arena length. */
+enum { COVAP_PLAN_PAD_BUCKETS = 1 };
 
 const char* covap_last_error(void);
 int covap_version(void);
@@ -94,6 +104,9 @@ covap_status covap_device_count(int* count);
 covap_status covap_plan_create(const uint64_t* layer_numel, const uint32_t* bytes_per_param,
                                size_t n_layers, uint64_t cap_bytes, uint32_t interval, int rule,
                                int shard, covap_plan** out);
+covap_status covap_plan_create_ex(const uint64_t* layer_numel, const uint32_t* bytes_per_param,
+                                  size_t n_layers, uint64_t cap_bytes, uint32_t interval,
+                                  int rule, int shard, int flags, covap_plan** out);
 void covap_plan_destroy(covap_plan* plan);
 covap_status covap_plan_get_info(const covap_plan* plan, covap_plan_info* info);
 /* Bucket::numel / flat begin / first layer / layer count (model.hpp:34-39). */
@@ -193,11 +206,20 @@ covap_status covap_sync_step_host(covap_state* state, covap_comm* comm, const vo
 /* Overlapped schedule (the DDP-hook shape): bucket b's gradient is ready on
  * `stream` -> K1(b) on `stream`, event -> on the state's comm stream:
  * allreduce of b's selected range, K2(b); with one rank K1F(b) on `stream`.
+ * All device buffers passed to the state's entry points use the plan's
+ * device layout (covap_plan_info.device_numel elements).
  * covap_step_finish makes `stream` wait for the comm stream and advances the
  * step. */
 covap_status covap_bucket_ready(covap_state* state, covap_comm* comm, size_t bucket,
                                 const void* grad, void* out, void* stream);
 covap_status covap_step_finish(covap_state* state, void* stream);
+/* The same two calls with a bucket held in its own buffer (DDP GradBucket):
+ * bucket_grad / bucket_out point at the bucket's first element.  Needs a
+ * padded plan (COVAP_PLAN_PAD_BUCKETS). */
+covap_status covap_bucket_ready_local(covap_state* state, covap_comm* comm, size_t bucket,
+                                      const void* bucket_grad, void* bucket_out, void* stream);
+covap_status covap_dense_bucket_ready_local(covap_state* state, covap_comm* comm, size_t bucket,
+                                            void* bucket_grad, void* bucket_out, void* stream);
 /* Dense baseline (no compression, trainer.cpp:387-389): bucket b is
  * allreduced in place on the comm stream, then out = (0 + sum) * 1/P. */
 covap_status covap_dense_bucket_ready(covap_state* state, covap_comm* comm, size_t bucket,

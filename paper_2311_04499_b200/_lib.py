@@ -38,12 +38,12 @@ class PlanInfoC(ctypes.Structure):
     _fields_ = [("n_layers", u64), ("n_buckets", u64), ("n_tensors", u64), ("total_numel", u64),
                 ("twice_median", u64), ("interval", u32), ("rule", ctypes.c_int32),
                 ("sharded", ctypes.c_int32), ("align", ctypes.c_int32),
-                ("max_send_elems", u64)]
+                ("max_send_elems", u64), ("device_numel", u64), ("padded", ctypes.c_int32)]
 
 
 class BucketRangeC(ctypes.Structure):
     _fields_ = [("bucket_begin", u64), ("bucket_end", u64), ("sel_begin", u64),
-                ("sel_end", u64), ("send_offset", u64)]
+                ("sel_end", u64), ("send_offset", u64), ("device_begin", u64)]
 
 
 # name -> (restype, argtypes); restype None means covap_status (int) checked.
@@ -52,6 +52,7 @@ _SIGS = {
     "covap_version": (i32, []),
     "covap_device_count": (None, [ctypes.POINTER(i32)]),
     "covap_plan_create": (None, [u64p, u32p, sz, u64, u32, i32, i32, ctypes.POINTER(vp)]),
+    "covap_plan_create_ex": (None, [u64p, u32p, sz, u64, u32, i32, i32, i32, ctypes.POINTER(vp)]),
     "covap_plan_destroy": ("void", [vp]),
     "covap_plan_get_info": (None, [vp, ctypes.POINTER(PlanInfoC)]),
     "covap_plan_buckets": (None, [vp, u64p, u64p, u64p, u64p]),
@@ -81,6 +82,8 @@ _SIGS = {
     "covap_sync_step_host": (None, [vp, vp, vp, vp, vp, vp, u64, vp]),
     "covap_bucket_ready": (None, [vp, vp, sz, vp, vp, vp]),
     "covap_step_finish": (None, [vp, vp]),
+    "covap_bucket_ready_local": (None, [vp, vp, sz, vp, vp, vp]),
+    "covap_dense_bucket_ready_local": (None, [vp, vp, sz, vp, vp, vp]),
     "covap_dense_bucket_ready": (None, [vp, vp, sz, vp, vp, vp]),
     "covap_state_last_comm_ms": (None, [vp, f64p, sz]),
     "covap_comm_unique_id": (None, [ctypes.c_char_p]),

@@ -141,7 +141,7 @@ class BucketPlan:
     per-phase send layout.  ``interval``/``rule`` fix the selection phases."""
 
     def __init__(self, model: ModelSpec, cap_bytes: Optional[int] = None, interval: int = 1,
-                 rule: int = SelectionRule.kMatchStep, shard: int = -1):
+                 rule: int = SelectionRule.kMatchStep, shard: int = -1, pad: bool = False):
         lib = L.lib()
         self.model = model
         self.cap_bytes = int(model.bucket_cap_bytes if cap_bytes is None else cap_bytes)
@@ -150,8 +150,8 @@ class BucketPlan:
         h = ctypes.c_void_p()
         if int(interval) < 1:
             raise InvalidInput("shard interval must be >= 1")
-        lib.covap_plan_create(numel, bpp, len(model.layers), self.cap_bytes, int(interval), int(rule),
-                              int(shard), ctypes.byref(h))
+        lib.covap_plan_create_ex(numel, bpp, len(model.layers), self.cap_bytes, int(interval),
+                                 int(rule), int(shard), 1 if pad else 0, ctypes.byref(h))
         self._h = h
         info = L.PlanInfoC()
         lib.covap_plan_get_info(h, ctypes.byref(info))
@@ -197,6 +197,17 @@ class BucketPlan:
     def total_numel(self) -> int:
         return self.info.total_numel
 
+    def device_numel(self) -> int:
+        """Length of device-side arenas: N, plus bucket padding for a padded plan."""
+        return self.info.device_numel
+
+    @property
+    def padded(self) -> bool:
+        return bool(self.info.padded)
+
+    def device_begin(self, bucket: int) -> int:
+        return self.bucket_range(0, bucket).device_begin
+
     def selection(self, step: int) -> List[int]:
         keep = (ctypes.c_uint8 * len(self.tensors))()
         L.lib().covap_plan_selection(self._h, int(step), keep)
@@ -233,10 +244,11 @@ def shard_plan(plan: BucketPlan, interval: int, rule: int = SelectionRule.kMatch
     return BucketPlan(plan.model, plan.cap_bytes, interval=interval, rule=rule, shard=1)
 
 
-def plan_for(model: ModelSpec, config: CovapConfig) -> BucketPlan:
+def plan_for(model: ModelSpec, config: CovapConfig, pad: bool = False) -> BucketPlan:
     """The plan train() builds: allocate, then shard only when K > 1
-    (trainer.cpp:266-271)."""
-    return BucketPlan(model, None, interval=config.interval, rule=config.rule, shard=-1)
+    (trainer.cpp:266-271).  pad=True: the padded device layout the
+    bucket-local (DDP GradBucket) calls need."""
+    return BucketPlan(model, None, interval=config.interval, rule=config.rule, shard=-1, pad=pad)
 
 
 def effective_tensors(plan: BucketPlan) -> List[EffectiveTensor]:
@@ -433,7 +445,7 @@ class CompressorState:
     def _check(self, t):
         if t.dtype != self.dtype or not t.is_cuda or not t.is_contiguous():
             raise InvalidInput("tensor must be a contiguous CUDA tensor of the state's dtype")
-        if t.numel() != self.plan.total_numel():
+        if t.numel() != self.plan.device_numel():
             raise InvalidState("gradient length does not match the plan")
 
 
@@ -484,7 +496,7 @@ def covap_decompress(update: CompressedUpdate, out=None, recv=None, world: int =
     state = update.state
     torch = _torch()
     if out is None:
-        out = torch.empty(state.plan.total_numel(), dtype=state.dtype,
+        out = torch.empty(state.plan.device_numel(), dtype=state.dtype,
                           device=torch.device("cuda", state.device))
     saved = state.num_steps
     state.num_steps = update.step
@@ -607,7 +619,7 @@ class CovapSync:
         """The sync step on host (pinned) buffers: chunked H2D -> kernels (+
         allreduce) -> D2H on three streams (covap_sync_step_host)."""
         torch = _torch()
-        n = self.plan.total_numel()
+        n = self.plan.device_numel()
         if host_grad.numel() != n or host_out.numel() != n:
             raise InvalidState("host buffer length does not match the plan")
         if host_grad.dtype != self.state.dtype or host_out.dtype != self.state.dtype:
@@ -627,6 +639,17 @@ class CovapSync:
     def bucket_ready(self, bucket: int, grad, out, stream=None):
         L.lib().covap_bucket_ready(self.state.handle, self._c(), int(bucket), _ptr(grad), _ptr(out),
                                    _stream_ptr(stream, self.device))
+
+    def bucket_ready_local(self, bucket: int, bucket_grad, bucket_out, stream=None):
+        """bucket_ready() with the bucket in its own buffer (a DDP GradBucket);
+        needs a padded plan."""
+        L.lib().covap_bucket_ready_local(self.state.handle, self._c(), int(bucket), _ptr(bucket_grad),
+                                         _ptr(bucket_out), _stream_ptr(stream, self.device))
+
+    def dense_bucket_ready_local(self, bucket: int, bucket_grad, bucket_out, stream=None):
+        L.lib().covap_dense_bucket_ready_local(self.state.handle, self._c(), int(bucket),
+                                               _ptr(bucket_grad), _ptr(bucket_out),
+                                               _stream_ptr(stream, self.device))
 
     def dense_bucket_ready(self, bucket: int, grad, out, stream=None):
         L.lib().covap_dense_bucket_ready(self.state.handle, self._c(), int(bucket), _ptr(grad),

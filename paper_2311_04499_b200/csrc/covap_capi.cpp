@@ -216,13 +216,21 @@ covap_status covap_device_count(int* count) {
 covap_status covap_plan_create(const uint64_t* layer_numel, const uint32_t* bytes_per_param,
                                size_t n_layers, uint64_t cap_bytes, uint32_t interval, int rule,
                                int shard, covap_plan** out) {
+  return covap_plan_create_ex(layer_numel, bytes_per_param, n_layers, cap_bytes, interval, rule,
+                              shard, 0, out);
+}
+
+covap_status covap_plan_create_ex(const uint64_t* layer_numel, const uint32_t* bytes_per_param,
+                                  size_t n_layers, uint64_t cap_bytes, uint32_t interval,
+                                  int rule, int shard, int flags, covap_plan** out) {
   return guarded([&] {
     need(out != nullptr, "out must not be NULL");
     need(n_layers == 0 || layer_numel != nullptr, "layer_numel must not be NULL");
+    need((flags & ~COVAP_PLAN_PAD_BUCKETS) == 0, "unknown plan flag");
     auto* p = new covap_plan;
     try {
       p->p = covapb::build_plan(layer_numel, bytes_per_param, n_layers, cap_bytes, interval, rule,
-                                shard);
+                                shard, (flags & COVAP_PLAN_PAD_BUCKETS) != 0);
     } catch (...) {
       delete p;
       throw;
@@ -247,6 +255,8 @@ covap_status covap_plan_get_info(const covap_plan* plan, covap_plan_info* info) 
     info->sharded = p.sharded ? 1 : 0;
     info->align = static_cast<int32_t>(covapb::kSendAlign);
     info->max_send_elems = p.max_send;
+    info->device_numel = p.dtotal;
+    info->padded = p.padded ? 1 : 0;
   });
 }
 
@@ -294,9 +304,11 @@ covap_status covap_plan_bucket_range(const covap_plan* plan, uint64_t num_steps,
     const auto& sel = phase_of(plan->p, num_steps).per_bucket[bucket];
     out->bucket_begin = bk.begin;
     out->bucket_end = bk.begin + bk.numel;
-    out->sel_begin = sel.sel_begin;
-    out->sel_end = sel.sel_end;
+    // the selected range in flat coordinates (the planner keeps device ones)
+    out->sel_begin = sel.sel_end > sel.sel_begin ? sel.sel_begin - bk.dbegin + bk.begin : bk.begin;
+    out->sel_end = sel.sel_end > sel.sel_begin ? sel.sel_end - bk.dbegin + bk.begin : bk.begin;
     out->send_offset = sel.send_offset;
+    out->device_begin = bk.dbegin;
   });
 }
 
@@ -403,7 +415,7 @@ covap_status covap_state_create(const covap_plan* plan, int dtype, int device,
     s->esize = dtype == COVAP_F64 ? 8 : 4;
     s->device = device;
     if (ef) s->ef = *ef;
-    const uint64_t n = s->plan.total;
+    const uint64_t n = s->plan.dtotal;
     CK(cudaMalloc(&s->residual, std::max<uint64_t>(n, 1) * s->esize));
     CK(cudaMemset(s->residual, 0, std::max<uint64_t>(n, 1) * s->esize));
     s->send_cap = std::max<uint64_t>(s->plan.max_send, 1);
@@ -452,7 +464,7 @@ covap_status covap_state_residual(covap_state* s, void** dev_ptr, uint64_t* n) {
   return guarded([&] {
     need(s != nullptr, "NULL state");
     if (dev_ptr) *dev_ptr = s->residual;
-    if (n) *n = s->plan.total;
+    if (n) *n = s->plan.dtotal;
   });
 }
 
@@ -489,7 +501,7 @@ covap_status covap_state_reset(covap_state* s, void* stream) {
   return guarded([&] {
     need(s != nullptr, "NULL state");
     DeviceGuard dg(s->device);
-    CK(cudaMemsetAsync(s->residual, 0, std::max<uint64_t>(s->plan.total, 1) * s->esize,
+    CK(cudaMemsetAsync(s->residual, 0, std::max<uint64_t>(s->plan.dtotal, 1) * s->esize,
                        as_stream(stream)));
   });
 }
@@ -505,8 +517,8 @@ covap_status covap_filter_pack(covap_state* s, const void* grad, void* send, siz
     if (send) need_aligned(send, "send");
     if (b0 == b1) return;
     DeviceGuard dg(s->device);
-    const uint64_t a = s->plan.buckets[b0].begin;
-    const uint64_t b = s->plan.buckets[b1 - 1].begin + s->plan.buckets[b1 - 1].numel;
+    const uint64_t a = s->plan.buckets[b0].dbegin;
+    const uint64_t b = s->plan.buckets[b1 - 1].dbegin + s->plan.buckets[b1 - 1].numel;
     k1_range(s, grad, send, a, b, as_stream(stream));
   });
 }
@@ -520,8 +532,8 @@ covap_status covap_unpack(covap_state* s, const void* recv, void* out, double sc
     if (recv) need_aligned(recv, "recv");
     if (b0 == b1) return;
     DeviceGuard dg(s->device);
-    const uint64_t a = s->plan.buckets[b0].begin;
-    const uint64_t b = s->plan.buckets[b1 - 1].begin + s->plan.buckets[b1 - 1].numel;
+    const uint64_t a = s->plan.buckets[b0].dbegin;
+    const uint64_t b = s->plan.buckets[b1 - 1].dbegin + s->plan.buckets[b1 - 1].numel;
     k2_range(s, recv, out, scale, mean, a, b, as_stream(stream));
   });
 }
@@ -535,8 +547,8 @@ covap_status covap_filter_unpack(covap_state* s, const void* grad, void* out, do
     need_aligned(out, "out");
     if (b0 == b1) return;
     DeviceGuard dg(s->device);
-    const uint64_t a = s->plan.buckets[b0].begin;
-    const uint64_t b = s->plan.buckets[b1 - 1].begin + s->plan.buckets[b1 - 1].numel;
+    const uint64_t a = s->plan.buckets[b0].dbegin;
+    const uint64_t b = s->plan.buckets[b1 - 1].dbegin + s->plan.buckets[b1 - 1].numel;
     k1f_range(s, grad, out, scale, a, b, as_stream(stream));
   });
 }
@@ -557,7 +569,7 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
     if (comm) need(comm->device == s->device, "communicator and state are on different devices");
     DeviceGuard dg(s->device);
     cudaStream_t st = as_stream(stream);
-    const uint64_t n = s->plan.total;
+    const uint64_t n = s->plan.dtotal;
     const auto& ph = phase_of(s->plan, s->num_steps);
     const int P = world(comm);
     if (P == 1 && s->fuse_single_rank) {
@@ -585,7 +597,7 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
     if (comm) need(comm->device == s->device, "communicator and state are on different devices");
     DeviceGuard dg(s->device);
     cudaStream_t st = as_stream(stream);
-    const uint64_t n = s->plan.total;
+    const uint64_t n = s->plan.dtotal;
     const size_t es = s->esize;
     // Chunk boundaries (multiples of 8192 elements): C-sized chunks in the
     // middle, ramping C/4, C/2 at both ends so the first H2D and the last
@@ -668,7 +680,7 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
     cudaStream_t st = as_stream(stream);
     const auto& bk = s->plan.buckets[bucket];
     const auto& sel = phase_of(s->plan, s->num_steps).per_bucket[bucket];
-    const uint64_t a = bk.begin, b = bk.begin + bk.numel;
+    const uint64_t a = bk.dbegin, b = bk.dbegin + bk.numel;
     const int P = world(comm);
     if (P == 1 && s->fuse_single_rank) {  // no exchange: the fused pass on the producing stream
       k1f_range(s, grad, out, 1.0, a, b, st);
@@ -700,7 +712,7 @@ covap_status covap_dense_bucket_ready(covap_state* s, covap_comm* comm, size_t b
     DeviceGuard dg(s->device);
     cudaStream_t st = as_stream(stream);
     const auto& bk = s->plan.buckets[bucket];
-    const uint64_t a = bk.begin, b = bk.begin + bk.numel;
+    const uint64_t a = bk.dbegin, b = bk.dbegin + bk.numel;
     CK(cudaEventRecord(s->ready[bucket], st));
     CK(cudaStreamWaitEvent(s->comm_stream, s->ready[bucket], 0));
     const int P = world(comm);
@@ -715,6 +727,44 @@ covap_status covap_dense_bucket_ready(covap_state* s, covap_comm* comm, size_t b
     CK(covapb::launch_unpack(s->dtype, grad, out, s->d_full, 1, a, b,
                              1.0 / static_cast<double>(P), 1, s->comm_stream));
   });
+}
+
+namespace {
+// A bucket's own buffer stands for its slice [dbegin, dbegin + numel) of the
+// arena: the kernels only touch that slice, so the arena base is the buffer
+// address minus dbegin elements.  Needs a 16-byte-aligned dbegin (padded plan).
+covap_status local_bases(covap_state* s, size_t bucket, const void* g, const void* o,
+                         const char** gb, char** ob) {
+  return guarded([&] {
+    need(s && g && o, "NULL argument");
+    need(bucket < s->plan.buckets.size(), "bucket index out of range");
+    need_aligned(g, "bucket grad");
+    need_aligned(o, "bucket out");
+    const uint64_t off = s->plan.buckets[bucket].dbegin * s->esize;
+    if (off % 16 != 0)
+      throw covap::InvalidInput("bucket-local calls need a padded plan (COVAP_PLAN_PAD_BUCKETS)");
+    *gb = static_cast<const char*>(g) - off;
+    *ob = static_cast<char*>(const_cast<void*>(o)) - off;
+  });
+}
+}  // namespace
+
+covap_status covap_bucket_ready_local(covap_state* s, covap_comm* comm, size_t bucket,
+                                      const void* bucket_grad, void* bucket_out, void* stream) {
+  const char* g = nullptr;
+  char* o = nullptr;
+  const covap_status st = local_bases(s, bucket, bucket_grad, bucket_out, &g, &o);
+  if (st != COVAP_OK) return st;
+  return covap_bucket_ready(s, comm, bucket, g, o, stream);
+}
+
+covap_status covap_dense_bucket_ready_local(covap_state* s, covap_comm* comm, size_t bucket,
+                                            void* bucket_grad, void* bucket_out, void* stream) {
+  const char* g = nullptr;
+  char* o = nullptr;
+  const covap_status st = local_bases(s, bucket, bucket_grad, bucket_out, &g, &o);
+  if (st != COVAP_OK) return st;
+  return covap_dense_bucket_ready(s, comm, bucket, const_cast<char*>(g), o, stream);
 }
 
 covap_status covap_step_finish(covap_state* s, void* stream) {

@@ -56,7 +56,7 @@ uint32_t choose_interval(double ccr_value) {
 }
 
 Plan build_plan(const uint64_t* layer_numel, const uint32_t* bpp, size_t n_layers,
-                uint64_t cap_bytes, uint32_t interval, int rule, int shard) {
+                uint64_t cap_bytes, uint32_t interval, int rule, int shard, bool pad) {
   // ModelSpec::validate (model.cpp:24-34).
   if (n_layers == 0) throw covap::InvalidInput("model has no layers");
   for (size_t i = 0; i < n_layers; ++i) {
@@ -101,6 +101,18 @@ Plan build_plan(const uint64_t* layer_numel, const uint32_t* bpp, size_t n_layer
   plan.buckets.push_back(cur);
   plan.total = flat;
 
+  // Device coordinates: the flat layout, or with every bucket starting on a
+  // kSendAlign-element boundary (padded), so a bucket's own 16-byte-aligned
+  // buffer (a DDP GradBucket) can stand for its slice of the arena.
+  plan.padded = pad;
+  uint64_t dev = 0;
+  for (auto& b : plan.buckets) {
+    b.dbegin = dev;
+    dev += b.numel;
+    if (pad) dev = (dev + kSendAlign - 1) / kSendAlign * kSendAlign;
+  }
+  plan.dtotal = plan.buckets.back().dbegin + plan.buckets.back().numel;
+
   std::vector<uint64_t> sizes;
   for (const auto& b : plan.buckets) sizes.push_back(b.numel);
   plan.twice_median = median_twice(sizes);
@@ -118,7 +130,8 @@ Plan build_plan(const uint64_t* layer_numel, const uint32_t* bpp, size_t n_layer
     uint64_t off = 0;
     for (uint64_t p = 0; p < parts; ++p) {
       const uint64_t size = base + (p < extra ? 1 : 0);  // first numel%parts get +1
-      plan.tensors.push_back(PlanTensor{b, bk.begin + off, bk.begin + off + size});
+      plan.tensors.push_back(PlanTensor{b, bk.begin + off, bk.begin + off + size, bk.dbegin + off,
+                                        bk.dbegin + off + size});
       off += size;
     }
   }
@@ -133,20 +146,20 @@ Plan build_plan(const uint64_t* layer_numel, const uint32_t* bpp, size_t n_layer
     uint64_t cursor = 0;
     for (size_t t = 0; t < plan.tensors.size(); ++t) {
       if (!ph.keep[t]) continue;
-      const PlanTensor& ts = plan.tensors[t];
-      if (!ph.runs.empty() && ph.runs.back().end == ts.begin && t > 0 && ph.keep[t - 1]) {
-        ph.runs.back().end = ts.end;  // extend the run: contiguous in flat and in send
+      const PlanTensor& ts = plan.tensors[t];  // runs live in device coordinates
+      if (!ph.runs.empty() && ph.runs.back().end == ts.dbegin && t > 0 && ph.keep[t - 1]) {
+        ph.runs.back().end = ts.dend;  // extend the run: contiguous in the arena and in send
       } else {
-        const uint64_t dst = cursor + ((ts.begin + kSendAlign - cursor % kSendAlign) % kSendAlign);
-        ph.runs.push_back(Run{ts.begin, ts.end, dst});
+        const uint64_t dst = cursor + ((ts.dbegin + kSendAlign - cursor % kSendAlign) % kSendAlign);
+        ph.runs.push_back(Run{ts.dbegin, ts.dend, dst});
       }
       cursor = ph.runs.back().dst + (ph.runs.back().end - ph.runs.back().begin);
       ph.payload_elems += ts.end - ts.begin;
       BucketSel& bs = ph.per_bucket[ts.bucket];
-      const uint64_t off = ph.runs.back().dst + (ts.begin - ph.runs.back().begin);
+      const uint64_t off = ph.runs.back().dst + (ts.dbegin - ph.runs.back().begin);
       if (bs.sel_end == bs.sel_begin) {
-        bs.sel_begin = ts.begin;
-        bs.sel_end = ts.end;
+        bs.sel_begin = ts.dbegin;
+        bs.sel_end = ts.dend;
         bs.send_offset = off;
       } else {
         // Shards of one bucket are <= K consecutive indices, so at most one

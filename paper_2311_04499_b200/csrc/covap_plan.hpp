@@ -18,7 +18,8 @@ namespace covapb {
 
 struct PlanBucket {
   uint64_t numel = 0;
-  uint64_t begin = 0;  // flat element offset
+  uint64_t begin = 0;   // flat element offset
+  uint64_t dbegin = 0;  // device offset (== begin unless the plan is padded)
   uint64_t bytes = 0;
   uint64_t first_layer = 0;
   uint64_t n_layers = 0;
@@ -26,18 +27,20 @@ struct PlanBucket {
 
 struct PlanTensor {
   uint64_t bucket = 0;
-  uint64_t begin = 0;
+  uint64_t begin = 0;  // flat
   uint64_t end = 0;
+  uint64_t dbegin = 0;  // device
+  uint64_t dend = 0;
 };
 
 struct BucketSel {
-  uint64_t sel_begin = 0, sel_end = 0;  // empty when equal
+  uint64_t sel_begin = 0, sel_end = 0;  // device coordinates; empty when equal
   uint64_t send_offset = 0;
 };
 
 struct Phase {
   std::vector<uint8_t> keep;          // per effective tensor
-  std::vector<Run> runs;              // maximal runs of selected tensors
+  std::vector<Run> runs;              // maximal runs of selected tensors (device coords)
   std::vector<BucketSel> per_bucket;  // at most one selected range per bucket
   uint64_t send_elems = 0;            // send-buffer length incl. alignment gaps
   uint64_t payload_elems = 0;         // sum of selected numels
@@ -48,7 +51,9 @@ struct Plan {
   std::vector<PlanBucket> buckets;
   std::vector<PlanTensor> tensors;
   uint64_t twice_median = 0;
-  uint64_t total = 0;
+  uint64_t total = 0;   // N
+  uint64_t dtotal = 0;  // device arena length (N plus bucket padding)
+  bool padded = false;
   uint32_t interval = 1;
   int rule = 0;
   bool sharded = false;
@@ -58,7 +63,7 @@ struct Plan {
 
 // Throws covap::InvalidInput exactly where the reference does.
 Plan build_plan(const uint64_t* layer_numel, const uint32_t* bytes_per_param, size_t n_layers,
-                uint64_t cap_bytes, uint32_t interval, int rule, int shard);
+                uint64_t cap_bytes, uint32_t interval, int rule, int shard, bool pad = false);
 
 uint64_t median_twice(std::vector<uint64_t> sizes);                       // model.cpp:66-82
 std::vector<uint8_t> select(uint64_t step, uint32_t interval, size_t count, int rule);
