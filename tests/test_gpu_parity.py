@@ -402,3 +402,37 @@ def test_multi_rank_code_path_on_one_gpu(covap, name, K):
     torch.cuda.synchronize()
     assert torch.equal(dense, g + 0.0)
     comm.close()
+
+
+@pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 3)])
+def test_padded_plan_equals_flat(covap, name, K):
+    """A padded plan on a padded arena gives the flat plan's results, element
+    for element, through sync() and through the bucket-local entry points."""
+    m = covap.load_layout(name)
+    fp = covap.plan_for(m, covap.CovapConfig(interval=K))
+    pp = covap.plan_for(m, covap.CovapConfig(interval=K), pad=True)
+    a = covap.CovapSync(fp, None, torch.float32, 0)
+    b = covap.CovapSync(pp, None, torch.float32, 0)
+    c = covap.CovapSync(pp, None, torch.float32, 0)
+    n, dn = fp.total_numel(), pp.device_numel()
+    idx = torch.cat([torch.arange(pp.device_begin(i), pp.device_begin(i) + bk.numel)
+                     for i, bk in enumerate(pp.buckets)]).to(DEV)
+    g = torch.empty(n, device=DEV)
+    oa = torch.empty(n, device=DEV)
+    gp = torch.zeros(dn, device=DEV)
+    ob = torch.empty(dn, device=DEV)
+    for s in range(K + 1):
+        covap.generate(g, covap.stream_key(44, 0, s))
+        gp[idx] = g
+        a.sync(g, oa)
+        b.sync(gp, ob)
+        bufs = [g[fp.buckets[i].begin:fp.buckets[i].begin + bk.numel].clone()
+                for i, bk in enumerate(pp.buckets)]
+        for i, buf in enumerate(bufs):
+            c.bucket_ready_local(i, buf, buf)
+        c.finish()
+        torch.cuda.synchronize()
+        assert torch.equal(ob[idx], oa)
+        assert torch.equal(torch.cat(bufs), oa)
+        assert torch.equal(b.state.residuals[idx], a.state.residuals)
+        assert torch.equal(c.state.residuals[idx], a.state.residuals)

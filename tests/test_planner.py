@@ -161,3 +161,31 @@ def test_send_layout_invariants(covap, name, K, rule):
         assert send_elems - payload <= align * len(spans)
     assert np.all(seen == 1)
     assert total_payload == p.total_numel()
+
+
+@pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 4), ("bert_large", 3), ("tablev", 19)])
+def test_padded_device_layout(covap, name, K):
+    """COVAP_PLAN_PAD_BUCKETS: flat coordinates (tensors, selection, payload
+    sizes) are those of the unpadded plan; device offsets start every bucket
+    on a 32-element boundary; send offsets stay vector-aligned."""
+    m = covap.load_layout(name)
+    flat = covap.plan_for(m, covap.CovapConfig(interval=K))
+    pad = covap.plan_for(m, covap.CovapConfig(interval=K), pad=True)
+    assert not flat.padded and pad.padded
+    assert [(t.bucket, t.begin, t.end) for t in pad.tensors] == \
+        [(t.bucket, t.begin, t.end) for t in flat.tensors]
+    assert flat.device_numel() == flat.total_numel()
+    dev = 0
+    for b, bk in enumerate(pad.buckets):
+        assert pad.device_begin(b) == dev and dev % 32 == 0
+        dev = (dev + bk.numel + 31) // 32 * 32
+    assert pad.device_numel() == pad.device_begin(len(pad.buckets) - 1) + pad.buckets[-1].numel
+    for s in range(K):
+        assert pad.selection(s) == flat.selection(s)
+        assert pad.send_elems(s)[1] == flat.send_elems(s)[1]
+        for b in range(len(pad.buckets)):
+            br, bf = pad.bucket_range(s, b), flat.bucket_range(s, b)
+            assert (br.sel_begin, br.sel_end) == (bf.sel_begin, bf.sel_end)
+            if br.sel_end > br.sel_begin:
+                dev_sel = br.sel_begin - br.bucket_begin + br.device_begin
+                assert br.send_offset % 32 == dev_sel % 32
