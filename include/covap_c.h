@@ -245,6 +245,28 @@ covap_status covap_allreduce(covap_comm* comm, void* buf, uint64_t count, int dt
 covap_status covap_comm_profile_exchange(covap_comm* comm, const double* dur, size_t n_coll,
                                          double comp_ms, double* aligned_ms, double* comp_out);
 
+/* ------------------------------------------- peer (NVLink) collective -- */
+/* C1 as one load/store kernel over peer memory instead of NCCL: two send
+ * buffers (step parity) and a flag block per rank, shared through CUDA IPC
+ * (covap_peer_export on every rank, gather the blobs, covap_peer_import) or,
+ * for ranks of one process, covap_peer_attach_local.  The sum runs in rank
+ * order, ((0 + v_0) + v_1) + ..., so results equal allreduce_mean
+ * (trainer.cpp:41-43) bit for bit for any P.  Spin-waits are bounded;
+ * covap_peer_check reports a timeout as COVAP_ERR_GENERIC. */
+typedef struct covap_peer covap_peer;
+covap_status covap_peer_create(covap_state* state, int nranks, int rank, covap_peer** out);
+void covap_peer_destroy(covap_peer* peer);
+covap_status covap_peer_export(covap_peer* peer, uint8_t* blob, size_t cap, size_t* len);
+covap_status covap_peer_import(covap_peer* peer, const uint8_t* blobs, size_t len);
+covap_status covap_peer_attach_local(covap_peer** peers, int nranks);
+/* max_ctas: cap the collective's grid (0 = one CTA per SM); timeout_s: bound
+ * of every spin-wait (0 = keep). */
+covap_status covap_peer_set_limits(covap_peer* peer, int max_ctas, double timeout_s);
+covap_status covap_peer_check(covap_peer* peer);
+/* K1 into the parity buffer -> peer allreduce -> K2 (x 1/P) -> ++step. */
+covap_status covap_peer_sync_step(covap_state* state, covap_peer* peer, const void* grad,
+                                  void* out, void* stream);
+
 /* ------------------------------------------- memory and generic kernels -- */
 /* Used by the C++ value-semantics layer (include/covap/b200_api.hpp) so it
  * needs no CUDA headers.  kind: 0 = host->device, 1 = device->host,

@@ -92,6 +92,14 @@ _SIGS = {
     "covap_comm_size": (None, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
     "covap_allreduce": (None, [vp, vp, u64, i32, vp]),
     "covap_comm_profile_exchange": (None, [vp, f64p, sz, f64, f64p, f64p]),
+    "covap_peer_create": (None, [vp, i32, i32, ctypes.POINTER(vp)]),
+    "covap_peer_destroy": ("void", [vp]),
+    "covap_peer_export": (None, [vp, ctypes.c_char_p, sz, ctypes.POINTER(sz)]),
+    "covap_peer_import": (None, [vp, ctypes.c_char_p, sz]),
+    "covap_peer_attach_local": (None, [ctypes.POINTER(vp), i32]),
+    "covap_peer_set_limits": (None, [vp, i32, f64]),
+    "covap_peer_check": (None, [vp]),
+    "covap_peer_sync_step": (None, [vp, vp, vp, vp, vp]),
     "covap_device_alloc": (None, [i32, u64, ctypes.POINTER(vp)]),
     "covap_device_free": (None, [i32, vp]),
     "covap_memcpy": (None, [vp, vp, u64, i32, vp]),

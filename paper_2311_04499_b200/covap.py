@@ -734,3 +734,68 @@ class CcrController:
         comm = float(sum(aligned))
         c = ccr(comm, comp0)
         return ProfileResult(c, comp0, comm, list(durs), choose_interval(c))
+
+
+# ------------------------------------------------------------ peer collective
+
+class PeerGroup:
+    """C1 as a load/store collective over NVLink peer memory (covap_peer_*):
+    the rank-ordered allreduce of the packed send buffers, bit-identical to
+    allreduce_mean (trainer.cpp:41-43) for any P.  Rendezvous: every rank
+    calls ``export()``, the blobs are gathered (torch.distributed), every
+    rank calls ``import_(blobs)``; ranks of one process use ``attach_local``."""
+
+    def __init__(self, state: CompressorState, nranks: int, rank: int):
+        h = ctypes.c_void_p()
+        L.lib().covap_peer_create(state.handle, int(nranks), int(rank), ctypes.byref(h))
+        self._h = h
+        self.state = state
+        self.nranks, self.rank = int(nranks), int(rank)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and L._LIB is not None:
+            L._LIB.covap_peer_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def export(self) -> bytes:
+        n = ctypes.c_size_t()
+        L.lib().covap_peer_export(self._h, None, 0, ctypes.byref(n))
+        buf = ctypes.create_string_buffer(n.value)
+        L.lib().covap_peer_export(self._h, buf, n.value, ctypes.byref(n))
+        return buf.raw
+
+    def import_(self, blobs: Sequence[bytes]):
+        blob = b"".join(blobs)
+        L.lib().covap_peer_import(self._h, blob, len(blobs[0]))
+
+    @staticmethod
+    def attach_local(groups: Sequence["PeerGroup"]):
+        arr = (ctypes.c_void_p * len(groups))(*[g.handle.value for g in groups])
+        L.lib().covap_peer_attach_local(arr, len(groups))
+
+    @staticmethod
+    def from_torch_distributed(state: CompressorState) -> "PeerGroup":
+        import torch.distributed as dist
+        g = PeerGroup(state, dist.get_world_size(), dist.get_rank())
+        blobs = [None] * dist.get_world_size()
+        dist.all_gather_object(blobs, g.export())
+        g.import_(blobs)
+        return g
+
+    def set_limits(self, max_ctas: int = 0, timeout_s: float = 0.0):
+        L.lib().covap_peer_set_limits(self._h, int(max_ctas), float(timeout_s))
+
+    def check(self):
+        L.lib().covap_peer_check(self._h)
+
+    def sync(self, grad, out, stream=None):
+        """K1 -> peer allreduce (rank order) -> K2 x 1/P -> ++step."""
+        self.state._check(grad)
+        self.state._check(out)
+        L.lib().covap_peer_sync_step(self.state.handle, self._h, _ptr(grad), _ptr(out),
+                                     _stream_ptr(stream, self.state.device))

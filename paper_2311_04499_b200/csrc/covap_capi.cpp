@@ -981,3 +981,189 @@ covap_status covap_spin(double us, int blocks, void* stream) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- peer collective
+//
+// C1 as one load/store kernel over NVLink peer memory (covap_peer.cu): the
+// packed send buffers live in memory every rank can address — CUDA IPC
+// between processes, plain device pointers within one process — and the
+// allreduce sums them in rank order.
+
+struct covap_peer {
+  int device = 0;
+  int P = 1, rank = 0;
+  uint64_t cap = 0;                 // send-buffer capacity, elements
+  size_t esize = 4;
+  void* bufs[2] = {nullptr, nullptr};  // my send buffers (step parity)
+  uint64_t* flags = nullptr;           // my flag block
+  unsigned* counter = nullptr;
+  int* err = nullptr;
+  void* peer_bufs[2][covapb::kMaxPeers] = {};
+  uint64_t* peer_flags[covapb::kMaxPeers] = {};
+  std::vector<void*> opened;  // IPC mappings to close
+  uint64_t epoch = 0;
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s
+  int max_ctas = 0;
+  bool attached = false;
+};
+
+extern "C" {
+
+covap_status covap_peer_create(covap_state* s, int nranks, int rank, covap_peer** out) {
+  covap_peer* p = nullptr;
+  const covap_status st = guarded([&] {
+    need(s && out, "NULL argument");
+    need(nranks >= 1 && nranks <= covapb::kMaxPeers && rank >= 0 && rank < nranks,
+         "peer collective supports 1..8 ranks");
+    DeviceGuard dg(s->device);
+    p = new covap_peer;
+    p->device = s->device;
+    p->P = nranks;
+    p->rank = rank;
+    p->esize = s->esize;
+    p->cap = s->send_cap + 64;  // room for the last vector
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaMalloc(&p->bufs[k], p->cap * p->esize));
+      CK(cudaMemset(p->bufs[k], 0, p->cap * p->esize));  // alignment gaps stay zero
+    }
+    CK(cudaMalloc(reinterpret_cast<void**>(&p->flags), 2 * covapb::kMaxPeers * sizeof(uint64_t)));
+    CK(cudaMemset(p->flags, 0, 2 * covapb::kMaxPeers * sizeof(uint64_t)));
+    CK(cudaMalloc(reinterpret_cast<void**>(&p->counter), sizeof(unsigned)));
+    CK(cudaMemset(p->counter, 0, sizeof(unsigned)));
+    CK(cudaMalloc(reinterpret_cast<void**>(&p->err), sizeof(int)));
+    CK(cudaMemset(p->err, 0, sizeof(int)));
+    for (int k = 0; k < 2; ++k) p->peer_bufs[k][rank] = p->bufs[k];
+    p->peer_flags[rank] = p->flags;
+    *out = p;
+  });
+  if (st != COVAP_OK && p) covap_peer_destroy(p);
+  return st;
+}
+
+void covap_peer_destroy(covap_peer* p) {
+  if (!p) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  for (void* q : p->opened) cudaIpcCloseMemHandle(q);
+  cudaFree(p->bufs[0]);
+  cudaFree(p->bufs[1]);
+  cudaFree(p->flags);
+  cudaFree(p->counter);
+  cudaFree(p->err);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete p;
+}
+
+covap_status covap_peer_export(covap_peer* p, uint8_t* blob, size_t cap, size_t* len) {
+  return guarded([&] {
+    need(p && len, "NULL argument");
+    constexpr size_t h = sizeof(cudaIpcMemHandle_t);
+    *len = 3 * h;
+    if (!blob) return;
+    need(cap >= 3 * h, "blob too small");
+    DeviceGuard dg(p->device);
+    cudaIpcMemHandle_t hs[3];
+    CK(cudaIpcGetMemHandle(&hs[0], p->bufs[0]));
+    CK(cudaIpcGetMemHandle(&hs[1], p->bufs[1]));
+    CK(cudaIpcGetMemHandle(&hs[2], p->flags));
+    std::memcpy(blob, hs, 3 * h);
+  });
+}
+
+covap_status covap_peer_import(covap_peer* p, const uint8_t* blobs, size_t len) {
+  return guarded([&] {
+    need(p && blobs, "NULL argument");
+    constexpr size_t h = sizeof(cudaIpcMemHandle_t);
+    need(len == 3 * h, "blob length mismatch");
+    DeviceGuard dg(p->device);
+    for (int q = 0; q < p->P; ++q) {
+      if (q == p->rank) continue;
+      cudaIpcMemHandle_t hs[3];
+      std::memcpy(hs, blobs + q * len, 3 * h);
+      void* ptr[3];
+      for (int k = 0; k < 3; ++k) {
+        CK(cudaIpcOpenMemHandle(&ptr[k], hs[k], cudaIpcMemLazyEnablePeerAccess));
+        p->opened.push_back(ptr[k]);
+      }
+      p->peer_bufs[0][q] = ptr[0];
+      p->peer_bufs[1][q] = ptr[1];
+      p->peer_flags[q] = static_cast<uint64_t*>(ptr[2]);
+    }
+    p->attached = true;
+  });
+}
+
+covap_status covap_peer_attach_local(covap_peer** peers, int nranks) {
+  return guarded([&] {
+    need(peers != nullptr && nranks >= 1 && nranks <= covapb::kMaxPeers, "bad peer list");
+    for (int i = 0; i < nranks; ++i) {
+      need(peers[i] && peers[i]->P == nranks && peers[i]->rank == i, "peer i must be rank i");
+    }
+    for (int i = 0; i < nranks; ++i) {
+      for (int q = 0; q < nranks; ++q) {
+        peers[i]->peer_bufs[0][q] = peers[q]->bufs[0];
+        peers[i]->peer_bufs[1][q] = peers[q]->bufs[1];
+        peers[i]->peer_flags[q] = peers[q]->flags;
+      }
+      peers[i]->attached = true;
+    }
+  });
+}
+
+covap_status covap_peer_set_limits(covap_peer* p, int max_ctas, double timeout_s) {
+  return guarded([&] {
+    need(p != nullptr, "NULL peer");
+    p->max_ctas = max_ctas;
+    if (timeout_s > 0) p->timeout_ns = static_cast<uint64_t>(timeout_s * 1e9);
+  });
+}
+
+covap_status covap_peer_check(covap_peer* p) {
+  return guarded([&] {
+    need(p != nullptr, "NULL peer");
+    DeviceGuard dg(p->device);
+    int err = 0;
+    CK(cudaMemcpy(&err, p->err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) throw covap::Error("peer collective timed out waiting for a rank");
+  });
+}
+
+covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* grad, void* out,
+                                  void* stream) {
+  return guarded([&] {
+    need(s && p && grad && out, "NULL argument");
+    need(p->attached || p->P == 1, "peer buffers are not attached (covap_peer_import)");
+    need(p->device == s->device && p->esize == s->esize, "peer and state differ");
+    need_aligned(grad, "grad");
+    need_aligned(out, "out");
+    DeviceGuard dg(s->device);
+    cudaStream_t st = as_stream(stream);
+    const uint64_t n = s->plan.dtotal;
+    const auto& ph = phase_of(s->plan, s->num_steps);
+    const int par = static_cast<int>(s->num_steps & 1);
+    void* buf = p->bufs[par];
+    k1_range(s, grad, buf, 0, n, st);
+    ++p->epoch;
+    if (ph.send_elems > 0) {
+      covapb::PeerArgs a{};
+      for (int q = 0; q < p->P; ++q) {
+        a.bufs[q] = p->peer_bufs[par][q];
+        a.flags[q] = p->peer_flags[q];
+      }
+      a.counter = p->counter;
+      a.err = p->err;
+      a.epoch = p->epoch;
+      a.len = ph.send_elems;
+      a.timeout_ns = p->timeout_ns;
+      a.P = p->P;
+      a.rank = p->rank;
+      CK(covapb::launch_peer_allreduce(s->dtype, a, p->max_ctas, st));
+    }
+    k2_range(s, buf, out, 1.0 / static_cast<double>(p->P), 1, 0, n, st);
+    ++s->num_steps;
+  });
+}
+
+}  // extern "C"

@@ -46,4 +46,21 @@ cudaError_t launch_spin(double us, int blocks, cudaStream_t s);
 
 uint64_t stream_key(uint64_t seed, uint64_t rank, uint64_t step);
 
+// Peer (NVLink load/store) allreduce of the packed send buffers, rank-ordered
+// (covap_peer.cu).  flags[p] is rank p's flag block: kMaxPeers uint64 per
+// phase, 2 phases.
+constexpr int kMaxPeers = 8;
+struct PeerArgs {
+  void* bufs[kMaxPeers];       // every rank's send buffer for this step
+  uint64_t* flags[kMaxPeers];  // every rank's flag block
+  unsigned* counter;           // this rank's grid-barrier counter
+  int* err;                    // this rank's error flag (timeout)
+  uint64_t epoch;              // monotonically increasing per collective
+  uint64_t len;                // elements
+  uint64_t timeout_ns;
+  int P;
+  int rank;
+};
+cudaError_t launch_peer_allreduce(int dtype, const PeerArgs& args, int max_ctas, cudaStream_t s);
+
 }  // namespace covapb

@@ -436,3 +436,75 @@ def test_padded_plan_equals_flat(covap, name, K):
         assert torch.equal(torch.cat(bufs), oa)
         assert torch.equal(b.state.residuals[idx], a.state.residuals)
         assert torch.equal(c.state.residuals[idx], a.state.residuals)
+
+
+def _virtual_ranks(covap, plan, P, dtype, ef):
+    """P ranks of the peer collective inside one process on one GPU: each has
+    its own state and send buffers, its kernels run on its own stream, and
+    the grids are capped so all P collectives are resident together."""
+    states = [covap.CompressorState(plan, dtype, 0, ef) for _ in range(P)]
+    groups = [covap.PeerGroup(st, P, r) for r, st in enumerate(states)]
+    covap.PeerGroup.attach_local(groups)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    for g in groups:
+        g.set_limits(max_ctas=max(1, sms // (2 * P)), timeout_s=10.0)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    return states, groups, streams
+
+
+@pytest.mark.parametrize("case", manifest()["session"], ids=lambda c: c["name"])
+def test_peer_collective_bit_exact_vs_reference(covap, orc, case):
+    """The NVLink load/store allreduce sums in rank order, so the whole
+    P-worker step equals the reference's (trainer.cpp:365-386) bit for bit —
+    for P = 2, 3 and 4 (fp64 fixtures from the reference library)."""
+    fx = np.load(os.path.join(GOLDEN, f"session_{case['name']}.npz"))
+    plan = covap.BucketPlan(mk_model(covap, case["sizes"], case["cap"]), interval=case["K"],
+                            rule=case["rule"])
+    en, init, asc, rng = case["ef"]
+    P = case["P"]
+    states, groups, streams = _virtual_ranks(covap, plan, P, torch.float64,
+                                             covap.EfSchedule(bool(en), init, asc, rng))
+    d = plan.total_numel()
+    outs = [torch.empty(d, dtype=torch.float64, device=DEV) for _ in range(P)]
+    for s in range(case["steps"]):
+        grads = [dev_gen(covap, orc.stream_key(case["seed"], w, s), d, case["kind"], torch.float64)
+                 for w in range(P)]
+        torch.cuda.synchronize()
+        for w in range(P):
+            groups[w].sync(grads[w], outs[w], streams[w])
+        torch.cuda.synchronize()
+        for g in groups:
+            g.check()
+        for w in range(P):
+            assert np.array_equal(bits(outs[w].cpu().numpy()), bits(fx[f"update_{s}"])), (s, w)
+        assert np.array_equal(bits(states[0].residuals.cpu().numpy()), bits(fx[f"residual0_{s}"]))
+
+
+@pytest.mark.parametrize("name,K,P", [("resnet50", 4, 2), ("vgg16", 4, 4), ("resnet50", 1, 8)])
+def test_peer_collective_fp32_full_layouts(covap, orc, name, K, P):
+    """fp32 at BASELINE sizes, P virtual ranks: every rank's synchronised
+    gradient equals the rank-ordered oracle mean, bit for bit."""
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    ef = covap.EfSchedule(True, 0.3, 1, 0.2)
+    states, groups, streams = _virtual_ranks(covap, plan, P, torch.float32, ef)
+    d = plan.total_numel()
+    tensors = [(t.bucket, t.begin, t.end) for t in plan.tensors]
+    rs = [np.zeros(d, np.float32) for _ in range(P)]
+    outs = [torch.empty(d, device=DEV) for _ in range(P)]
+    for s in range(2):
+        keys = [orc.stream_key(9, w, s) for w in range(P)]
+        grads = [dev_gen(covap, k, d, 0, torch.float32) for k in keys]
+        torch.cuda.synchronize()
+        for w in range(P):
+            groups[w].sync(grads[w], outs[w], streams[w])
+        keep = orc.select(s, K, len(tensors))
+        coeff = np.float32(orc.ef_coefficient(s, 0.3, 1, 0.2))
+        pays = [orc.compress(orc.generate(keys[w], d, 0, 0, np.float32), rs[w], tensors, keep, 1, coeff)
+                for w in range(P)]
+        want = orc.decompress(orc.allreduce_mean(np.stack(pays)), tensors, keep, d, np.float32)
+        torch.cuda.synchronize()
+        for g in groups:
+            g.check()
+        for w in range(P):
+            assert np.array_equal(bits(outs[w].cpu().numpy()), bits(want)), (s, w)
+            assert np.array_equal(bits(states[w].residuals.cpu().numpy()), bits(rs[w]))
