@@ -262,6 +262,10 @@ covap_status covap_peer_attach_local(covap_peer** peers, int nranks);
 /* max_ctas: cap the collective's grid (0 = one CTA per SM); timeout_s: bound
  * of every spin-wait (0 = keep). */
 covap_status covap_peer_set_limits(covap_peer* peer, int max_ctas, double timeout_s);
+/* fused = 1 (default): the collective's last phase reads the reduced slices
+ * straight from their owners and writes the synchronised gradient (C1 + K2 in
+ * one kernel); fused = 0: all-gather into the local send buffer, then K2. */
+covap_status covap_peer_set_fused(covap_peer* peer, int fused);
 covap_status covap_peer_check(covap_peer* peer);
 /* K1 into the parity buffer -> peer allreduce -> K2 (x 1/P) -> ++step. */
 covap_status covap_peer_sync_step(covap_state* state, covap_peer* peer, const void* grad,

@@ -98,6 +98,7 @@ _SIGS = {
     "covap_peer_import": (None, [vp, ctypes.c_char_p, sz]),
     "covap_peer_attach_local": (None, [ctypes.POINTER(vp), i32]),
     "covap_peer_set_limits": (None, [vp, i32, f64]),
+    "covap_peer_set_fused": (None, [vp, i32]),
     "covap_peer_check": (None, [vp]),
     "covap_peer_sync_step": (None, [vp, vp, vp, vp, vp]),
     "covap_device_alloc": (None, [i32, u64, ctypes.POINTER(vp)]),

@@ -790,6 +790,10 @@ class PeerGroup:
     def set_limits(self, max_ctas: int = 0, timeout_s: float = 0.0):
         L.lib().covap_peer_set_limits(self._h, int(max_ctas), float(timeout_s))
 
+    def set_fused(self, fused: bool):
+        """C1 + K2 in one kernel (default) or all-gather then K2."""
+        L.lib().covap_peer_set_fused(self._h, 1 if fused else 0)
+
     def check(self):
         L.lib().covap_peer_check(self._h)
 

@@ -1005,6 +1005,7 @@ struct covap_peer {
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s
   int max_ctas = 0;
   bool attached = false;
+  bool fused = true;  // the collective's last phase writes out (no separate K2)
 };
 
 extern "C" {
@@ -1120,6 +1121,13 @@ covap_status covap_peer_set_limits(covap_peer* p, int max_ctas, double timeout_s
   });
 }
 
+covap_status covap_peer_set_fused(covap_peer* p, int fused) {
+  return guarded([&] {
+    need(p != nullptr, "NULL peer");
+    p->fused = fused != 0;
+  });
+}
+
 covap_status covap_peer_check(covap_peer* p) {
   return guarded([&] {
     need(p != nullptr, "NULL peer");
@@ -1159,9 +1167,17 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
       a.timeout_ns = p->timeout_ns;
       a.P = p->P;
       a.rank = p->rank;
+      a.fused = p->fused ? 1 : 0;
+      a.out = out;
+      a.runs = s->d_runs + s->phase_off[s->num_steps % s->plan.interval];
+      a.nruns = static_cast<int>(ph.runs.size());
+      a.n_out = n;
+      a.inv = 1.0 / static_cast<double>(p->P);
       CK(covapb::launch_peer_allreduce(s->dtype, a, p->max_ctas, st));
     }
-    k2_range(s, buf, out, 1.0 / static_cast<double>(p->P), 1, 0, n, st);
+    // fused: the collective already wrote out (C1 + K2 in one kernel)
+    if (!(p->fused && ph.send_elems > 0))
+      k2_range(s, buf, out, 1.0 / static_cast<double>(p->P), 1, 0, n, st);
     ++s->num_steps;
   });
 }

@@ -60,6 +60,14 @@ struct PeerArgs {
   uint64_t timeout_ns;
   int P;
   int rank;
+  // fused unpack (phase 2 writes the synchronised gradient directly, K2's
+  // work: out[sel] = sum * inv read from the slice owner, out[unsel] = 0)
+  int fused;
+  void* out;
+  const Run* runs;  // device pointer, this phase's run table
+  int nruns;
+  uint64_t n_out;   // device elements of out
+  double inv;
 };
 cudaError_t launch_peer_allreduce(int dtype, const PeerArgs& args, int max_ctas, cudaStream_t s);
 

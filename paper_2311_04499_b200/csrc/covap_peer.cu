@@ -48,6 +48,7 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
 }
 
 __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t umax(uint64_t a, uint64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 
@@ -67,6 +68,16 @@ __device__ __forceinline__ float4 vadd(float4 a, float4 b) {
 __device__ __forceinline__ double2 vadd(double2 a, double2 b) {
   return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
 }
+// (0 + sum) * inv: the sum already starts from +0 (phase 1), so this is
+// allreduce_mean's scale step (trainer.cpp:44-45).
+__device__ __forceinline__ float4 vscale(float4 a, float s) {
+  return make_float4(__fmul_rn(a.x, s), __fmul_rn(a.y, s), __fmul_rn(a.z, s), __fmul_rn(a.w, s));
+}
+__device__ __forceinline__ double2 vscale(double2 a, double s) {
+  return make_double2(__dmul_rn(a.x, s), __dmul_rn(a.y, s));
+}
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 template <typename V>
 __device__ __forceinline__ V vzero();
 template <>
@@ -147,6 +158,55 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
   }
   __syncthreads();
   if (!ok) return;
+
+  // ---- phase 2 (fused): unpack straight from the slice owners -----------
+  if (args.fused) {
+    T* out = static_cast<T*>(args.out);
+    const T inv = static_cast<T>(args.inv);
+    const Run* runs = args.runs;
+    // the owner of send element o: its vector's slice; the scalar tail is
+    // the last rank's (phase 1)
+    auto owner = [&](uint64_t o) -> int {
+      const uint64_t v = o / W;
+      return v >= nvec ? P - 1 : static_cast<int>(v / per);
+    };
+    auto zero_range = [&](uint64_t a, uint64_t b) {
+      if (a >= b) return;
+      const uint64_t a16 = umin(b, (a + W - 1) / W * W), b16 = umax(a16, b / W * W);
+      if (blockIdx.x == 0)
+        for (uint64_t e = a + threadIdx.x; e < a16; e += kPeerThreads) out[e] = T(0);
+      if (blockIdx.x == gridDim.x - 1)
+        for (uint64_t e = b16 + threadIdx.x; e < b; e += kPeerThreads) out[e] = T(0);
+      const V z = vzero<V>();
+      for (uint64_t v = a16 / W + blockIdx.x * kPeerThreads + threadIdx.x; v < b16 / W; v += stride)
+        reinterpret_cast<V*>(out)[v] = z;
+    };
+    uint64_t prev = 0;
+    for (int j = 0; j < args.nruns; ++j) {
+      const uint64_t rb = runs[j].begin, re = runs[j].end, rd = runs[j].dst;
+      zero_range(prev, rb);
+      prev = re;
+      // dst == begin (mod 32): out vectors map onto send vectors
+      const uint64_t a16 = umin(re, (rb + W - 1) / W * W), b16 = umax(a16, re / W * W);
+      if (blockIdx.x == 0)
+        for (uint64_t e = rb + threadIdx.x; e < a16; e += kPeerThreads) {
+          const uint64_t o = rd + (e - rb);
+          out[e] = mul_rn(bufs[owner(o)][o], inv);
+        }
+      if (blockIdx.x == gridDim.x - 1)
+        for (uint64_t e = b16 + threadIdx.x; e < re; e += kPeerThreads) {
+          const uint64_t o = rd + (e - rb);
+          out[e] = mul_rn(bufs[owner(o)][o], inv);
+        }
+      for (uint64_t v = a16 / W + blockIdx.x * kPeerThreads + threadIdx.x; v < b16 / W; v += stride) {
+        const uint64_t o = rd + (v * W - rb);
+        V x = *reinterpret_cast<const V*>(bufs[owner(o)] + o);
+        reinterpret_cast<V*>(out)[v] = vscale(x, inv);
+      }
+    }
+    zero_range(prev, args.n_out);
+    return;
+  }
 
   // ---- phase 2: gather the other ranks' reduced slices -----------------
   for (int q = 1; q < P; ++q) {

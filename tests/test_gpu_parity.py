@@ -438,7 +438,7 @@ def test_padded_plan_equals_flat(covap, name, K):
         assert torch.equal(c.state.residuals[idx], a.state.residuals)
 
 
-def _virtual_ranks(covap, plan, P, dtype, ef):
+def _virtual_ranks(covap, plan, P, dtype, ef, fused=True):
     """P ranks of the peer collective inside one process on one GPU: each has
     its own state and send buffers, its kernels run on its own stream, and
     the grids are capped so all P collectives are resident together."""
@@ -448,12 +448,14 @@ def _virtual_ranks(covap, plan, P, dtype, ef):
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     for g in groups:
         g.set_limits(max_ctas=max(1, sms // (2 * P)), timeout_s=10.0)
+        g.set_fused(fused)
     streams = [torch.cuda.Stream() for _ in range(P)]
     return states, groups, streams
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "gather"])
 @pytest.mark.parametrize("case", manifest()["session"], ids=lambda c: c["name"])
-def test_peer_collective_bit_exact_vs_reference(covap, orc, case):
+def test_peer_collective_bit_exact_vs_reference(covap, orc, case, fused):
     """The NVLink load/store allreduce sums in rank order, so the whole
     P-worker step equals the reference's (trainer.cpp:365-386) bit for bit —
     for P = 2, 3 and 4 (fp64 fixtures from the reference library)."""
@@ -463,7 +465,7 @@ def test_peer_collective_bit_exact_vs_reference(covap, orc, case):
     en, init, asc, rng = case["ef"]
     P = case["P"]
     states, groups, streams = _virtual_ranks(covap, plan, P, torch.float64,
-                                             covap.EfSchedule(bool(en), init, asc, rng))
+                                             covap.EfSchedule(bool(en), init, asc, rng), fused)
     d = plan.total_numel()
     outs = [torch.empty(d, dtype=torch.float64, device=DEV) for _ in range(P)]
     for s in range(case["steps"]):
@@ -480,13 +482,15 @@ def test_peer_collective_bit_exact_vs_reference(covap, orc, case):
         assert np.array_equal(bits(states[0].residuals.cpu().numpy()), bits(fx[f"residual0_{s}"]))
 
 
-@pytest.mark.parametrize("name,K,P", [("resnet50", 4, 2), ("vgg16", 4, 4), ("resnet50", 1, 8)])
-def test_peer_collective_fp32_full_layouts(covap, orc, name, K, P):
+@pytest.mark.parametrize("name,K,P,fused", [("resnet50", 4, 2, True), ("vgg16", 4, 4, True),
+                                            ("resnet50", 1, 8, True), ("vgg16", 3, 3, False),
+                                            ("tablev", 19, 2, True)])
+def test_peer_collective_fp32_full_layouts(covap, orc, name, K, P, fused):
     """fp32 at BASELINE sizes, P virtual ranks: every rank's synchronised
     gradient equals the rank-ordered oracle mean, bit for bit."""
     plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
     ef = covap.EfSchedule(True, 0.3, 1, 0.2)
-    states, groups, streams = _virtual_ranks(covap, plan, P, torch.float32, ef)
+    states, groups, streams = _virtual_ranks(covap, plan, P, torch.float32, ef, fused)
     d = plan.total_numel()
     tensors = [(t.bucket, t.begin, t.end) for t in plan.tensors]
     rs = [np.zeros(d, np.float32) for _ in range(P)]
