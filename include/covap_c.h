@@ -182,6 +182,21 @@ covap_status covap_unpack(covap_state* state, const void* recv, void* out, doubl
  * identity (P = 1); 16N instead of 24N bytes at K = 1.  out may alias grad. */
 covap_status covap_filter_unpack(covap_state* state, const void* grad, void* out, double scale,
                                  size_t b0, size_t b1, void* stream);
+/* The step after the path, fused: plain SGD on the
+ * synchronised gradient, params -= lr * update (trainer.cpp:408-409, multiply
+ * and subtraction rounded separately).  Unselected elements have update 0, so
+ * their parameters are neither read nor written.
+ *   covap_filter_sgd: K1F + SGD for one rank (selected -> params -= lr *
+ *     ((0 + c) * scale), r = 0; unselected -> r = c);
+ *   covap_unpack_sgd: K2 + SGD (selected -> params -= lr * f(recv));
+ *   covap_sync_step_sgd: the sync step ending in the SGD update instead of
+ *     writing `out`. */
+covap_status covap_filter_sgd(covap_state* state, const void* grad, void* params, double lr,
+                              double scale, size_t b0, size_t b1, void* stream);
+covap_status covap_unpack_sgd(covap_state* state, const void* recv, void* params, double lr,
+                              double scale, int mean, size_t b0, size_t b1, void* stream);
+covap_status covap_sync_step_sgd(covap_state* state, covap_comm* comm, const void* grad,
+                                 void* params, double lr, void* stream);
 /* ++num_steps (compress.cpp:83). */
 covap_status covap_step_end(covap_state* state);
 

@@ -77,6 +77,9 @@ _SIGS = {
     "covap_filter_pack": (None, [vp, vp, vp, sz, sz, vp]),
     "covap_unpack": (None, [vp, vp, vp, f64, i32, sz, sz, vp]),
     "covap_filter_unpack": (None, [vp, vp, vp, f64, sz, sz, vp]),
+    "covap_filter_sgd": (None, [vp, vp, vp, f64, f64, sz, sz, vp]),
+    "covap_unpack_sgd": (None, [vp, vp, vp, f64, f64, i32, sz, sz, vp]),
+    "covap_sync_step_sgd": (None, [vp, vp, vp, vp, f64, vp]),
     "covap_step_end": (None, [vp]),
     "covap_sync_step": (None, [vp, vp, vp, vp, vp]),
     "covap_sync_step_host": (None, [vp, vp, vp, vp, vp, vp, u64, vp]),

@@ -636,6 +636,15 @@ class CovapSync:
                                      _ptr(dev_out), int(chunk_elems),
                                      _stream_ptr(stream, self.device))
 
+    def sync_sgd(self, grad, params, lr: float, stream=None):
+        """The sync step ending in the SGD update (trainer.cpp:408-409) instead
+        of writing a synchronised gradient: params -= lr * update, fused into
+        the last kernel (one rank: K1F+SGD; P ranks: K1 -> C1 -> K2+SGD)."""
+        self.state._check(grad)
+        self.state._check(params)
+        L.lib().covap_sync_step_sgd(self.state.handle, self._c(), _ptr(grad), _ptr(params),
+                                    float(lr), _stream_ptr(stream, self.device))
+
     def bucket_ready(self, bucket: int, grad, out, stream=None):
         L.lib().covap_bucket_ready(self.state.handle, self._c(), int(bucket), _ptr(grad), _ptr(out),
                                    _stream_ptr(stream, self.device))

@@ -553,6 +553,72 @@ covap_status covap_filter_unpack(covap_state* s, const void* grad, void* out, do
   });
 }
 
+covap_status covap_filter_sgd(covap_state* s, const void* grad, void* params, double lr,
+                              double scale, size_t b0, size_t b1, void* stream) {
+  return guarded([&] {
+    need(s && grad && params, "NULL argument");
+    need(b0 <= b1 && b1 <= s->plan.buckets.size(), "bucket range out of bounds");
+    need_aligned(grad, "grad");
+    need_aligned(params, "params");
+    if (b0 == b1) return;
+    DeviceGuard dg(s->device);
+    const uint64_t a = s->plan.buckets[b0].dbegin;
+    const uint64_t b = s->plan.buckets[b1 - 1].dbegin + s->plan.buckets[b1 - 1].numel;
+    const size_t ph = s->num_steps % s->plan.interval;
+    CK(covapb::launch_filter_sgd(s->dtype, grad, s->residual, params, s->d_runs + s->phase_off[ph],
+                                 static_cast<int>(s->plan.phases[ph].runs.size()), a, b,
+                                 coeff_of(s), s->ef.enabled, scale, lr, as_stream(stream)));
+  });
+}
+
+covap_status covap_unpack_sgd(covap_state* s, const void* recv, void* params, double lr,
+                              double scale, int mean, size_t b0, size_t b1, void* stream) {
+  return guarded([&] {
+    need(s && params, "NULL argument");
+    need(b0 <= b1 && b1 <= s->plan.buckets.size(), "bucket range out of bounds");
+    need_aligned(params, "params");
+    if (recv) need_aligned(recv, "recv");
+    if (b0 == b1) return;
+    DeviceGuard dg(s->device);
+    const uint64_t a = s->plan.buckets[b0].dbegin;
+    const uint64_t b = s->plan.buckets[b1 - 1].dbegin + s->plan.buckets[b1 - 1].numel;
+    const size_t ph = s->num_steps % s->plan.interval;
+    CK(covapb::launch_unpack_sgd(s->dtype, recv ? recv : s->send, params,
+                                 s->d_runs + s->phase_off[ph],
+                                 static_cast<int>(s->plan.phases[ph].runs.size()), a, b, scale,
+                                 mean, lr, as_stream(stream)));
+  });
+}
+
+covap_status covap_sync_step_sgd(covap_state* s, covap_comm* comm, const void* grad,
+                                 void* params, double lr, void* stream) {
+  return guarded([&] {
+    need(s && grad && params, "NULL argument");
+    need_aligned(grad, "grad");
+    need_aligned(params, "params");
+    if (comm) need(comm->device == s->device, "communicator and state are on different devices");
+    DeviceGuard dg(s->device);
+    cudaStream_t st = as_stream(stream);
+    const uint64_t n = s->plan.dtotal;
+    const auto& ph = phase_of(s->plan, s->num_steps);
+    const int P = world(comm);
+    const int nr = static_cast<int>(ph.runs.size());
+    const covapb::Run* runs = s->d_runs + s->phase_off[s->num_steps % s->plan.interval];
+    if (P == 1 && s->fuse_single_rank) {
+      CK(covapb::launch_filter_sgd(s->dtype, grad, s->residual, params, runs, nr, 0, n, coeff_of(s),
+                                   s->ef.enabled, 1.0, lr, st));
+    } else {
+      k1_range(s, grad, nullptr, 0, n, st);
+      if (comm && ph.send_elems > 0)
+        NK(ncclAllReduce(s->send, s->send, ph.send_elems, nccl_type(s->dtype), ncclSum,
+                         comm->nccl, st));
+      CK(covapb::launch_unpack_sgd(s->dtype, s->send, params, runs, nr, 0, n,
+                                   1.0 / static_cast<double>(P), 1, lr, st));
+    }
+    ++s->num_steps;
+  });
+}
+
 covap_status covap_step_end(covap_state* s) {
   return guarded([&] {
     need(s != nullptr, "NULL state");

@@ -31,6 +31,15 @@ cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, co
 cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, const Run* runs,
                                  int nruns, uint64_t a, uint64_t b, double coeff, int ef,
                                  double inv, cudaStream_t s);
+// K1F + SGD (one rank): selected -> params -= lr * ((0 + c) * inv), r = 0;
+// unselected -> r = c, params untouched (trainer.cpp:408-409 fused).
+cudaError_t launch_filter_sgd(int dtype, const void* g, void* r, void* params, const Run* runs,
+                              int nruns, uint64_t a, uint64_t b, double coeff, int ef, double inv,
+                              double lr, cudaStream_t s);
+// K2 + SGD: selected -> params -= lr * f(recv); unselected untouched.
+cudaError_t launch_unpack_sgd(int dtype, const void* recv, void* params, const Run* runs,
+                              int nruns, uint64_t a, uint64_t b, double inv, int mean, double lr,
+                              cudaStream_t s);
 // K2: out = in-run ? f(recv[dst + e - begin]) : 0 for flat [a, b), with
 // f(x) = (0 + x) * inv when mean (allreduce_mean), x * inv otherwise.
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,

@@ -55,36 +55,30 @@ namespace {
 #ifndef COVAP_K2_TILE
 #define COVAP_K2_TILE 32768
 #endif
-#ifndef COVAP_K1_CTAS  // K1/K1F CTAs per SM (the smem footprint must allow it)
-#define COVAP_K1_CTAS 1
-#endif
-#ifndef COVAP_ZERO_BULK  // 1: zero streams are bulk stores of a zero tile; 0: 128-bit STG
-#define COVAP_ZERO_BULK 1
-#endif
 #ifndef COVAP_PDL  // programmatic dependent launch between consecutive sync kernels
 #define COVAP_PDL 1
 #endif
-#ifndef COVAP_K1_STG  // 1: K1 results leave by 128-bit STG from registers (no staging tiles)
-#define COVAP_K1_STG 0
-#endif
-#ifndef COVAP_K2_STG  // 1: K2 results leave by 128-bit STG from registers (no staging tiles)
-#define COVAP_K2_STG 0
-#endif
 constexpr int kThreads = 256;
-constexpr int kZeroTiles = COVAP_ZERO_BULK ? 1 : 0;
-// K1/K1F: kStages slots of (g, r) tiles + 2 staging tiles (+ zero tile).
+// K1/K1F: kStages slots of (g, r) tiles + 2 staging tiles + 1 zero tile;
+// K1F+SGD adds a params tile per slot.
 constexpr uint32_t kTileK1 = COVAP_K1_TILE;
 constexpr int kStages = COVAP_K1_STAGES;
-constexpr uint32_t kSmemK1 = (2 * kStages + 2 + kZeroTiles) * kTileK1;
-// K2: kStagesK2 recv slots + 2 staging tiles (+ zero tile).
+constexpr uint32_t kSmemK1 = (2 * kStages + 3) * kTileK1;
+constexpr uint32_t kSmemK1Sgd = (3 * kStages + 3) * kTileK1;
+// K2: kStagesK2 recv slots + 2 staging tiles + 1 zero tile; K2+SGD adds a
+// params tile per slot.
 constexpr uint32_t kTileK2 = COVAP_K2_TILE;
 constexpr int kStagesK2 = COVAP_K2_STAGES;
-constexpr uint32_t kSmemK2 = (kStagesK2 + 2 + kZeroTiles) * kTileK2;
+constexpr uint32_t kSmemK2 = (kStagesK2 + 3) * kTileK2;
+constexpr int kStagesK2Sgd = 2;
+constexpr uint32_t kSmemK2Sgd = (2 * kStagesK2Sgd + 3) * kTileK2;
 
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
 // allreduce_mean's (0.0 + sum) * (1/P) (trainer.cpp:41-45) when mean — the
 // leading +0 turns a -0 sum into +0 exactly as the reference does — else the
@@ -228,32 +222,49 @@ struct Args {
   const T* g;      // K1/K1F: fresh gradient
   T* r;            // K1/K1F: residual store (in/out)
   T* send;         // K1: packed send buffer
-  T* out;          // K1F/K2: synchronised gradient (flat layout)
+  T* out;          // K1F/K2: synchronised gradient; SGD variants: the parameters
   const T* recv;   // K2: allreduced send buffer
   const Run* runs;
   int nruns;
-  uint64_t a, b;   // flat element range of the launch
+  uint64_t a, b;   // element range of the launch (device coordinates)
   T coeff;         // EF coefficient (K1/K1F)
   int ef;          // EF enabled: read r
   T inv;           // K1F/K2 scale (1/P)
   int mean;        // K2: allreduce_mean semantics
+  T lr;            // SGD variants: learning rate
 };
 
-// Element path (scalar head/tail and mixed tiles).
+// Operations of the element path / the filter kernel:
+//   0 K1 pack, 1 K1F (one rank, out), 2 K2 unpack,
+//   3 K1F + SGD (one rank, params -= lr * update), 4 K2 + SGD.
+// SGD restates trainer.cpp:408-409, params -= learning_rate * update, with
+// the multiply and the subtraction rounded separately.  Unselected elements
+// have update 0 and p - lr * 0 == p, so their parameters are not touched.
+template <typename T>
+__device__ __forceinline__ T sgd(T p, T lr, T u) {
+  return sub_rn(p, mul_rn(lr, u));
+}
+
 template <typename T, int OP>
 __device__ __forceinline__ void element(const Args<T>& A, int& j, uint64_t e, T gv, T rv) {
   const int k = run_at(A.runs, A.nruns, j, e);
-  if (OP == 2) {
-    A.out[e] = k >= 0 ? scale_of(A.recv[A.runs[k].dst + (e - A.runs[k].begin)], A.inv, A.mean)
-                      : T(0);
+  if (OP == 2 || OP == 4) {
+    if (k < 0) {
+      if (OP == 2) A.out[e] = T(0);
+      return;
+    }
+    const T u = scale_of(A.recv[A.runs[k].dst + (e - A.runs[k].begin)], A.inv, A.mean);
+    A.out[e] = OP == 2 ? u : sgd(A.out[e], A.lr, u);
     return;
   }
   const T c = A.ef ? add_rn(gv, mul_rn(A.coeff, rv)) : gv;
   if (k >= 0) {
     if (OP == 0)
       A.send[A.runs[k].dst + (e - A.runs[k].begin)] = c;
-    else
+    else if (OP == 1)
       A.out[e] = scale_of(c, A.inv, 1);
+    else
+      A.out[e] = sgd(A.out[e], A.lr, scale_of(c, A.inv, 1));
     A.r[e] = T(0);
   } else {
     A.r[e] = c;
@@ -264,47 +275,43 @@ __device__ __forceinline__ void element(const Args<T>& A, int& j, uint64_t e, T 
 // Elements [a, a16) and [b16, b) that do not fill a 16-byte vector.
 template <typename T, int OP>
 __device__ void edges(const Args<T>& A, uint64_t a16, uint64_t b16) {
+  constexpr bool reads_g = OP == 0 || OP == 1 || OP == 3;
   for (uint64_t e = A.a + threadIdx.x; e < a16; e += blockDim.x) {
     int j = first_run_after(A.runs, A.nruns, e);
-    element<T, OP>(A, j, e, OP == 2 ? T(0) : A.g[e], (OP != 2 && A.ef) ? A.r[e] : T(0));
+    element<T, OP>(A, j, e, reads_g ? A.g[e] : T(0), (reads_g && A.ef) ? A.r[e] : T(0));
   }
   for (uint64_t e = b16 + threadIdx.x; e < A.b; e += blockDim.x) {
     int j = first_run_after(A.runs, A.nruns, e);
-    element<T, OP>(A, j, e, OP == 2 ? T(0) : A.g[e], (OP != 2 && A.ef) ? A.r[e] : T(0));
+    element<T, OP>(A, j, e, reads_g ? A.g[e] : T(0), (reads_g && A.ef) ? A.r[e] : T(0));
   }
 }
 
-// Zero-fill of a 16-byte-aligned tile by all threads (128-bit stores): the
-// residual reset of selected shards and the zero fill of unselected output.
-template <typename T>
-__device__ __forceinline__ void zero_tile(T* dst, uint32_t n) {
-  using V = typename Vec16<T>::type;
-  constexpr uint32_t W = 16 / sizeof(T);
-  V z;
-  for (uint32_t q = 0; q < W; ++q) lane(z, q) = T(0);
-  V* d = reinterpret_cast<V*>(dst);
-  for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) d[v] = z;
+// ------------------------------------------------------------ K1 / K1F / K1F+SGD
+//
+// Input ring: kStages slots of (g, r[, params]) tiles, refilled as soon as the
+// tile has been consumed.  Results go to one of two staging tiles and leave
+// with a bulk store; before a staging tile is rewritten, thread 0 waits until
+// the bulk store issued two tiles earlier has read it.  Zero streams (r of
+// selected tiles, out of unselected tiles in K1F) are bulk stores of a
+// persistent zero tile.  K1F+SGD loads a params tile only for selected tiles.
+
+template <int OP>
+constexpr int k1_slot_tiles() {
+  return OP == 3 ? 3 : 2;
 }
 
-// ------------------------------------------------------------ K1 / K1F
-//
-// Input ring: kStages slots of (g tile, r tile), refilled as soon as the tile
-// has been consumed.  Results go to one of two staging tiles and leave with a
-// bulk store; before a staging tile is rewritten, thread 0 waits until the
-// bulk store issued two tiles earlier has read it.  Zero streams (r of
-// selected tiles, out of unselected tiles in K1F) are plain 128-bit stores.
-
-// OP 0 = K1 filter_pack (selected -> send), OP 1 = K1F (selected -> out).
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const Args<T> A) {
+__global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
+  static_assert(OP == 0 || OP == 1 || OP == 3, "filter_kernel ops: 0 pack, 1 K1F, 3 K1F+SGD");
   constexpr uint32_t TE = kTileK1 / sizeof(T);  // elements per tile
   using V = typename Vec16<T>::type;
   constexpr uint32_t W = 16 / sizeof(T);
   extern __shared__ __align__(128) unsigned char smem[];
-  T* gin = reinterpret_cast<T*>(smem);  // kStages tiles (g)
-  T* rin = gin + kStages * TE;          // kStages tiles (r)
-  T* stage = rin + kStages * TE;        // 2 staging tiles
-  T* zero = stage + 2 * TE;             // zero tile (COVAP_ZERO_BULK)
+  T* gin = reinterpret_cast<T*>(smem);                  // kStages tiles (g)
+  T* rin = gin + kStages * TE;                          // kStages tiles (r)
+  T* pin = rin + kStages * TE;                          // kStages tiles (params, OP 3)
+  T* stage = (OP == 3 ? pin + kStages * TE : pin);      // 2 staging tiles
+  T* zero = stage + 2 * TE;                             // zero tile
   __shared__ __align__(8) uint64_t bar[kStages];
 
   pdl_launch_dependents();
@@ -322,8 +329,7 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
   }
   const uint64_t ntiles = (b16 - a16 + TE - 1) / TE;
   const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  if (COVAP_ZERO_BULK)
-    for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
+  for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&bar[i]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -336,11 +342,14 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
   auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * TE; };
   auto issue = [&](uint64_t k) {  // thread 0 only
     const int s = static_cast<int>(k % kStages);
-    const uint64_t e0 = tile_lo(k);
-    const uint32_t bytes = static_cast<uint32_t>((min(e0 + TE, b16) - e0) * sizeof(T));
-    mbar_arrive_tx(&bar[s], A.ef ? 2 * bytes : bytes);
+    const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
+    const uint32_t bytes = static_cast<uint32_t>((e1 - e0) * sizeof(T));
+    bool with_params = false;
+    if (OP == 3) with_params = classify<T>(A.runs, A.nruns, e0, e1).cls == kFull;
+    mbar_arrive_tx(&bar[s], (A.ef ? 2 : 1) * bytes + (with_params ? bytes : 0));
     bulk_load(gin + s * TE, A.g + e0, bytes, &bar[s]);
     if (A.ef) bulk_load(rin + s * TE, A.r + e0, bytes, &bar[s]);
+    if (with_params) bulk_load(pin + s * TE, A.out + e0, bytes, &bar[s]);
   };
   if (threadIdx.x == 0)
     for (uint64_t k = 0; k < my && k < kStages; ++k) issue(k);
@@ -353,45 +362,7 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
     T* st = stage + (k & 1) * TE;
     const T* gs = gin + s * TE;
     const T* rs = rin + s * TE;
-    if constexpr (COVAP_K1_STG != 0) {
-      // Results go straight from registers to global memory; the slot is
-      // free once every thread has read it.
-      mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
-      if (sel.cls != kMixed) {
-        const bool full = sel.cls == kFull;
-        const V* gv = reinterpret_cast<const V*>(gs);
-        const V* rv = reinterpret_cast<const V*>(rs);
-        V z;
-#pragma unroll
-        for (int q = 0; q < static_cast<int>(W); ++q) lane(z, q) = T(0);
-        V* dst = full ? reinterpret_cast<V*>(OP == 0 ? A.send + sel.rd + (e0 - sel.rb) : A.out + e0)
-                      : reinterpret_cast<V*>(A.r + e0);
-        V* zdst = full ? reinterpret_cast<V*>(A.r + e0)
-                       : (OP == 1 ? reinterpret_cast<V*>(A.out + e0) : nullptr);
-        for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
-          V x = gv[v];
-          if (A.ef) {
-            const V y = rv[v];
-#pragma unroll
-            for (int q = 0; q < static_cast<int>(W); ++q)
-              lane(x, q) = add_rn(lane(x, q), mul_rn(A.coeff, lane(y, q)));
-          }
-          if (OP == 1 && full) {
-#pragma unroll
-            for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, 1);
-          }
-          dst[v] = x;
-          if (zdst) zdst[v] = z;
-        }
-      } else {
-        int j = sel.j;
-        for (uint32_t i = threadIdx.x; i < n; i += kThreads)
-          element<T, OP>(A, j, e0 + i, gs[i], A.ef ? rs[i] : T(0));
-      }
-      __syncthreads();
-      if (threadIdx.x == 0 && k + kStages < my) issue(k + kStages);
-      continue;
-    }
+    const T* ps = pin + s * TE;
     if (threadIdx.x == 0) bulk_wait_read<1>();  // staging tile (k & 1) free again
     mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
     __syncthreads();
@@ -400,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
       const bool full = sel.cls == kFull;
       const V* gv = reinterpret_cast<const V*>(gs);
       const V* rv = reinterpret_cast<const V*>(rs);
+      const V* pv = reinterpret_cast<const V*>(ps);
       V* sv = reinterpret_cast<V*>(st);
       for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
         V x = gv[v];
@@ -409,17 +381,16 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
           for (int q = 0; q < static_cast<int>(W); ++q)
             lane(x, q) = add_rn(lane(x, q), mul_rn(A.coeff, lane(y, q)));
         }
-        if (OP == 1 && full) {
+        if (OP != 0 && full) {
 #pragma unroll
           for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, 1);
         }
+        if (OP == 3 && full) {
+          const V p = pv[v];
+#pragma unroll
+          for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = sgd(lane(p, q), A.lr, lane(x, q));
+        }
         sv[v] = x;
-      }
-      if (!COVAP_ZERO_BULK) {
-        if (full)
-          zero_tile(A.r + e0, n);    // residual reset (compress.cpp:77)
-        else if (OP == 1)
-          zero_tile(A.out + e0, n);  // unselected output is zero (compress.cpp:91)
       }
     } else {
       int j = sel.j;
@@ -434,11 +405,11 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
         if (OP == 0)
           bulk_store(A.send + sel.rd + (e0 - sel.rb), st, bytes);
         else
-          bulk_store(A.out + e0, st, bytes);
-        if (COVAP_ZERO_BULK) bulk_store(A.r + e0, zero, bytes);  // residual reset
+          bulk_store(A.out + e0, st, bytes);  // K1F: out; K1F+SGD: params
+        bulk_store(A.r + e0, zero, bytes);    // residual reset (compress.cpp:77)
       } else if (sel.cls == kNone) {
-        bulk_store(A.r + e0, st, bytes);  // r = compensated (compress.cpp:79)
-        if (COVAP_ZERO_BULK && OP == 1) bulk_store(A.out + e0, zero, bytes);
+        bulk_store(A.r + e0, st, bytes);      // r = compensated (compress.cpp:79)
+        if (OP == 1) bulk_store(A.out + e0, zero, bytes);
       }
       bulk_commit();  // one group per tile (possibly empty)
       if (k + kStages < my) issue(k + kStages);  // input slot s is consumed
@@ -447,23 +418,26 @@ __global__ void __launch_bounds__(kThreads, COVAP_K1_CTAS) filter_kernel(const A
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
-// ------------------------------------------------------------ K2
+// ------------------------------------------------------------ K2 / K2+SGD
 //
 // Only "all selected" tiles need their recv slice: they go through a
 // kStagesK2-slot input ring and two staging tiles as in K1.  "None selected"
-// tiles are a 128-bit zero fill by all threads; "mixed" tiles take the
-// element path.
+// tiles are a bulk store of the zero tile (K2) or nothing at all (K2+SGD:
+// their update is zero); "mixed" tiles take the element path.
 
-template <typename T>
+template <typename T, bool SGD>
 __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   constexpr uint32_t TE = kTileK2 / sizeof(T);
+  constexpr int OP = SGD ? 4 : 2;
   using V = typename Vec16<T>::type;
   constexpr uint32_t W = 16 / sizeof(T);
+  constexpr int kSlotTiles = SGD ? 2 : 1;  // recv [+ params]
+  constexpr int NS = SGD ? kStagesK2Sgd : kStagesK2;
   extern __shared__ __align__(128) unsigned char smem[];
-  T* in = reinterpret_cast<T*>(smem);  // kStagesK2 slots
-  T* stage = in + kStagesK2 * TE;      // 2 staging tiles
-  T* zero = stage + 2 * TE;            // zero tile (COVAP_ZERO_BULK)
-  __shared__ __align__(8) uint64_t bar[kStagesK2];
+  T* in = reinterpret_cast<T*>(smem);                // NS x kSlotTiles tiles
+  T* stage = in + NS * kSlotTiles * TE;              // 2 staging tiles
+  T* zero = stage + 2 * TE;                          // zero tile
+  __shared__ __align__(8) uint64_t bar[NS];
 
   pdl_launch_dependents();
   const uint64_t a16 = (A.a + W - 1) / W * W;
@@ -473,22 +447,21 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
     if (blockIdx.x == 0)
       for (uint64_t e = A.a + threadIdx.x; e < A.b; e += blockDim.x) {
         int j = first_run_after(A.runs, A.nruns, e);
-        element<T, 2>(A, j, e, T(0), T(0));
+        element<T, OP>(A, j, e, T(0), T(0));
       }
     return;
   }
   const uint64_t ntiles = (b16 - a16 + TE - 1) / TE;
   const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  if (COVAP_ZERO_BULK)
-    for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
+  for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStagesK2; ++i) mbar_init(&bar[i]);
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_async_smem();
   __syncthreads();
   pdl_wait();
-  if (blockIdx.x == 0) edges<T, 2>(A, a16, b16);
+  if (blockIdx.x == 0) edges<T, OP>(A, a16, b16);
 
   auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * TE; };
   // Producer (thread 0): next tile to examine, next slot sequence number;
@@ -500,28 +473,26 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
       const TileSel sel = classify<T>(A.runs, A.nruns, e0, e1);
       ++kp;
       if (sel.cls == kFull) {
-        const int s = static_cast<int>(qp % kStagesK2);
+        const int s = static_cast<int>(qp % NS);
         const uint32_t bytes = static_cast<uint32_t>((e1 - e0) * sizeof(T));
-        mbar_arrive_tx(&bar[s], bytes);
-        bulk_load(in + s * TE, A.recv + sel.rd + (e0 - sel.rb), bytes, &bar[s]);
+        mbar_arrive_tx(&bar[s], kSlotTiles * bytes);
+        bulk_load(in + s * kSlotTiles * TE, A.recv + sel.rd + (e0 - sel.rb), bytes, &bar[s]);
+        if (SGD) bulk_load(in + (s * kSlotTiles + 1) * TE, A.out + e0, bytes, &bar[s]);
         ++qp;
         return;
       }
     }
   };
   if (threadIdx.x == 0)
-    for (int i = 0; i < kStagesK2; ++i) produce_one();
+    for (int i = 0; i < NS; ++i) produce_one();
 
   uint64_t qc = 0;  // consumer slot sequence number
   for (uint64_t k = 0; k < my; ++k) {
     const uint64_t e0 = tile_lo(k), e1 = min(e0 + TE, b16);
     const uint32_t n = static_cast<uint32_t>(e1 - e0);
     const TileSel sel = classify<T>(A.runs, A.nruns, e0, e1);
-    if (sel.cls == kNone) {  // zero fill (compress.cpp:91)
-      if (!COVAP_ZERO_BULK)
-        zero_tile(A.out + e0, n);
-      else if (threadIdx.x == 0)
-        bulk_store(A.out + e0, zero, n * sizeof(T));
+    if (sel.cls == kNone) {  // zero fill (compress.cpp:91); SGD: nothing to do
+      if (!SGD && threadIdx.x == 0) bulk_store(A.out + e0, zero, n * sizeof(T));
       continue;
     }
     if (sel.cls == kMixed) {
@@ -550,36 +521,32 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
         const uint32_t i = threadIdx.x + q * kThreads;
-        if (i < n) A.out[e0 + i] = ((hit >> q) & 1u) ? scale_of(vals[q], A.inv, A.mean) : T(0);
+        if (i >= n) continue;
+        const bool h = (hit >> q) & 1u;
+        if (!SGD)
+          A.out[e0 + i] = h ? scale_of(vals[q], A.inv, A.mean) : T(0);
+        else if (h)
+          A.out[e0 + i] = sgd(A.out[e0 + i], A.lr, scale_of(vals[q], A.inv, A.mean));
       }
       continue;
     }
-    const int s = static_cast<int>(qc % kStagesK2);
+    const int s = static_cast<int>(qc % NS);
     T* st = stage + (qc & 1) * TE;
-    if constexpr (COVAP_K2_STG != 0) {
-      mbar_wait(&bar[s], static_cast<uint32_t>((qc / kStagesK2) & 1));
-      const V* xv = reinterpret_cast<const V*>(in + s * TE);
-      V* ov = reinterpret_cast<V*>(A.out + e0);
-      for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
-        V x = xv[v];
-#pragma unroll
-        for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, A.mean);
-        ov[v] = x;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) produce_one();
-      ++qc;
-      continue;
-    }
     if (threadIdx.x == 0) bulk_wait_read<1>();
-    mbar_wait(&bar[s], static_cast<uint32_t>((qc / kStagesK2) & 1));
+    mbar_wait(&bar[s], static_cast<uint32_t>((qc / NS) & 1));
     __syncthreads();
-    const V* xv = reinterpret_cast<const V*>(in + s * TE);
+    const V* xv = reinterpret_cast<const V*>(in + s * kSlotTiles * TE);
+    const V* pv = reinterpret_cast<const V*>(in + (s * kSlotTiles + 1) * TE);
     V* sv = reinterpret_cast<V*>(st);
     for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
       V x = xv[v];
 #pragma unroll
       for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, A.mean);
+      if (SGD) {
+        const V p = pv[v];
+#pragma unroll
+        for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = sgd(lane(p, q), A.lr, lane(x, q));
+      }
       sv[v] = x;
     }
     fence_async_smem();
@@ -669,6 +636,12 @@ struct DeviceShape {
   bool ready = false;
 };
 
+template <typename K>
+cudaError_t opt_in(K kernel, uint32_t smem) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem));
+}
+
 // One-time per-device setup: SM count and the >48 KB dynamic-smem opt-in of
 // every instantiation.
 cudaError_t shape(DeviceShape** out) {
@@ -681,19 +654,15 @@ cudaError_t shape(DeviceShape** out) {
   DeviceShape& s = shapes[dev & 63];
   if (!s.ready) {
     if ((e = cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev))) return e;
-    const int k1 = static_cast<int>(kSmemK1), k2 = static_cast<int>(kSmemK2);
-    if ((e = cudaFuncSetAttribute(filter_kernel<float, 0>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k1)) ||
-        (e = cudaFuncSetAttribute(filter_kernel<float, 1>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k1)) ||
-        (e = cudaFuncSetAttribute(filter_kernel<double, 0>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k1)) ||
-        (e = cudaFuncSetAttribute(filter_kernel<double, 1>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k1)) ||
-        (e = cudaFuncSetAttribute(unpack_kernel<float>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k2)) ||
-        (e = cudaFuncSetAttribute(unpack_kernel<double>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, k2)))
+    if ((e = opt_in(filter_kernel<float, 0>, kSmemK1)) || (e = opt_in(filter_kernel<float, 1>, kSmemK1)) ||
+        (e = opt_in(filter_kernel<float, 3>, kSmemK1Sgd)) ||
+        (e = opt_in(filter_kernel<double, 0>, kSmemK1)) ||
+        (e = opt_in(filter_kernel<double, 1>, kSmemK1)) ||
+        (e = opt_in(filter_kernel<double, 3>, kSmemK1Sgd)) ||
+        (e = opt_in(unpack_kernel<float, false>, kSmemK2)) ||
+        (e = opt_in(unpack_kernel<float, true>, kSmemK2Sgd)) ||
+        (e = opt_in(unpack_kernel<double, false>, kSmemK2)) ||
+        (e = opt_in(unpack_kernel<double, true>, kSmemK2Sgd)))
       return e;
     s.ready = true;
   }
@@ -702,7 +671,7 @@ cudaError_t shape(DeviceShape** out) {
 }
 
 // Persistent grid: one CTA per SM (the smem footprint allows one), fewer
-// when the range has fewer 16 KB tiles than SMs.
+// when the range has fewer tiles than SMs.
 unsigned grid_for(uint64_t n_elems, size_t esize, int sms, uint32_t tile_bytes) {
   const uint64_t te = tile_bytes / esize;
   const uint64_t tiles = (n_elems + te - 1) / te;
@@ -712,7 +681,7 @@ unsigned grid_for(uint64_t n_elems, size_t esize, int sms, uint32_t tile_bytes) 
 template <typename T>
 Args<T> make_args(const void* g, void* r, void* send, void* out, const void* recv,
                   const Run* runs, int nruns, uint64_t a, uint64_t b, double coeff, int ef,
-                  double inv, int mean) {
+                  double inv, int mean, double lr) {
   Args<T> A;
   A.g = static_cast<const T*>(g);
   A.r = static_cast<T*>(r);
@@ -727,14 +696,15 @@ Args<T> make_args(const void* g, void* r, void* send, void* out, const void* rec
   A.ef = ef;
   A.inv = static_cast<T>(inv);
   A.mean = mean;
+  A.lr = static_cast<T>(lr);
   return A;
 }
 
 // Launch with the programmatic-stream-serialization attribute (PDL) so the
 // kernel may start while the previous kernel in the stream drains.
-template <typename... KArgs, typename... Args2>
-cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, unsigned smem, cudaStream_t s,
-                   Args2&&... args) {
+template <typename T>
+cudaError_t launch(void (*kernel)(const Args<T>), unsigned grid, unsigned smem, cudaStream_t s,
+                   const Args<T>& args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -745,7 +715,32 @@ cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, unsigned smem, cudaS
   attr[0].val.programmaticStreamSerializationAllowed = COVAP_PDL ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args2>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// One of the streaming passes over [a, b): filter ops 0/1/3, unpack (2) or
+// unpack + SGD (4), fp32 or fp64.
+template <typename T>
+cudaError_t pass(int op, const Args<T>& A, cudaStream_t s) {
+  if (A.b <= A.a) return cudaSuccess;
+  DeviceShape* sh;
+  cudaError_t e = shape(&sh);
+  if (e) return e;
+  const uint64_t n = A.b - A.a;
+  switch (op) {
+    case 0: return launch(filter_kernel<T, 0>, grid_for(n, sizeof(T), sh->sms, kTileK1), kSmemK1, s, A);
+    case 1: return launch(filter_kernel<T, 1>, grid_for(n, sizeof(T), sh->sms, kTileK1), kSmemK1, s, A);
+    case 3: return launch(filter_kernel<T, 3>, grid_for(n, sizeof(T), sh->sms, kTileK1), kSmemK1Sgd, s, A);
+    case 2: return launch(unpack_kernel<T, false>, grid_for(n, sizeof(T), sh->sms, kTileK2), kSmemK2, s, A);
+    default: return launch(unpack_kernel<T, true>, grid_for(n, sizeof(T), sh->sms, kTileK2), kSmemK2Sgd, s, A);
+  }
+}
+
+template <typename... X>
+cudaError_t pass_dt(int dtype, int op, cudaStream_t s, X... x) {
+  if (dtype == 0) return pass<float>(op, make_args<float>(x...), s);
+  return pass<double>(op, make_args<double>(x...), s);
 }
 
 }  // namespace
@@ -753,50 +748,33 @@ cudaError_t launch(void (*kernel)(KArgs...), unsigned grid, unsigned smem, cudaS
 cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, const Run* runs,
                                int nruns, uint64_t a, uint64_t b, double coeff, int ef,
                                cudaStream_t s) {
-  if (b <= a) return cudaSuccess;
-  DeviceShape* sh;
-  cudaError_t e = shape(&sh);
-  if (e) return e;
-  if (dtype == 0)
-    e = launch(filter_kernel<float, 0>, grid_for(b - a, 4, sh->sms * COVAP_K1_CTAS, kTileK1), kSmemK1, s,
-               make_args<float>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
-  else
-    e = launch(filter_kernel<double, 0>, grid_for(b - a, 8, sh->sms * COVAP_K1_CTAS, kTileK1), kSmemK1, s,
-               make_args<double>(g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1));
-  return e != cudaSuccess ? e : cudaGetLastError();
+  return pass_dt(dtype, 0, s, g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1, 0.0);
 }
 
 cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, const Run* runs,
                                  int nruns, uint64_t a, uint64_t b, double coeff, int ef,
                                  double inv, cudaStream_t s) {
-  if (b <= a) return cudaSuccess;
-  DeviceShape* sh;
-  cudaError_t e = shape(&sh);
-  if (e) return e;
-  if (dtype == 0)
-    e = launch(filter_kernel<float, 1>, grid_for(b - a, 4, sh->sms * COVAP_K1_CTAS, kTileK1), kSmemK1, s,
-               make_args<float>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
-  else
-    e = launch(filter_kernel<double, 1>, grid_for(b - a, 8, sh->sms * COVAP_K1_CTAS, kTileK1), kSmemK1, s,
-               make_args<double>(g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1));
-  return e != cudaSuccess ? e : cudaGetLastError();
+  return pass_dt(dtype, 1, s, g, r, nullptr, out, nullptr, runs, nruns, a, b, coeff, ef, inv, 1, 0.0);
+}
+
+cudaError_t launch_filter_sgd(int dtype, const void* g, void* r, void* params, const Run* runs,
+                              int nruns, uint64_t a, uint64_t b, double coeff, int ef, double inv,
+                              double lr, cudaStream_t s) {
+  return pass_dt(dtype, 3, s, g, r, nullptr, params, nullptr, runs, nruns, a, b, coeff, ef, inv, 1,
+                 lr);
 }
 
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
                           uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s) {
-  if (b <= a) return cudaSuccess;
-  DeviceShape* sh;
-  cudaError_t e = shape(&sh);
-  if (e) return e;
-  if (dtype == 0)
-    e = launch(unpack_kernel<float>, grid_for(b - a, 4, sh->sms, kTileK2), kSmemK2, s,
-               make_args<float>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
-                                mean));
-  else
-    e = launch(unpack_kernel<double>, grid_for(b - a, 8, sh->sms, kTileK2), kSmemK2, s,
-               make_args<double>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
-                                 mean));
-  return e != cudaSuccess ? e : cudaGetLastError();
+  return pass_dt(dtype, 2, s, nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
+                 mean, 0.0);
+}
+
+cudaError_t launch_unpack_sgd(int dtype, const void* recv, void* params, const Run* runs,
+                              int nruns, uint64_t a, uint64_t b, double inv, int mean, double lr,
+                              cudaStream_t s) {
+  return pass_dt(dtype, 4, s, nullptr, nullptr, nullptr, params, recv, runs, nruns, a, b, 0.0, 0,
+                 inv, mean, lr);
 }
 
 cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,

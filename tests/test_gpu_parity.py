@@ -512,3 +512,36 @@ def test_peer_collective_fp32_full_layouts(covap, orc, name, K, P, fused):
         for w in range(P):
             assert np.array_equal(bits(outs[w].cpu().numpy()), bits(want)), (s, w)
             assert np.array_equal(bits(states[w].residuals.cpu().numpy()), bits(rs[w]))
+
+
+@pytest.mark.parametrize("name,K,fuse", [("resnet50", 1, True), ("resnet50", 4, True),
+                                         ("vgg16", 4, False), ("tablev", 19, True),
+                                         ("vgg16", 3, True)])
+def test_fused_sgd_step_bit_exact(covap, orc, name, K, fuse):
+    """The sync step ending in the SGD update (trainer.cpp:408-409) — one rank
+    K1F+SGD, or K1 -> K2+SGD — equals the oracle's synchronised gradient
+    followed by params - lr * update (fp32, mul then sub), bit for bit, with
+    the residual carried; unselected parameters are untouched."""
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    ef = covap.EfSchedule(True, 0.3, 1, 0.2)
+    sync = covap.CovapSync(plan, None, torch.float32, 0, ef, fuse_single_rank=fuse)
+    d = plan.total_numel()
+    tensors = [(t.bucket, t.begin, t.end) for t in plan.tensors]
+    lr = 0.0625 * 1.1
+    params = dev_gen(covap, 99, d, 0, torch.float32)
+    p_ref = params.cpu().numpy().copy()
+    r = np.zeros(d, np.float32)
+    for s in range(K + 2):
+        key = orc.stream_key(12, 0, s)
+        g = dev_gen(covap, key, d, 0, torch.float32)
+        sync.sync_sgd(g, params, lr)
+        keep = orc.select(s, K, len(tensors))
+        p = orc.compress(orc.generate(key, d, 0, 0, np.float32), r, tensors, keep, 1,
+                         np.float32(orc.ef_coefficient(s, 0.3, 1, 0.2)))
+        upd = orc.decompress(orc.allreduce_mean(p[None, :]) if len(p) else p, tensors, keep, d,
+                             np.float32)
+        with np.errstate(all="ignore"):
+            p_ref = (p_ref - (np.float32(lr) * upd).astype(np.float32)).astype(np.float32)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(params.cpu().numpy()), bits(p_ref)), s
+        assert np.array_equal(bits(sync.state.residuals.cpu().numpy()), bits(r)), s
