@@ -4,9 +4,14 @@
 #   bash scripts/variants.sh run > gpurun_out/variants.txt
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
+# Knobs of csrc/covap_kernels.cu: COVAP_K1_TILE / COVAP_K1_STAGES (K1, K1F),
+# COVAP_K2_TILE / COVAP_K2_STAGES (K2), COVAP_PDL.  Earlier variants (STG
+# outputs, STG zero fill, in-place slots, 2 CTAs/SM) were measured slower and
+# removed from the kernels; see profiles/r1_design_study.md.
 declare -A V=(
-  [pdl]=""
+  [base]=""
   [nopdl]="-DCOVAP_PDL=0"
+  [k1t16]="-DCOVAP_K1_TILE=16384"
 )
 if [ "$1" = "build" ]; then
   for name in "${!V[@]}"; do
@@ -16,7 +21,7 @@ if [ "$1" = "build" ]; then
   done
   exit 0
 fi
-for name in ${NAMES:-pdl nopdl}; do
+for name in ${NAMES:-base nopdl k1t16}; do
   lib=$ROOT/paper_2311_04499_b200/_variants/$name/libcovap_b200.so
   for cfg in "--layout resnet50 --interval 1" "--layout resnet50 --interval 4" "--layout vgg16 --interval 4" "--layout bert_large --interval 1" "--layout bert_large --interval 4"; do
     COVAP_LIB_PATH=$lib timeout 300 python $ROOT/bench.py $cfg --no-cpu-baseline --no-overhead --steps 30 --warmup 5 2>/dev/null | \
