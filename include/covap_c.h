@@ -245,6 +245,26 @@ covap_status covap_dense_bucket_ready(covap_state* state, covap_comm* comm, size
  * the bucket sent nothing.  Used by the CCR controller. */
 covap_status covap_state_last_comm_ms(covap_state* state, double* dur, size_t n);
 
+/* Timeline of the last overlapped step: with
+ * recording on, every bucket_ready / dense_bucket_ready records CUDA events;
+ * covap_state_timeline returns, per bucket, 5 times in ms relative to bucket
+ * 0's K1 start: K1 start, K1 end (pack done), collective start, collective end,
+ * K2 end (-1: no collective, fused single-rank pass). */
+covap_status covap_state_set_timeline(covap_state* state, int on);
+covap_status covap_state_timeline(covap_state* state, double* rows, size_t n_buckets);
+
+/* overlap_schedule (perf.cpp:63-103): the exact overlapped iteration over
+ * per-tensor times.  compress_ms and communicated may be NULL.  Outputs (any
+ * may be NULL): total, stream end, unoverlapped comm, per communicated tensor
+ * start/end/index (n_comm of them), bubbles (after-tensor, duration). */
+covap_status covap_overlap_schedule(double before_ms, const double* comp_ms,
+                                    const double* compress_ms, const double* comm_ms,
+                                    const uint8_t* communicated, size_t n, double* total_ms,
+                                    double* stream_end_ms, double* unoverlapped_ms,
+                                    double* comm_start_ms, double* comm_end_ms,
+                                    int64_t* comm_tensor, size_t* n_comm, int64_t* bubble_after,
+                                    double* bubble_ms, size_t* n_bubbles);
+
 /* ---------------------------------------------------- communicator ------ */
 
 covap_status covap_comm_unique_id(uint8_t id[128]);

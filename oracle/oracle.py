@@ -307,6 +307,31 @@ class Ref:
         _ck(self.d.ref_choose_interval(c, ctypes.byref(k)), "ref_choose")
         return k.value
 
+    def overlap_schedule(self, before, comp, compress, comm, communicated):
+        n = len(comp)
+        c = _arr(comp, np.float64)
+        cm = _arr(comm, np.float64)
+        cp = None if compress is None else _p(_arr(compress, np.float64), _f64)
+        sent = None if communicated is None else _p(_arr(communicated, np.uint8), _u8)
+        tot, se, un = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        cs, ce = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        ct = np.zeros(max(n, 1), np.int64)
+        ba, bm = np.zeros(max(n, 1), np.int64), np.zeros(max(n, 1))
+        nc, nb = _sz(), _sz()
+        i64 = ctypes.POINTER(ctypes.c_int64)
+        self.d.ref_overlap_schedule.argtypes = [ctypes.c_double, _f64, _f64, _f64, _u8, _sz, _f64, _f64,
+                                                _f64, _f64, _f64, i64, ctypes.POINTER(_sz), i64, _f64,
+                                                ctypes.POINTER(_sz)]
+        _ck(self.d.ref_overlap_schedule(before, _p(c, _f64), cp, _p(cm, _f64), sent, n,
+                                        ctypes.byref(tot), ctypes.byref(se), ctypes.byref(un),
+                                        _p(cs, _f64), _p(ce, _f64), _p(ct, i64), ctypes.byref(nc),
+                                        _p(ba, i64), _p(bm, _f64), ctypes.byref(nb)), "ref_overlap")
+        k, b = nc.value, nb.value
+        return {"total": tot.value, "stream_end": se.value, "unoverlapped": un.value,
+                "comm_start": cs[:k].tolist(), "comm_end": ce[:k].tolist(),
+                "comm_tensor": ct[:k].tolist(), "bubble_after": ba[:b].tolist(),
+                "bubble_ms": bm[:b].tolist()}
+
     def profile_ccr(self, starts, ends, comp_ms, expected=None):
         s = _arr(starts, np.float64)
         e = _arr(ends, np.float64)

@@ -275,3 +275,39 @@ int ref_session_step(void* h, const double* grads, double* update, double* resid
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// overlap_schedule (perf.cpp:63-103).
+int ref_overlap_schedule(double before, const double* comp, const double* compress,
+                         const double* comm, const uint8_t* communicated, std::size_t n,
+                         double* total, double* stream_end, double* unoverlapped,
+                         double* comm_start, double* comm_end, std::int64_t* comm_tensor,
+                         std::size_t* n_comm, std::int64_t* bubble_after, double* bubble_ms,
+                         std::size_t* n_bubbles) {
+  GUARD({
+    std::vector<bool> sent;
+    if (communicated)
+      for (std::size_t i = 0; i < n; ++i) sent.push_back(communicated[i] != 0);
+    const auto sc = overlap_schedule(before, std::span<const double>(comp, n),
+                                     compress ? std::span<const double>(compress, n)
+                                              : std::span<const double>(),
+                                     std::span<const double>(comm, n), sent);
+    *total = sc.total_ms;
+    *stream_end = sc.stream_end_ms;
+    *unoverlapped = sc.unoverlapped_comm_ms;
+    *n_comm = sc.comm_tensor.size();
+    for (std::size_t i = 0; i < sc.comm_tensor.size(); ++i) {
+      comm_start[i] = sc.comm_start_ms[i];
+      comm_end[i] = sc.comm_end_ms[i];
+      comm_tensor[i] = sc.comm_tensor[i];
+    }
+    *n_bubbles = sc.bubbles.size();
+    for (std::size_t i = 0; i < sc.bubbles.size(); ++i) {
+      bubble_after[i] = sc.bubbles[i].after_tensor;
+      bubble_ms[i] = sc.bubbles[i].duration_ms;
+    }
+  })
+}
+
+}  // extern "C"

@@ -89,6 +89,11 @@ _SIGS = {
     "covap_dense_bucket_ready_local": (None, [vp, vp, sz, vp, vp, vp]),
     "covap_dense_bucket_ready": (None, [vp, vp, sz, vp, vp, vp]),
     "covap_state_last_comm_ms": (None, [vp, f64p, sz]),
+    "covap_state_set_timeline": (None, [vp, i32]),
+    "covap_state_timeline": (None, [vp, f64p, sz]),
+    "covap_overlap_schedule": (None, [f64, f64p, f64p, f64p, u8p, sz, f64p, f64p, f64p, f64p, f64p,
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(sz),
+                                      ctypes.POINTER(ctypes.c_int64), f64p, ctypes.POINTER(sz)]),
     "covap_comm_unique_id": (None, [ctypes.c_char_p]),
     "covap_comm_create": (None, [ctypes.c_char_p, i32, i32, i32, ctypes.POINTER(vp)]),
     "covap_comm_destroy": ("void", [vp]),

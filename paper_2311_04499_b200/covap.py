@@ -812,3 +812,41 @@ class PeerGroup:
         self.state._check(out)
         L.lib().covap_peer_sync_step(self.state.handle, self._h, _ptr(grad), _ptr(out),
                                      _stream_ptr(stream, self.state.device))
+
+
+# ------------------------------------------------------------ timeline / overlap model
+
+@dataclass
+class OverlapSchedule:
+    """OverlapSchedule (perf.hpp:40-58)."""
+    total_ms: float
+    stream_end_ms: float
+    unoverlapped_comm_ms: float
+    comm_start_ms: List[float]
+    comm_end_ms: List[float]
+    comm_tensor: List[int]
+    bubbles: List[tuple]  # (after_tensor, duration_ms)
+
+
+def overlap_schedule(before_ms: float, comp_ms: Sequence[float],
+                     compress_ms: Optional[Sequence[float]], comm_ms: Sequence[float],
+                     communicated: Optional[Sequence[bool]] = None) -> OverlapSchedule:
+    """overlap_schedule (perf.cpp:63-103): the exact overlapped iteration."""
+    n = len(comp_ms)
+    if len(comm_ms) != n or (compress_ms is not None and len(compress_ms) != n) or \
+            (communicated is not None and len(communicated) != n):
+        raise InvalidInput("per-tensor lists have inconsistent lengths")
+    dbl = ctypes.c_double * max(n, 1)
+    c, m = dbl(*comp_ms), dbl(*comm_ms)
+    cp = None if compress_ms is None else dbl(*compress_ms)
+    sent = None if communicated is None else (ctypes.c_uint8 * max(n, 1))(*[1 if x else 0 for x in communicated])
+    tot, se, un = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    cs, ce, bm = dbl(), dbl(), dbl()
+    ct, ba = (ctypes.c_int64 * max(n, 1))(), (ctypes.c_int64 * max(n, 1))()
+    nc, nb = ctypes.c_size_t(), ctypes.c_size_t()
+    L.lib().covap_overlap_schedule(float(before_ms), c, cp, m, sent, n, ctypes.byref(tot),
+                                   ctypes.byref(se), ctypes.byref(un), cs, ce, ct, ctypes.byref(nc),
+                                   ba, bm, ctypes.byref(nb))
+    k, b = nc.value, nb.value
+    return OverlapSchedule(tot.value, se.value, un.value, list(cs[:k]), list(ce[:k]), list(ct[:k]),
+                           [(ba[i], bm[i]) for i in range(b)])

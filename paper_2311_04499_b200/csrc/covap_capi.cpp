@@ -56,6 +56,9 @@ struct covap_state {
   std::vector<cudaEvent_t> ev_in, ev_k;  // per-chunk event pools (reused cyclically)
   cudaEvent_t done = nullptr;
   std::vector<cudaEvent_t> ready, arrive, end;  // per bucket
+  std::vector<cudaEvent_t> k1s, k2e;            // timeline: K1 start, K2 end, per bucket
+  bool timeline = false;                        // record k1s / k2e in the overlapped schedule
+  std::vector<uint8_t> tl_mode;                 // per bucket: 0 fused, 1 covap, 2 dense
   std::vector<uint8_t> timed;                   // bucket had a collective in the last step
   bool fuse_single_rank = true;                 // P = 1: run K1F instead of K1 -> C1 -> K2
 };
@@ -376,6 +379,34 @@ covap_status covap_profile_ccr(const double* comm_start, const double* comm_end,
   });
 }
 
+covap_status covap_overlap_schedule(double before_ms, const double* comp_ms,
+                                    const double* compress_ms, const double* comm_ms,
+                                    const uint8_t* communicated, size_t n, double* total_ms,
+                                    double* stream_end_ms, double* unoverlapped_ms,
+                                    double* comm_start_ms, double* comm_end_ms,
+                                    int64_t* comm_tensor, size_t* n_comm, int64_t* bubble_after,
+                                    double* bubble_ms, size_t* n_bubbles) {
+  return guarded([&] {
+    need(n == 0 || (comp_ms && comm_ms), "NULL per-tensor list");
+    const covapb::Schedule sc =
+        covapb::overlap_schedule(before_ms, comp_ms, compress_ms, comm_ms, communicated, n);
+    if (total_ms) *total_ms = sc.total;
+    if (stream_end_ms) *stream_end_ms = sc.stream_end;
+    if (unoverlapped_ms) *unoverlapped_ms = sc.unoverlapped;
+    if (n_comm) *n_comm = sc.comm_tensor.size();
+    for (size_t i = 0; i < sc.comm_tensor.size(); ++i) {
+      if (comm_start_ms) comm_start_ms[i] = sc.comm_start[i];
+      if (comm_end_ms) comm_end_ms[i] = sc.comm_end[i];
+      if (comm_tensor) comm_tensor[i] = sc.comm_tensor[i];
+    }
+    if (n_bubbles) *n_bubbles = sc.bubbles.size();
+    for (size_t i = 0; i < sc.bubbles.size(); ++i) {
+      if (bubble_after) bubble_after[i] = sc.bubbles[i].first;
+      if (bubble_ms) bubble_ms[i] = sc.bubbles[i].second;
+    }
+  });
+}
+
 // ---------------------------------------------------------------- state
 
 void covap_state_destroy(covap_state* s) {
@@ -388,6 +419,8 @@ void covap_state_destroy(covap_state* s) {
   cudaFree(s->send);
   cudaFree(s->d_runs);
   for (auto e : s->ready) cudaEventDestroy(e);
+  for (auto e : s->k1s) cudaEventDestroy(e);
+  for (auto e : s->k2e) cudaEventDestroy(e);
   for (auto e : s->arrive) cudaEventDestroy(e);
   for (auto e : s->end) cudaEventDestroy(e);
   if (s->done) cudaEventDestroy(s->done);
@@ -447,8 +480,15 @@ covap_status covap_state_create(const covap_plan* plan, int dtype, int device,
     s->arrive.resize(nb);
     s->end.resize(nb);
     s->timed.assign(nb, 0);
+    s->k1s.resize(nb);
+    s->k2e.resize(nb);
+    s->tl_mode.assign(nb, 0);
     for (size_t b = 0; b < nb; ++b) {
-      CK(cudaEventCreateWithFlags(&s->ready[b], cudaEventDisableTiming));
+      CK(cudaEventCreate(&s->k1s[b]));
+      CK(cudaEventCreate(&s->k2e[b]));
+    }
+    for (size_t b = 0; b < nb; ++b) {
+      CK(cudaEventCreate(&s->ready[b]));  // timed: the K1-end mark of the timeline
       CK(cudaEventCreate(&s->arrive[b]));
       CK(cudaEventCreate(&s->end[b]));
     }
@@ -748,9 +788,12 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
     const auto& sel = phase_of(s->plan, s->num_steps).per_bucket[bucket];
     const uint64_t a = bk.dbegin, b = bk.dbegin + bk.numel;
     const int P = world(comm);
+    if (s->timeline) CK(cudaEventRecord(s->k1s[bucket], st));
     if (P == 1 && s->fuse_single_rank) {  // no exchange: the fused pass on the producing stream
       k1f_range(s, grad, out, 1.0, a, b, st);
+      if (s->timeline) CK(cudaEventRecord(s->ready[bucket], st));
       s->timed[bucket] = 0;
+      s->tl_mode[bucket] = 0;
       return;
     }
     k1_range(s, grad, nullptr, a, b, st);
@@ -758,6 +801,7 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
     CK(cudaStreamWaitEvent(s->comm_stream, s->ready[bucket], 0));
     const uint64_t len = sel.sel_end - sel.sel_begin;
     s->timed[bucket] = len > 0 ? 1 : 0;
+    s->tl_mode[bucket] = 1;
     CK(cudaEventRecord(s->arrive[bucket], s->comm_stream));
     if (comm && len > 0)
       NK(ncclAllReduce(static_cast<char*>(s->send) + sel.send_offset * s->esize,
@@ -765,6 +809,38 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
                        nccl_type(s->dtype), ncclSum, comm->nccl, s->comm_stream));
     CK(cudaEventRecord(s->end[bucket], s->comm_stream));
     k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, a, b, s->comm_stream);
+    if (s->timeline) CK(cudaEventRecord(s->k2e[bucket], s->comm_stream));
+  });
+}
+
+covap_status covap_state_set_timeline(covap_state* s, int on) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    s->timeline = on != 0;
+  });
+}
+
+covap_status covap_state_timeline(covap_state* s, double* rows, size_t n) {
+  return guarded([&] {
+    need(s && rows, "NULL argument");
+    need(s->timeline, "timeline recording is off (covap_state_set_timeline)");
+    need(n <= s->plan.buckets.size(), "n exceeds bucket count");
+    DeviceGuard dg(s->device);
+    CK(cudaStreamSynchronize(s->comm_stream));
+    CK(cudaDeviceSynchronize());
+    auto ms = [&](cudaEvent_t e) {
+      float v = 0.f;
+      CK(cudaEventElapsedTime(&v, s->k1s[0], e));
+      return static_cast<double>(v);
+    };
+    for (size_t b = 0; b < n; ++b) {
+      double* r = rows + 5 * b;
+      r[0] = ms(s->k1s[b]);
+      r[1] = s->tl_mode[b] == 2 ? r[0] : ms(s->ready[b]);
+      r[2] = s->tl_mode[b] == 0 ? -1.0 : ms(s->arrive[b]);
+      r[3] = s->tl_mode[b] == 0 ? -1.0 : ms(s->end[b]);
+      r[4] = s->tl_mode[b] == 0 ? r[1] : ms(s->k2e[b]);
+    }
   });
 }
 
@@ -779,10 +855,12 @@ covap_status covap_dense_bucket_ready(covap_state* s, covap_comm* comm, size_t b
     cudaStream_t st = as_stream(stream);
     const auto& bk = s->plan.buckets[bucket];
     const uint64_t a = bk.dbegin, b = bk.dbegin + bk.numel;
+    if (s->timeline) CK(cudaEventRecord(s->k1s[bucket], st));
     CK(cudaEventRecord(s->ready[bucket], st));
     CK(cudaStreamWaitEvent(s->comm_stream, s->ready[bucket], 0));
     const int P = world(comm);
     s->timed[bucket] = 1;
+    s->tl_mode[bucket] = 2;
     CK(cudaEventRecord(s->arrive[bucket], s->comm_stream));
     if (comm)
       NK(ncclAllReduce(static_cast<char*>(grad) + a * s->esize,
@@ -792,6 +870,7 @@ covap_status covap_dense_bucket_ready(covap_state* s, covap_comm* comm, size_t b
     // allreduce_mean's "0 + sum, then x 1/P" (trainer.cpp:41-45) in place.
     CK(covapb::launch_unpack(s->dtype, grad, out, s->d_full, 1, a, b,
                              1.0 / static_cast<double>(P), 1, s->comm_stream));
+    if (s->timeline) CK(cudaEventRecord(s->k2e[bucket], s->comm_stream));
   });
 }
 

@@ -175,3 +175,40 @@ Plan build_plan(const uint64_t* layer_numel, const uint32_t* bpp, size_t n_layer
 }
 
 }  // namespace covapb
+
+namespace covapb {
+
+// perf.cpp:63-103: the exact overlapped schedule over per-tensor times.
+// Tensor i leaves the compute stream at the start of its block; its transfer
+// starts when the channel is free and the tensor is available; a gap between
+// transfers is a bubble; total = max(stream end, last transfer end).
+Schedule overlap_schedule(double before_ms, const double* comp_ms, const double* compress_ms,
+                          const double* comm_ms, const uint8_t* communicated, size_t n) {
+  Schedule sc;
+  double stream = before_ms;
+  double channel = 0.0;
+  bool channel_used = false;
+  int64_t prev = -1;
+  for (size_t i = 0; i < n; ++i) {
+    const double available = stream;
+    stream += comp_ms[i];
+    if (compress_ms) stream += compress_ms[i];
+    const bool sends = communicated == nullptr || communicated[i] != 0;
+    if (!sends) continue;
+    const double start = channel_used ? std::max(channel, available) : available;
+    if (channel_used && start > channel) sc.bubbles.push_back({prev, start - channel});
+    const double end = start + comm_ms[i];
+    sc.comm_tensor.push_back(static_cast<int64_t>(i));
+    sc.comm_start.push_back(start);
+    sc.comm_end.push_back(end);
+    channel = end;
+    channel_used = true;
+    prev = static_cast<int64_t>(i);
+  }
+  sc.stream_end = stream;
+  sc.total = channel_used ? std::max(stream, channel) : stream;
+  sc.unoverlapped = std::max(0.0, sc.total - sc.stream_end);
+  return sc;
+}
+
+}  // namespace covapb

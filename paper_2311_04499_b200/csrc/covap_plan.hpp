@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "covap_internal.h"
@@ -70,5 +71,14 @@ std::vector<uint8_t> select(uint64_t step, uint32_t interval, size_t count, int 
 double ef_coefficient(uint64_t step, int enabled, double init, uint64_t ascend, double range);
 double ccr(double comm_ms, double comp_ms);                                // perf.cpp:40-47
 uint32_t choose_interval(double ccr_value);                                // perf.cpp:49-53
+
+struct Schedule {  // OverlapSchedule (perf.hpp:40-58)
+  double total = 0.0, stream_end = 0.0, unoverlapped = 0.0;
+  std::vector<double> comm_start, comm_end;
+  std::vector<int64_t> comm_tensor;
+  std::vector<std::pair<int64_t, double>> bubbles;  // (after tensor, duration)
+};
+Schedule overlap_schedule(double before_ms, const double* comp_ms, const double* compress_ms,
+                          const double* comm_ms, const uint8_t* communicated, size_t n);
 
 }  // namespace covapb

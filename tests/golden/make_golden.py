@@ -129,6 +129,19 @@ def main():
         a, naive, cc, k = ref.profile_ccr(starts, ends, comp)
         ccr["profile"].append({"starts": starts, "ends": ends, "comp": comp, "aligned": a,
                                "naive": naive, "ccr": cc, "interval": k})
+    # overlap_schedule (perf.cpp:63-103): random per-tensor times, with and
+    # without compress blocks and with a communicated mask
+    ccr["overlap"] = []
+    for trial in range(24):
+        n = 1 + rng() % 12
+        comp = [(1 + rng() % 64) * 0.25 for _ in range(n)]
+        comm = [(rng() % 128) * 0.25 for _ in range(n)]
+        compress = [(rng() % 8) * 0.125 for _ in range(n)] if trial % 2 else None
+        sent = [int(rng() % 3 != 0) for _ in range(n)] if trial % 3 else None
+        before = (rng() % 40) * 0.5
+        res = ref.overlap_schedule(before, comp, compress, comm, sent)
+        ccr["overlap"].append({"before": before, "comp": comp, "compress": compress, "comm": comm,
+                               "communicated": sent, **res})
     with open(os.path.join(HERE, "ccr.json"), "w") as f:
         json.dump(ccr, f)
 

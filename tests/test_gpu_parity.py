@@ -545,3 +545,42 @@ def test_fused_sgd_step_bit_exact(covap, orc, name, K, fuse):
         torch.cuda.synchronize()
         assert np.array_equal(bits(params.cpu().numpy()), bits(p_ref)), s
         assert np.array_equal(bits(sync.state.residuals.cpu().numpy()), bits(r)), s
+
+
+def test_timeline_and_chrome_trace(covap, tmp_path):
+    """The real-timeline profiler: per-bucket K1 / collective / K2 marks of an
+    overlapped step are ordered and non-overlapping per stream; the Chrome
+    trace is written; overlap_schedule over the measured times predicts the
+    step."""
+    import json
+    from paper_2311_04499_b200 import trace
+    comm = covap.Communicator(covap.Communicator.unique_id(), 1, 0, 0)
+    plan = covap.plan_for(covap.load_layout("resnet50"), covap.CovapConfig(interval=4))
+    for fuse in (True, False):
+        sync = covap.CovapSync(plan, None if fuse else comm, torch.float32, 0, fuse_single_rank=fuse)
+        d = plan.total_numel()
+        g, out = torch.empty(d, device=DEV), torch.empty(d, device=DEV)
+        covap.generate(g, 5)
+
+        def step():
+            for b in range(len(plan.buckets)):
+                covap.spin(200.0)
+                sync.bucket_ready(b, g, out)
+            sync.finish()
+        step()
+        tl = trace.record_step(sync, step)
+        assert len(tl) == len(plan.buckets) and tl[0]["k1_start"] == 0.0
+        for b, r in enumerate(tl):
+            assert r["k1_end"] >= r["k1_start"]
+            if b:
+                assert r["k1_start"] >= tl[b - 1]["k1_end"] + 0.15  # the 200 us spin in between
+            if fuse:
+                assert r["comm_start"] == -1.0
+            else:
+                assert r["k1_end"] <= r["comm_start"] + 1e-3 <= r["comm_end"] + 2e-3 <= r["k2_end"] + 3e-3
+        trace.chrome_trace(str(tmp_path / "t.json"), tl)
+        doc = json.load(open(tmp_path / "t.json"))
+        assert len(doc["traceEvents"]) == len(plan.buckets) * (1 if fuse else 3)
+        mc = trace.model_check(tl, [0.2] * len(tl), tl[-1]["k2_end"])
+        assert mc["predicted_step_ms"] > 0.9
+    comm.close()

@@ -189,3 +189,23 @@ def test_padded_device_layout(covap, name, K):
             if br.sel_end > br.sel_begin:
                 dev_sel = br.sel_begin - br.bucket_begin + br.device_begin
                 assert br.send_offset % 32 == dev_sel % 32
+
+
+def test_overlap_schedule_matches_reference(covap):
+    """overlap_schedule (perf.cpp:63-103) bit-exact against the reference's
+    outputs on 24 random cases (with/without compress blocks and masks), and
+    the reference's own test_perf.cpp:59-83 cases."""
+    for c in load("ccr.json")["overlap"]:
+        sc = covap.overlap_schedule(c["before"], c["comp"], c["compress"], c["comm"],
+                                    None if c["communicated"] is None else [bool(x) for x in c["communicated"]])
+        assert (sc.total_ms, sc.stream_end_ms, sc.unoverlapped_comm_ms) == \
+            (c["total"], c["stream_end"], c["unoverlapped"])
+        assert sc.comm_start_ms == c["comm_start"] and sc.comm_end_ms == c["comm_end"]
+        assert sc.comm_tensor == c["comm_tensor"]
+        assert [b[0] for b in sc.bubbles] == c["bubble_after"]
+        assert [b[1] for b in sc.bubbles] == c["bubble_ms"]
+    # test_perf.cpp:59-65: zero communication ends with the stream
+    sc = covap.overlap_schedule(5, [10, 20], None, [0, 0])
+    assert sc.total_ms == 35 and sc.unoverlapped_comm_ms == 0
+    with pytest.raises(covap.InvalidInput):
+        covap.overlap_schedule(0, [1, 2], None, [1])
