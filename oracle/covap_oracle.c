@@ -304,3 +304,231 @@ void oc_generate_f64(uint64_t key, int kind, uint64_t begin, uint64_t n, double*
     }
   }
 }
+
+/* ------------------------------------------- baseline compressors (f4) */
+
+int oc_sparsifier_k(uint64_t d, double k_fraction, uint64_t* k) { /* compress.cpp:107-116 */
+  if (d == 0) return OC_INVALID_INPUT;
+  if (!(k_fraction > 0.0) || k_fraction > 1.0) return OC_INVALID_INPUT;
+  double c = ceil(k_fraction * (double)d);
+  uint64_t v = (uint64_t)c;
+  if (v < 1) v = 1;
+  if (v > d) v = d;
+  *k = v;
+  return OC_OK;
+}
+
+static uint32_t f32_bits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+static float bits_f32(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+
+uint16_t oc_half_bits_from_float(float value, int* saturated) { /* compress.cpp:157-205 */
+  const uint32_t bits = f32_bits(value);
+  const uint16_t sign = (uint16_t)((bits >> 16) & 0x8000u);
+  const uint32_t abs_bits = bits & 0x7fffffffu;
+  if (abs_bits > 0x7f800000u) return (uint16_t)(sign | 0x7e00u);
+  if (bits_f32(abs_bits) > 65504.0f) {
+    if (saturated) *saturated = 1;
+    return (uint16_t)(sign | 0x7bffu);
+  }
+  const int32_t e = (int32_t)((abs_bits >> 23) & 0xff) - 127;
+  uint32_t mant = abs_bits & 0x7fffffu;
+  if (e < -24) return sign;
+  if (e < -14) {
+    mant |= 0x800000u;
+    const uint32_t shift = (uint32_t)(-14 - e) + 13;
+    const uint32_t hm = mant >> shift;
+    const uint32_t rest = mant & ((1u << shift) - 1);
+    const uint32_t halfway = 1u << (shift - 1);
+    uint32_t rounded = hm;
+    if (rest > halfway || (rest == halfway && (hm & 1u))) ++rounded;
+    return (uint16_t)(sign | rounded);
+  }
+  uint32_t he = (uint32_t)(e + 15);
+  uint32_t hm = mant >> 13;
+  const uint32_t rest = mant & 0x1fffu;
+  if (rest > 0x1000u || (rest == 0x1000u && (hm & 1u))) {
+    ++hm;
+    if (hm == 0x400u) {
+      hm = 0;
+      ++he;
+    }
+  }
+  if (he >= 31) {
+    if (saturated) *saturated = 1;
+    return (uint16_t)(sign | 0x7bffu);
+  }
+  return (uint16_t)(sign | (he << 10) | hm);
+}
+
+float oc_float_from_half_bits(uint16_t h) { /* compress.cpp:207-224 */
+  const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+  const uint32_t e = (h >> 10) & 0x1fu;
+  const uint32_t m = h & 0x3ffu;
+  if (e == 0) {
+    if (m == 0) return bits_f32(sign);
+    uint32_t mm = m;
+    int32_t ee = -14;
+    while ((mm & 0x400u) == 0) {
+      mm <<= 1;
+      --ee;
+    }
+    mm &= 0x3ffu;
+    return bits_f32(sign | ((uint32_t)(ee + 127) << 23) | (mm << 13));
+  }
+  if (e == 31) return bits_f32(sign | 0x7f800000u | (m << 13));
+  return bits_f32(sign | ((e - 15 + 127) << 23) | (m << 13));
+}
+
+void oc_fp16_roundtrip_f64(const double* x, uint64_t n, double* out, uint64_t* saturations) {
+  for (uint64_t i = 0; i < n; ++i) {
+    int sat = 0;
+    const uint16_t h = oc_half_bits_from_float((float)x[i], &sat);
+    if (sat && saturations) ++*saturations;
+    out[i] = (double)oc_float_from_half_bits(h);
+  }
+}
+
+void oc_fp16_roundtrip_f32(const float* x, uint64_t n, float* out, uint64_t* saturations) {
+  for (uint64_t i = 0; i < n; ++i) {
+    int sat = 0;
+    const uint16_t h = oc_half_bits_from_float(x[i], &sat);
+    if (sat && saturations) ++*saturations;
+    out[i] = oc_float_from_half_bits(h);
+  }
+}
+
+/* std::stable_sort by |x| descending == sort by (|x| desc, index asc). */
+static const void* g_topk_x;
+static int g_topk_f32;
+static int cmp_topk(const void* a, const void* b) {
+  const uint64_t i = *(const uint64_t*)a, j = *(const uint64_t*)b;
+  double xi, xj;
+  if (g_topk_f32) {
+    xi = fabs((double)((const float*)g_topk_x)[i]);
+    xj = fabs((double)((const float*)g_topk_x)[j]);
+  } else {
+    xi = fabs(((const double*)g_topk_x)[i]);
+    xj = fabs(((const double*)g_topk_x)[j]);
+  }
+  if (xi > xj) return -1;
+  if (xj > xi) return 1;
+  return i < j ? -1 : (i > j);
+}
+
+static int topk_any(const void* x, int is_f32, uint64_t d, double k_fraction, uint64_t* indices,
+                    uint64_t* k) {
+  int st = oc_sparsifier_k(d, k_fraction, k);
+  if (st) return st;
+  for (uint64_t i = 0; i < d; ++i) indices[i] = i;
+  g_topk_x = x;
+  g_topk_f32 = is_f32;
+  qsort(indices, d, sizeof(uint64_t), cmp_topk);
+  return OC_OK;
+}
+
+int oc_topk_f64(const double* x, uint64_t d, double k_fraction, uint64_t* indices, uint64_t* k) {
+  return topk_any(x, 0, d, k_fraction, indices, k);
+}
+int oc_topk_f32(const float* x, uint64_t d, double k_fraction, uint64_t* indices, uint64_t* k) {
+  return topk_any(x, 1, d, k_fraction, indices, k);
+}
+
+uint64_t oc_mix_seed(uint64_t seed, uint64_t tag) { return mix_seed(seed, tag); }
+
+static int cmp_u64(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : (x > y);
+}
+
+int oc_randomk(uint64_t d, double k_fraction, uint64_t seed, uint64_t* pool, uint64_t* k) {
+  int st = oc_sparsifier_k(d, k_fraction, k);
+  if (st) return st;
+  uint64_t state = seed; /* SplitMix64(seed) (rng.hpp:14) */
+  for (uint64_t i = 0; i < d; ++i) pool[i] = i;
+  for (uint64_t i = 0; i < *k; ++i) { /* compress.cpp:145-155 */
+    const uint64_t n = d - i;
+    const uint64_t threshold = (0ULL - n) % n; /* next_below, rng.hpp:27-34 */
+    uint64_t r;
+    do {
+      state += 0x9e3779b97f4a7c15ULL;
+      r = splitmix_out(state);
+    } while (r < threshold);
+    const uint64_t j = i + r % n;
+    const uint64_t t = pool[i];
+    pool[i] = pool[j];
+    pool[j] = t;
+  }
+  qsort(pool, *k, sizeof(uint64_t), cmp_u64);
+  return OC_OK;
+}
+
+/* ErrorFeedback::step (compress.cpp:323-344).  The kept gradient of one
+ * tensor is built in kept[begin, end) by the filter's keep(). */
+#define OC_FEEDBACK_BODY(T, TOPK)                                               \
+  if (f->kind < 0 || f->kind > 4) return OC_INVALID_INPUT;                      \
+  uint64_t sent = 0;                                                            \
+  uint8_t* keep = NULL;                                                         \
+  if (f->kind == 1) {                                                           \
+    keep = (uint8_t*)malloc(n_tensors ? n_tensors : 1);                         \
+    int st = oc_select(num_steps, f->interval, n_tensors, f->rule, keep);       \
+    if (st) { free(keep); return st; }                                          \
+  }                                                                             \
+  for (size_t t = 0; t < n_tensors; ++t) {                                      \
+    const uint64_t b = t_begin[t], e = t_end[t], d = e - b;                     \
+    T* c = kept + b; /* compensated, filtered in place below */                 \
+    for (uint64_t i = 0; i < d; ++i) {                                          \
+      T v = g[b + i];                                                           \
+      if (ef_enabled) {                                                         \
+        T prod = coeff * r[b + i];                                              \
+        v = v + prod;                                                           \
+      }                                                                         \
+      c[i] = v;                                                                 \
+    }                                                                           \
+    for (uint64_t i = 0; i < d; ++i) r[b + i] = c[i]; /* hold compensated */    \
+    if (f->kind == 0) {                                                         \
+      sent += d;                                                                \
+    } else if (f->kind == 1) {                                                  \
+      if (!keep[t])                                                             \
+        for (uint64_t i = 0; i < d; ++i) c[i] = (T)0;                           \
+      else                                                                      \
+        sent += d;                                                              \
+    } else if (f->kind == 4) {                                                  \
+      for (uint64_t i = 0; i < d; ++i) {                                        \
+        int sat = 0;                                                            \
+        const uint16_t h = oc_half_bits_from_float((float)c[i], &sat);          \
+        if (sat && saturations) ++*saturations;                                 \
+        c[i] = (T)oc_float_from_half_bits(h);                                   \
+      }                                                                         \
+      sent += d;                                                                \
+    } else {                                                                    \
+      uint64_t* idx = (uint64_t*)malloc((d ? d : 1) * sizeof(uint64_t));        \
+      uint64_t k = 0;                                                           \
+      int st = f->kind == 2                                                     \
+                   ? TOPK(r + b, d, f->k_fraction, idx, &k)                     \
+                   : oc_randomk(d, f->k_fraction,                               \
+                                mix_seed(f->seed, num_steps * 0x10001ULL + t), idx, &k); \
+      if (st) { free(idx); free(keep); return st; }                             \
+      for (uint64_t i = 0; i < d; ++i) c[i] = (T)0;                             \
+      for (uint64_t q = 0; q < k; ++q) c[idx[q]] = r[b + idx[q]];               \
+      free(idx);                                                                \
+      sent += k;                                                                \
+    }                                                                           \
+    for (uint64_t i = 0; i < d; ++i) r[b + i] = r[b + i] - c[i];                \
+  }                                                                             \
+  free(keep);                                                                   \
+  if (transmitted) *transmitted = sent;                                         \
+  return OC_OK;
+
+int oc_feedback_step_f64(const oc_filter* f, uint64_t num_steps, const double* g, double* r,
+                         size_t n_tensors, const uint64_t* t_begin, const uint64_t* t_end,
+                         int ef_enabled, double coeff, double* kept, uint64_t* transmitted,
+                         uint64_t* saturations) {
+  OC_FEEDBACK_BODY(double, oc_topk_f64)
+}
+
+int oc_feedback_step_f32(const oc_filter* f, uint64_t num_steps, const float* g, float* r,
+                         size_t n_tensors, const uint64_t* t_begin, const uint64_t* t_end,
+                         int ef_enabled, float coeff, float* kept, uint64_t* transmitted,
+                         uint64_t* saturations) {
+  OC_FEEDBACK_BODY(float, oc_topk_f32)
+}

@@ -57,6 +57,12 @@ def _ck(code, where):
         raise OracleError(code, where)
 
 
+class OcFilter(ctypes.Structure):
+    """oc_filter (covap_oracle.h)."""
+    _fields_ = [("kind", ctypes.c_int), ("interval", ctypes.c_uint32), ("rule", ctypes.c_int),
+                ("k_fraction", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
 class Oracle:
     def __init__(self, path=ORACLE_SO):
         if not os.path.exists(path):
@@ -189,6 +195,85 @@ class Oracle:
         _ck(self.d.oc_profile_ccr(_p(s, _f64), _p(e, _f64), W, C, comp_ms, ctypes.byref(a),
                                   _p(naive, _f64), ctypes.byref(c), ctypes.byref(k)), "profile")
         return a.value, naive.tolist(), c.value, k.value
+
+    # baseline compressors / error feedback ---------------
+    def sparsifier_k(self, d, k_fraction):
+        k = ctypes.c_uint64()
+        self.d.oc_sparsifier_k.argtypes = [ctypes.c_uint64, ctypes.c_double, _u64]
+        _ck(self.d.oc_sparsifier_k(d, k_fraction, ctypes.byref(k)), "sparsifier_k")
+        return k.value
+
+    def half_bits(self, v):
+        self.d.oc_half_bits_from_float.restype = ctypes.c_uint16
+        self.d.oc_half_bits_from_float.argtypes = [ctypes.c_float, ctypes.POINTER(ctypes.c_int)]
+        sat = ctypes.c_int(0)
+        h = self.d.oc_half_bits_from_float(float(v), ctypes.byref(sat))
+        return h, bool(sat.value)
+
+    def float_from_half(self, h):
+        self.d.oc_float_from_half_bits.restype = ctypes.c_float
+        self.d.oc_float_from_half_bits.argtypes = [ctypes.c_uint16]
+        return self.d.oc_float_from_half_bits(int(h))
+
+    def fp16_roundtrip(self, x):
+        x = np.ascontiguousarray(x)
+        out = np.empty_like(x)
+        sat = ctypes.c_uint64(0)
+        if x.dtype == np.float32:
+            self.d.oc_fp16_roundtrip_f32.argtypes = [_f32, ctypes.c_uint64, _f32, _u64]
+            self.d.oc_fp16_roundtrip_f32(_p(x, _f32), len(x), _p(out, _f32), ctypes.byref(sat))
+        else:
+            self.d.oc_fp16_roundtrip_f64.argtypes = [_f64, ctypes.c_uint64, _f64, _u64]
+            self.d.oc_fp16_roundtrip_f64(_p(x, _f64), len(x), _p(out, _f64), ctypes.byref(sat))
+        return out, sat.value
+
+    def topk(self, x, k_fraction):
+        """(indices in the reference's order, values)."""
+        x = np.ascontiguousarray(x)
+        idx = np.zeros(max(len(x), 1), np.uint64)
+        k = ctypes.c_uint64()
+        if x.dtype == np.float32:
+            self.d.oc_topk_f32.argtypes = [_f32, ctypes.c_uint64, ctypes.c_double, _u64, _u64]
+            _ck(self.d.oc_topk_f32(_p(x, _f32), len(x), k_fraction, _p(idx, _u64),
+                                   ctypes.byref(k)), "topk")
+        else:
+            self.d.oc_topk_f64.argtypes = [_f64, ctypes.c_uint64, ctypes.c_double, _u64, _u64]
+            _ck(self.d.oc_topk_f64(_p(x, _f64), len(x), k_fraction, _p(idx, _u64),
+                                   ctypes.byref(k)), "topk")
+        i = idx[:k.value].copy()
+        return i, x[i]
+
+    def randomk(self, d, k_fraction, seed):
+        idx = np.zeros(max(d, 1), np.uint64)
+        k = ctypes.c_uint64()
+        self.d.oc_randomk.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_uint64, _u64, _u64]
+        _ck(self.d.oc_randomk(d, k_fraction, ctypes.c_uint64(seed), _p(idx, _u64),
+                              ctypes.byref(k)), "randomk")
+        return idx[:k.value].copy()
+
+    def mix_seed(self, seed, tag):
+        self.d.oc_mix_seed.restype = ctypes.c_uint64
+        self.d.oc_mix_seed.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        return self.d.oc_mix_seed(seed, tag)
+
+    def feedback_step(self, kind, num_steps, g, r, tensors, ef_enabled, coeff, interval=1,
+                      rule=0, k_fraction=0.01, seed=0):
+        """ErrorFeedback::step; r updated in place; returns (kept, transmitted, saturations)."""
+        f = OcFilter(kind, interval, rule, k_fraction, seed)
+        tb = _arr([t[1] for t in tensors], np.uint64)
+        te = _arr([t[2] for t in tensors], np.uint64)
+        kept = np.zeros_like(g)
+        sent, sat = ctypes.c_uint64(), ctypes.c_uint64(0)
+        if g.dtype == np.float32:
+            fn, pt, c = self.d.oc_feedback_step_f32, _f32, ctypes.c_float(np.float32(coeff).item())
+        else:
+            fn, pt, c = self.d.oc_feedback_step_f64, _f64, ctypes.c_double(float(coeff))
+        fn.argtypes = [ctypes.POINTER(OcFilter), ctypes.c_uint64, pt, pt, _sz, _u64, _u64,
+                       ctypes.c_int, type(c), pt, _u64, _u64]
+        _ck(fn(ctypes.byref(f), num_steps, _p(g, pt), _p(r, pt), len(tensors), _p(tb, _u64),
+               _p(te, _u64), int(ef_enabled), c, _p(kept, pt), ctypes.byref(sent),
+               ctypes.byref(sat)), "feedback_step")
+        return kept, sent.value, sat.value
 
     # inputs --------------------------------------------------------------
     def stream_key(self, seed, rank, step):
@@ -332,6 +417,49 @@ class Ref:
                 "comm_tensor": ct[:k].tolist(), "bubble_after": ba[:b].tolist(),
                 "bubble_ms": bm[:b].tolist()}
 
+    # baseline compressors / error feedback (compress.cpp:107-344) ---------
+    def topk(self, x, k_fraction):
+        x = np.ascontiguousarray(x, np.float64)
+        idx = np.zeros(max(len(x), 1), np.uint64)
+        val = np.zeros(max(len(x), 1))
+        k = _sz()
+        self.d.ref_topk.argtypes = [_f64, _sz, ctypes.c_double, _u64, _f64, ctypes.POINTER(_sz)]
+        _ck(self.d.ref_topk(_p(x, _f64), len(x), k_fraction, _p(idx, _u64), _p(val, _f64),
+                            ctypes.byref(k)), "ref_topk")
+        return idx[:k.value].copy(), val[:k.value].copy()
+
+    def randomk(self, x, k_fraction, seed):
+        x = np.ascontiguousarray(x, np.float64)
+        idx = np.zeros(max(len(x), 1), np.uint64)
+        val = np.zeros(max(len(x), 1))
+        k = _sz()
+        self.d.ref_randomk.argtypes = [_f64, _sz, ctypes.c_double, ctypes.c_uint64, _u64, _f64,
+                                       ctypes.POINTER(_sz)]
+        _ck(self.d.ref_randomk(_p(x, _f64), len(x), k_fraction, ctypes.c_uint64(seed),
+                               _p(idx, _u64), _p(val, _f64), ctypes.byref(k)), "ref_randomk")
+        return idx[:k.value].copy(), val[:k.value].copy()
+
+    def fp16_roundtrip(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.empty_like(x)
+        sat = ctypes.c_uint64()
+        self.d.ref_fp16_roundtrip.argtypes = [_f64, _sz, _f64, _u64]
+        _ck(self.d.ref_fp16_roundtrip(_p(x, _f64), len(x), _p(out, _f64), ctypes.byref(sat)),
+            "ref_fp16")
+        return out, sat.value
+
+    def half_bits(self, v):
+        self.d.ref_half_bits.restype = ctypes.c_uint16
+        self.d.ref_half_bits.argtypes = [ctypes.c_float, ctypes.POINTER(ctypes.c_int)]
+        sat = ctypes.c_int(0)
+        h = self.d.ref_half_bits(float(v), ctypes.byref(sat))
+        return h, bool(sat.value)
+
+    def float_from_half(self, h):
+        self.d.ref_float_from_half.restype = ctypes.c_float
+        self.d.ref_float_from_half.argtypes = [ctypes.c_uint16]
+        return self.d.ref_float_from_half(int(h))
+
     def profile_ccr(self, starts, ends, comp_ms, expected=None):
         s = _arr(starts, np.float64)
         e = _arr(ends, np.float64)
@@ -369,4 +497,40 @@ class RefSession:
     def close(self):
         if self.h:
             self.ref.d.ref_session_destroy(self.h)
+            self.h = None
+
+
+class RefFeedback:
+    """The reference's ErrorFeedback around one GradientFilter
+    (compress.cpp:241-344).  kind: 0 identity, 1 covap, 2 topk, 3 randomk, 4 fp16."""
+
+    def __init__(self, ref, numels, kind, interval=1, rule=0, k_fraction=0.01, seed=0,
+                 ef=(1, 0.3, 100, 0.1)):
+        self.ref = ref
+        self.numels = list(numels)
+        self.d = int(sum(numels))
+        nv = _arr(numels, np.uint64)
+        f = ref.d
+        f.ref_feedback_create.restype = ctypes.c_void_p
+        f.ref_feedback_create.argtypes = [_u64, _sz, ctypes.c_int, ctypes.c_uint32, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_uint64, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_uint64, ctypes.c_double]
+        f.ref_feedback_destroy.argtypes = [ctypes.c_void_p]
+        f.ref_feedback_step.argtypes = [ctypes.c_void_p, _f64, _f64, _f64, _u64, _f64]
+        self.h = f.ref_feedback_create(_p(nv, _u64), len(nv), kind, interval, rule, k_fraction,
+                                       ctypes.c_uint64(seed), int(ef[0]), float(ef[1]),
+                                       int(ef[2]), float(ef[3]))
+
+    def step(self, g):
+        """Returns (kept, residual, transmitted elements, seconds)."""
+        g = np.ascontiguousarray(g, np.float64)
+        kept, res = np.empty(self.d), np.empty(self.d)
+        sent, sec = ctypes.c_uint64(), ctypes.c_double()
+        _ck(self.ref.d.ref_feedback_step(self.h, _p(g, _f64), _p(kept, _f64), _p(res, _f64),
+                                         ctypes.byref(sent), ctypes.byref(sec)), "ref_feedback")
+        return kept, res, sent.value, sec.value
+
+    def close(self):
+        if self.h:
+            self.ref.d.ref_feedback_destroy(self.h)
             self.h = None

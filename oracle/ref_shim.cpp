@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <vector>
 
 #include "covap/compress.hpp"
@@ -306,6 +307,112 @@ int ref_overlap_schedule(double before, const double* comp, const double* compre
     for (std::size_t i = 0; i < sc.bubbles.size(); ++i) {
       bubble_after[i] = sc.bubbles[i].after_tensor;
       bubble_ms[i] = sc.bubbles[i].duration_ms;
+    }
+  })
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Baseline compressors and the generic error-feedback wrapper.
+extern "C" {
+
+// topk_compress (compress.cpp:119-133): indices in the reference's order
+// (largest magnitude first, ties to the lower index) and their values.
+int ref_topk(const double* x, std::size_t d, double k_fraction, std::uint64_t* indices,
+             double* values, std::size_t* k) {
+  GUARD({
+    const auto s = topk_compress(std::span<const double>(x, d), k_fraction);
+    *k = s.indices.size();
+    for (std::size_t i = 0; i < s.indices.size(); ++i) {
+      indices[i] = s.indices[i];
+      values[i] = s.values[i];
+    }
+  })
+}
+
+// randomk_compress (compress.cpp:135-143): ascending indices.
+int ref_randomk(const double* x, std::size_t d, double k_fraction, std::uint64_t seed,
+                std::uint64_t* indices, double* values, std::size_t* k) {
+  GUARD({
+    const auto s = randomk_compress(std::span<const double>(x, d), k_fraction, seed);
+    *k = s.indices.size();
+    for (std::size_t i = 0; i < s.indices.size(); ++i) {
+      indices[i] = s.indices[i];
+      values[i] = s.values[i];
+    }
+  })
+}
+
+// fp16_roundtrip (compress.cpp:226-236) and half_bits_from_float (157-205).
+int ref_fp16_roundtrip(const double* x, std::size_t n, double* out, std::uint64_t* saturated) {
+  GUARD({
+    std::uint64_t sat = 0;
+    const auto y = fp16_roundtrip(std::span<const double>(x, n), &sat);
+    for (std::size_t i = 0; i < n; ++i) out[i] = y[i];
+    if (saturated) *saturated = sat;
+  })
+}
+
+std::uint16_t ref_half_bits(float v, int* saturated) {
+  bool s = false;
+  const std::uint16_t h = half_bits_from_float(v, &s);
+  if (saturated) *saturated = s ? 1 : 0;
+  return h;
+}
+
+float ref_float_from_half(std::uint16_t h) { return float_from_half_bits(h); }
+
+// ErrorFeedback (compress.cpp:316-344) around one GradientFilter
+// (compress.cpp:241-314).  kind: 0 identity, 1 covap, 2 topk, 3 randomk, 4 fp16.
+struct RefFeedback {
+  std::vector<std::uint64_t> numels;
+  std::unique_ptr<GradientFilter> filter;
+  std::unique_ptr<ErrorFeedback> ef;
+};
+
+void* ref_feedback_create(const std::uint64_t* numels, std::size_t n, int kind,
+                          std::uint32_t interval, int rule, double k_fraction,
+                          std::uint64_t seed, int ef_enabled, double init, std::uint64_t ascend,
+                          double range) {
+  auto* s = new RefFeedback;
+  s->numels.assign(numels, numels + n);
+  switch (kind) {
+    case 0: s->filter = std::make_unique<IdentityFilter>(); break;
+    case 1:
+      s->filter = std::make_unique<CovapFilter>(
+          interval, rule ? SelectionRule::kPlusStep : SelectionRule::kMatchStep);
+      break;
+    case 2: s->filter = std::make_unique<TopkFilter>(k_fraction); break;
+    case 3: s->filter = std::make_unique<RandomkFilter>(k_fraction, seed); break;
+    default: s->filter = std::make_unique<Fp16Filter>(); break;
+  }
+  s->ef = std::make_unique<ErrorFeedback>(s->numels,
+                                          EfSchedule{ef_enabled != 0, init, ascend, range});
+  return s;
+}
+
+void ref_feedback_destroy(void* h) { delete static_cast<RefFeedback*>(h); }
+
+// One ErrorFeedback::step on a flat gradient; kept and the residual come back
+// flat.  *transmitted = filter.transmitted_elements(g, step) (trainer.cpp:397).
+int ref_feedback_step(void* h, const double* g, double* kept, double* residual,
+                      std::uint64_t* transmitted, double* seconds) {
+  auto* s = static_cast<RefFeedback*>(h);
+  GUARD({
+    const GradientSet gs = split(g, s->numels);
+    const std::uint64_t step = s->ef->num_steps();
+    const auto t0 = std::chrono::steady_clock::now();
+    const GradientSet k = s->ef->step(gs, *s->filter);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (transmitted) *transmitted = s->filter->transmitted_elements(gs, step);
+    std::uint64_t off = 0;
+    for (std::size_t t = 0; t < k.size(); ++t) {
+      std::memcpy(kept + off, k[t].data(), k[t].size() * sizeof(double));
+      if (residual)
+        std::memcpy(residual + off, s->ef->residuals()[t].data(), k[t].size() * sizeof(double));
+      off += k[t].size();
     }
   })
 }
