@@ -326,6 +326,101 @@ covap_status covap_embed(int device, int dtype, const void* payload, void* out, 
 covap_status covap_mean_rows(int device, int dtype, const void* rows, void* out, uint64_t P,
                              uint64_t n, void* stream);
 
+/* ------------------------------- baseline compressors under error feedback --
+ * SURVEY.md §8(f4).  The reference's GradientFilter family and ErrorFeedback
+ * wrapper (compress.hpp:66-164, compress.cpp:107-344) and the non-COVAP
+ * branch of train() (trainer.cpp:387-403), on the device.  A covap_feedback
+ * owns one worker's residuals (ErrorFeedback::residuals_) over a list of
+ * tensors laid out back to back, plus the scratch its filter needs. */
+
+enum {
+  COVAP_FILTER_IDENTITY = 0, /* IdentityFilter        compress.hpp:106-110 */
+  COVAP_FILTER_COVAP = 1,    /* CovapFilter           compress.hpp:112-120 */
+  COVAP_FILTER_TOPK = 2,     /* TopkFilter            compress.hpp:122-130 */
+  COVAP_FILTER_RANDOMK = 3,  /* RandomkFilter         compress.hpp:132-141 */
+  COVAP_FILTER_FP16 = 4      /* Fp16Filter            compress.hpp:143-147 */
+};
+
+typedef struct covap_filter {
+  int kind;          /* COVAP_FILTER_* */
+  uint32_t interval; /* covap: K */
+  int rule;          /* covap: 0 kMatchStep, 1 kPlusStep */
+  double k_fraction; /* topk / randomk: (0, 1] */
+  uint64_t seed;     /* randomk: RandomkFilter's seed (per tensor: mix_seed(seed, step*0x10001+t)) */
+} covap_filter;
+
+typedef struct covap_feedback covap_feedback;
+
+/* ErrorFeedback(numels, schedule) with its filter; residuals zero.
+ * InvalidInput: empty tensor list or an empty tensor for top-k / random-k
+ * (sparsifier_k, compress.cpp:109), k_fraction outside (0, 1], K < 1, more
+ * than 2^32 - 1 elements. */
+covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int dtype,
+                                   const covap_ef* schedule, const covap_filter* filter,
+                                   int device, covap_feedback** out);
+void covap_feedback_destroy(covap_feedback* fb);
+covap_status covap_feedback_residual(covap_feedback* fb, void** dev_ptr, uint64_t* n);
+covap_status covap_feedback_get_step(const covap_feedback* fb, uint64_t* num_steps);
+covap_status covap_feedback_set_step(covap_feedback* fb, uint64_t num_steps);
+/* Zero the residuals and num_steps (stream-ordered). */
+covap_status covap_feedback_reset(covap_feedback* fb, void* stream);
+
+/* ErrorFeedback::step (compress.cpp:323-344): kept (dense, device) =
+ * filter.keep(grad + coeff*residual, num_steps); residual = compensated -
+ * kept; ++num_steps.  Stream-ordered, no host synchronisation. */
+covap_status covap_feedback_step(covap_feedback* fb, const void* grad, void* kept, void* stream);
+
+/* GradientFilter::transmitted_elements at `step` (compress.cpp:246-314) and
+ * the wire bytes train() accounts for it (trainer.cpp:396-400: 2 B per
+ * element for fp16, 8 B per index+value pair for the sparsifiers). */
+covap_status covap_feedback_transmitted(const covap_feedback* fb, uint64_t step,
+                                        uint64_t* elements, uint64_t* wire_bytes);
+
+/* fp16 values clamped to +-65504 since creation (fp16_roundtrip's
+ * saturation_count).  Synchronises the stream. */
+covap_status covap_feedback_saturations(covap_feedback* fb, uint64_t* count, void* stream);
+
+/* One synchronisation step of the non-COVAP branch of train()
+ * (trainer.cpp:387-403): the error-feedback step on this rank's gradient,
+ * the exchange of the wire payload over `comm` (NULL = one rank) and
+ * out = allreduce_mean of every rank's kept gradient, summed in rank order
+ * (trainer.cpp:35-47) so the result is bit-identical on every rank.  Wire:
+ * fp16 = 2 B per element (all-gather of halves); top-k = (uint32 index,
+ * value) pairs (all-gather, scatter-add in rank order); random-k = values
+ * only (indices are identical on every rank).  Filters top-k / random-k /
+ * fp16; ++num_steps. */
+covap_status covap_feedback_sync_step(covap_feedback* fb, covap_comm* comm, const void* grad,
+                                      void* out, void* stream);
+
+/* The two halves of covap_feedback_sync_step for callers with their own
+ * transport (and for virtual-rank tests): pack runs the error-feedback step
+ * and leaves the wire payload in the buffers covap_feedback_wire returns
+ * (a: fp16 halves or uint32 indices, b: values; NULL when unused); combine
+ * writes out = the rank-ordered mean of P ranks' payloads laid out rank-major
+ * (recv_a: P x bytes_a, recv_b: P x bytes_b).  pack zero-fills out first, so
+ * pass the same out to both. */
+covap_status covap_feedback_pack(covap_feedback* fb, const void* grad, void* out, void* stream);
+covap_status covap_feedback_wire(covap_feedback* fb, void** a, uint64_t* bytes_a, void** b,
+                                 uint64_t* bytes_b);
+covap_status covap_feedback_combine(covap_feedback* fb, const void* recv_a, const void* recv_b,
+                                    int P, void* out, void* stream);
+
+/* The standalone compressors (compress.hpp:66-89) on a device vector.
+ * topk: k = sparsifier_k(d) indices by |x| descending, ties to the lower
+ * index, and their values; randomk: k indices sampled without replacement
+ * from SplitMix64(seed), ascending.  indices (uint64) / values hold d
+ * entries.  fp16_roundtrip: out = widen(half(x)), *saturations += clamps.
+ * All blocking (the count comes back to the host). */
+covap_status covap_sparsifier_k(uint64_t d, double k_fraction, uint64_t* k);
+covap_status covap_topk_compress(int device, int dtype, const void* x, uint64_t d,
+                                 double k_fraction, uint64_t* indices, void* values, uint64_t* k,
+                                 void* stream);
+covap_status covap_randomk_compress(int device, int dtype, const void* x, uint64_t d,
+                                    double k_fraction, uint64_t seed, uint64_t* indices,
+                                    void* values, uint64_t* k, void* stream);
+covap_status covap_fp16_roundtrip(int device, int dtype, const void* x, uint64_t n, void* out,
+                                  uint64_t* saturations, void* stream);
+
 /* ------------------------------------------------------ harness kernels -- */
 
 /* K0: synthetic gradients, element i = generator(key, begin + i); the

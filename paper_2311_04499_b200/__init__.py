@@ -2,7 +2,8 @@
 
 The product is ``libcovap_b200.so`` (sm_100a kernels + NCCL + host planner,
 C-ABI in ``include/covap_c.h``); this package is its Python host mirror of
-the reference API (``covap.py``).  Importing it loads the shared library and
+the reference API (``covap.py``; the baseline compressors under error
+feedback in ``feedback.py``).  Importing it loads the shared library and
 fails loudly when it is missing: there is no CPU fallback.
 """
 from .errors import (ConfigError, CudaError, Error, IncompleteProfile, InvalidInput,  # noqa: F401
@@ -15,5 +16,9 @@ from .covap import (BucketPlan, CompressedUpdate, CompressorState, Communicator,
                     covap_compress, covap_decompress, ef_coefficient, effective_numels,
                     effective_tensors, generate, load_layout, median_numel, plan_for,
                     profile_ccr, select_tensors, shard_plan, spin, stream_key)
+from . import feedback  # noqa: F401
+from .feedback import (CovapFilter, ErrorFeedback, Fp16Filter, IdentityFilter,  # noqa: F401
+                       RandomkFilter, TopkFilter, fp16_roundtrip, randomk_compress, sparsifier_k,
+                       topk_compress)
 
 _lib.lib()  # load now: a missing extension is an import error, not a silent fallback

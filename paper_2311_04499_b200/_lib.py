@@ -46,6 +46,11 @@ class BucketRangeC(ctypes.Structure):
                 ("sel_end", u64), ("send_offset", u64), ("device_begin", u64)]
 
 
+class FilterC(ctypes.Structure):
+    _fields_ = [("kind", i32), ("interval", u32), ("rule", i32), ("k_fraction", f64),
+                ("seed", u64)]
+
+
 # name -> (restype, argtypes); restype None means covap_status (int) checked.
 _SIGS = {
     "covap_last_error": (ctypes.c_char_p, []),
@@ -115,6 +120,25 @@ _SIGS = {
     "covap_stream_synchronize": (None, [vp]),
     "covap_embed": (None, [i32, i32, vp, vp, u64, u64p, u64p, u64p, sz, f64, i32, vp]),
     "covap_mean_rows": (None, [i32, i32, vp, vp, u64, u64, vp]),
+    # baseline compressors under error feedback
+    "covap_feedback_create": (None, [u64p, sz, i32, ctypes.POINTER(EfC), ctypes.POINTER(FilterC),
+                                     i32, ctypes.POINTER(vp)]),
+    "covap_feedback_destroy": ("void", [vp]),
+    "covap_feedback_residual": (None, [vp, ctypes.POINTER(vp), u64p]),
+    "covap_feedback_get_step": (None, [vp, u64p]),
+    "covap_feedback_set_step": (None, [vp, u64]),
+    "covap_feedback_reset": (None, [vp, vp]),
+    "covap_feedback_step": (None, [vp, vp, vp, vp]),
+    "covap_feedback_transmitted": (None, [vp, u64, u64p, u64p]),
+    "covap_feedback_saturations": (None, [vp, u64p, vp]),
+    "covap_feedback_sync_step": (None, [vp, vp, vp, vp, vp]),
+    "covap_feedback_pack": (None, [vp, vp, vp, vp]),
+    "covap_feedback_wire": (None, [vp, ctypes.POINTER(vp), u64p, ctypes.POINTER(vp), u64p]),
+    "covap_feedback_combine": (None, [vp, vp, vp, i32, vp, vp]),
+    "covap_sparsifier_k": (None, [u64, f64, u64p]),
+    "covap_topk_compress": (None, [i32, i32, vp, u64, f64, vp, vp, u64p, vp]),
+    "covap_randomk_compress": (None, [i32, i32, vp, u64, f64, u64, vp, vp, u64p, vp]),
+    "covap_fp16_roundtrip": (None, [i32, i32, vp, u64, vp, u64p, vp]),
     "covap_stream_key": (u64, [u64, u64, u64]),
     "covap_generate": (None, [vp, u64, i32, u64, i32, u64, vp]),
     "covap_spin": (None, [f64, i32, vp]),

@@ -25,17 +25,12 @@
 #include "covap/errors.hpp"
 #include "covap_internal.h"
 #include "covap_plan.hpp"
+#include "covap_capi_common.hpp"
 
 struct covap_plan {
   covapb::Plan p;
 };
 
-struct covap_comm {
-  ncclComm_t nccl = nullptr;
-  int nranks = 1;
-  int rank = 0;
-  int device = 0;
-};
 
 struct covap_state {
   covapb::Plan plan;
@@ -63,100 +58,14 @@ struct covap_state {
   bool fuse_single_rank = true;                 // P = 1: run K1F instead of K1 -> C1 -> K2
 };
 
+namespace covapb {
+thread_local std::string g_last_error;
+}  // namespace covapb
+
 namespace {
 
-thread_local std::string g_last_error;
 constexpr int kChunkEvents = 64;
 
-covap_status fail(covap_status code, const std::string& msg) {
-  g_last_error = msg;
-  return code;
-}
-
-covap_status from_exception() {
-  try {
-    throw;
-  } catch (const covap::InvalidInput& e) {
-    return fail(COVAP_ERR_INVALID_INPUT, e.what());
-  } catch (const covap::InvalidState& e) {
-    return fail(COVAP_ERR_INVALID_STATE, e.what());
-  } catch (const covap::UndefinedRatio& e) {
-    return fail(COVAP_ERR_UNDEFINED_RATIO, e.what());
-  } catch (const covap::IncompleteProfile& e) {
-    return fail(COVAP_ERR_INCOMPLETE_PROFILE, e.what());
-  } catch (const covap::ConfigError& e) {
-    return fail(COVAP_ERR_CONFIG, e.what());
-  } catch (const covap::Error& e) {
-    return fail(COVAP_ERR_GENERIC, e.what());
-  } catch (const std::bad_alloc&) {
-    return fail(COVAP_ERR_GENERIC, "host allocation failed");
-  } catch (const std::exception& e) {
-    return fail(COVAP_ERR_GENERIC, e.what());
-  } catch (...) {
-    return fail(COVAP_ERR_GENERIC, "unknown error");
-  }
-}
-
-struct CudaError {
-  cudaError_t e;
-  const char* where;
-};
-struct NcclError {
-  ncclResult_t r;
-  const char* where;
-};
-
-#define CK(x)                                            \
-  do {                                                   \
-    cudaError_t _e = (x);                                \
-    if (_e != cudaSuccess) throw CudaError{_e, #x};      \
-  } while (0)
-#define NK(x)                                            \
-  do {                                                   \
-    ncclResult_t _r = (x);                               \
-    if (_r != ncclSuccess) throw NcclError{_r, #x};      \
-  } while (0)
-
-// Runs body; maps every failure onto a status code + message.
-template <typename F>
-covap_status guarded(F&& body) {
-  try {
-    body();
-    return COVAP_OK;
-  } catch (const CudaError& ce) {
-    return fail(ce.e == cudaErrorNoDevice || ce.e == cudaErrorInsufficientDriver
-                    ? COVAP_ERR_NO_DEVICE
-                    : COVAP_ERR_CUDA,
-                std::string(ce.where) + ": " + cudaGetErrorString(ce.e));
-  } catch (const NcclError& ne) {
-    return fail(COVAP_ERR_NCCL, std::string(ne.where) + ": " + ncclGetErrorString(ne.r));
-  } catch (...) {
-    return from_exception();
-  }
-}
-
-// Restores the caller's current device on scope exit.
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    CK(cudaSetDevice(dev));
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-void need(bool cond, const char* msg) {
-  if (!cond) throw covap::InvalidInput(msg);
-}
-
-void need_aligned(const void* p, const char* what) {
-  if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
-    throw covap::InvalidInput(std::string(what) + " must be 16-byte aligned");
-}
-
-inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 const covapb::Phase& phase_of(const covapb::Plan& p, uint64_t step) {
   return p.phases[step % p.interval];
@@ -168,9 +77,6 @@ double coeff_of(const covap_state* s) {
                        : 0.0;
 }
 
-ncclDataType_t nccl_type(int dtype) { return dtype == COVAP_F64 ? ncclFloat64 : ncclFloat32; }
-
-int world(const covap_comm* c) { return c ? c->nranks : 1; }
 
 void k1_range(covap_state* s, const void* grad, void* send, uint64_t a, uint64_t b,
               cudaStream_t st) {

@@ -1,0 +1,893 @@
+// covap_feedback.cu — sm_100a kernels for the baseline compressors under the
+// generic error-feedback wrapper.
+//
+//   dense      identity / covap / fp16 filter in one pass: c = g + coeff*r,
+//              kept = f(c), r = c - kept, fp16 wire bits    (compress.cpp:323-344)
+//   compensate sparsifier pass 1: r = c, out = 0, per-tensor histogram of |c|
+//   topk_*     exact top-k per tensor: threshold bin from the histogram, one
+//              collect pass over c, radix select among the threshold-bin
+//              candidates by (|c| desc, index asc)         (compress.cpp:119-133)
+//   randomk_*  sample_without_replacement (compress.cpp:145-155) in parallel:
+//              draws are counter-based splitmix64 outputs; the partial
+//              Fisher-Yates swap chain is resolved with per-position lists
+//   *_mean     the mean of the kept gradients over P ranks, in rank order
+//              (trainer.cpp:35-47, 402): fp16 wire widened and summed; sparse
+//              lists scattered into an accumulator
+//
+// Arithmetic follows the reference operation by operation with FMA
+// contraction disabled (__fmul_rn / __fadd_rn / __fsub_rn), so the fp64
+// instantiation is bit-exact against the reference and the fp32 one against
+// the same sequence in single precision (the tests' fp32 restatement).
+#include <cub/cub.cuh>
+
+#include "covap_feedback.h"
+
+namespace covapb {
+namespace fb {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 8;
+constexpr int kDigitBits = 11;
+constexpr int kDigits = 1 << kDigitBits;
+
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T>
+struct KeyOf;
+template <>
+struct KeyOf<float> {
+  using K = uint32_t;
+  static constexpr int kBits = 31;  // |x| bit pattern: order == magnitude order
+  static __device__ __forceinline__ K key(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+};
+template <>
+struct KeyOf<double> {
+  using K = uint64_t;
+  static constexpr int kBits = 63;
+  static __device__ __forceinline__ K key(double x) {
+    return static_cast<uint64_t>(__double_as_longlong(x)) & 0x7fffffffffffffffull;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t bin_of(T c) {
+  return static_cast<uint32_t>(KeyOf<T>::key(c) >> (KeyOf<T>::kBits - kBinBits));
+}
+
+// half_bits_from_float (compress.cpp:157-205): round to nearest even,
+// saturate to +-65504, NaN -> 0x7e00, below 2^-24 -> signed zero.
+__device__ __forceinline__ uint16_t half_bits(float value, bool& saturated) {
+  const uint32_t bits = __float_as_uint(value);
+  const uint32_t sign = (bits >> 16) & 0x8000u;
+  const uint32_t abs_bits = bits & 0x7fffffffu;
+  if (abs_bits > 0x7f800000u) return static_cast<uint16_t>(sign | 0x7e00u);
+  if (__uint_as_float(abs_bits) > 65504.0f) {
+    saturated = true;
+    return static_cast<uint16_t>(sign | 0x7bffu);
+  }
+  const int32_t e = static_cast<int32_t>((abs_bits >> 23) & 0xff) - 127;
+  uint32_t mant = abs_bits & 0x7fffffu;
+  if (e < -24) return static_cast<uint16_t>(sign);
+  if (e < -14) {
+    mant |= 0x800000u;
+    const uint32_t shift = static_cast<uint32_t>(-14 - e) + 13;
+    const uint32_t hm = mant >> shift;
+    const uint32_t rest = mant & ((1u << shift) - 1);
+    const uint32_t halfway = 1u << (shift - 1);
+    const uint32_t rounded = hm + ((rest > halfway || (rest == halfway && (hm & 1u))) ? 1u : 0u);
+    return static_cast<uint16_t>(sign | rounded);
+  }
+  uint32_t he = static_cast<uint32_t>(e + 15);
+  uint32_t hm = mant >> 13;
+  const uint32_t rest = mant & 0x1fffu;
+  if (rest > 0x1000u || (rest == 0x1000u && (hm & 1u))) {
+    ++hm;
+    if (hm == 0x400u) {
+      hm = 0;
+      ++he;
+    }
+  }
+  if (he >= 31) {
+    saturated = true;
+    return static_cast<uint16_t>(sign | 0x7bffu);
+  }
+  return static_cast<uint16_t>(sign | (he << 10) | hm);
+}
+
+// float_from_half_bits (compress.cpp:207-224).
+__device__ __forceinline__ float half_to_float(uint16_t h) {
+  const uint32_t sign = static_cast<uint32_t>(h & 0x8000u) << 16;
+  const uint32_t e = (h >> 10) & 0x1fu;
+  const uint32_t m = h & 0x3ffu;
+  if (e == 0) {
+    if (m == 0) return __uint_as_float(sign);
+    const int s = __clz(m) - 21;  // shifts until bit 10 is set
+    const uint32_t mm = (m << s) & 0x3ffu;
+    return __uint_as_float(sign | (static_cast<uint32_t>(-14 - s + 127) << 23) | (mm << 13));
+  }
+  if (e == 31) return __uint_as_float(sign | 0x7f800000u | (m << 13));
+  return __uint_as_float(sign | ((e - 15 + 127) << 23) | (m << 13));
+}
+
+__device__ __forceinline__ uint64_t splitmix_out(uint64_t z) {  // rng.hpp:17-20
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t tag) {  // rng.hpp:58-63
+  return splitmix_out((seed ^ (0x632be59bd9b4e019ULL + tag * 0x9e3779b97f4a7c15ULL)) +
+                      0x9e3779b97f4a7c15ULL);
+}
+
+// Warp-aggregated append: returns this lane's slot (valid when pred).
+__device__ __forceinline__ uint32_t append_slot(bool pred, uint32_t* counter) {
+  const unsigned mask = __ballot_sync(0xffffffffu, pred);
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (mask) {
+    const int leader = __ffs(mask) - 1;
+    if (lane == leader) base = atomicAdd(counter, static_cast<uint32_t>(__popc(mask)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+  }
+  return base + static_cast<uint32_t>(__popc(mask & ((1u << lane) - 1u)));
+}
+
+template <typename T>
+__device__ __forceinline__ T compensate(T g, T r, T coeff, int ef) {
+  return ef ? add_rn(g, mul_rn(coeff, r)) : g;  // compress.cpp:332-336
+}
+
+// ---------------------------------------------------------------- dense
+
+template <typename T, int KIND>
+__global__ void __launch_bounds__(kThreads) dense_kernel(DenseArgs A) {
+  const T* __restrict__ g = static_cast<const T*>(A.g);
+  T* __restrict__ r = static_cast<T*>(A.r);
+  T* __restrict__ kept = static_cast<T*>(A.kept);
+  const T coeff = static_cast<T>(A.coeff);
+  unsigned long long nsat = 0;
+  for (uint32_t ci = blockIdx.x; ci < A.nchunks; ci += gridDim.x) {
+    const Chunk ch = A.chunks[ci];
+    bool sel = true;
+    if (KIND == kCovap) {  // select_tensors (compress.cpp:13-28)
+      const uint64_t phase = A.step % A.interval, rem = ch.tensor % A.interval;
+      sel = A.rule ? ((rem + phase) % A.interval == 0) : (rem == phase);
+    }
+    for (uint64_t base = ch.begin; base < ch.end; base += kThreads * kUnroll) {
+      T gv[kUnroll], rv[kUnroll];
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const uint64_t i = base + q * kThreads + threadIdx.x;
+        if (i < ch.end) {
+          gv[q] = g[i];
+          rv[q] = A.ef ? r[i] : T(0);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const uint64_t i = base + q * kThreads + threadIdx.x;
+        if (i >= ch.end) continue;
+        const T c = compensate(gv[q], rv[q], coeff, A.ef);
+        T k;
+        if (KIND == kFp16) {
+          bool s = false;
+          const uint16_t h = half_bits(static_cast<float>(c), s);
+          nsat += s ? 1 : 0;
+          k = static_cast<T>(half_to_float(h));
+          if (A.wire) A.wire[i] = h;
+        } else if (KIND == kCovap) {
+          k = sel ? c : T(0);
+        } else {
+          k = c;
+        }
+        if (kept) kept[i] = k;
+        if (r) r[i] = sub_rn(c, k);  // residual = compensated - kept (compress.cpp:339-341)
+      }
+    }
+  }
+  if (KIND == kFp16 && A.sat) {
+    for (int o = 16; o > 0; o >>= 1) nsat += __shfl_xor_sync(0xffffffffu, nsat, o);
+    if ((threadIdx.x & 31) == 0 && nsat) atomicAdd(A.sat, nsat);
+  }
+}
+
+// ---------------------------------------------------------- compensate
+
+template <typename T, bool HIST>
+__global__ void __launch_bounds__(kThreads)
+    compensate_kernel(const T* __restrict__ g, T* __restrict__ r, T* __restrict__ zero,
+                      uint32_t* __restrict__ ghist, const Chunk* __restrict__ chunks,
+                      uint32_t nchunks, int ef, T coeff) {
+  __shared__ uint32_t hist[HIST ? kBins : 1];
+  uint32_t cur = kNone;
+  if (HIST) {
+    for (int b = threadIdx.x; b < kBins; b += kThreads) hist[b] = 0;
+    __syncthreads();
+  }
+  auto flush = [&]() {
+    __syncthreads();
+    uint32_t* dst = ghist + static_cast<uint64_t>(cur) * kBins;
+    for (int b = threadIdx.x; b < kBins; b += kThreads) {
+      const uint32_t v = hist[b];
+      if (v) {
+        atomicAdd(dst + b, v);
+        hist[b] = 0;
+      }
+    }
+    __syncthreads();
+  };
+  for (uint32_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    const Chunk ch = chunks[ci];
+    if (HIST && ch.tensor != cur) {
+      if (cur != kNone) flush();
+      cur = ch.tensor;
+    }
+    for (uint64_t base = ch.begin; base < ch.end; base += kThreads * kUnroll) {
+      T gv[kUnroll], rv[kUnroll];
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const uint64_t i = base + q * kThreads + threadIdx.x;
+        if (i < ch.end) {
+          gv[q] = g[i];
+          rv[q] = ef ? r[i] : T(0);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const uint64_t i = base + q * kThreads + threadIdx.x;
+        if (i >= ch.end) continue;
+        const T c = compensate(gv[q], rv[q], coeff, ef);
+        r[i] = c;
+        if (zero) zero[i] = T(0);
+        if (HIST) atomicAdd(&hist[bin_of(c)], 1u);
+      }
+    }
+  }
+  if (HIST && cur != kNone) flush();
+}
+
+// --------------------------------------------------------------- top-k
+
+// One CTA per tensor: the bin holding the k-th largest |c|.
+__global__ void __launch_bounds__(kThreads)
+    topk_threshold_kernel(uint32_t* hist, const uint32_t* k, uint32_t* thr, uint32_t* need,
+                          uint32_t* sel_cnt, uint32_t* cand_cnt) {
+  using Scan = cub::BlockScan<uint32_t, kThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  constexpr int kPer = kBins / kThreads;
+  const uint32_t t = blockIdx.x;
+  uint32_t* h = hist + static_cast<uint64_t>(t) * kBins;
+  // thread j owns bins [kBins - kPer*(j+1), kBins - kPer*j): highest first
+  const int hi = kBins - kPer * threadIdx.x;
+  uint32_t mine = 0;
+  for (int b = hi - 1; b >= hi - kPer; --b) mine += h[b];
+  uint32_t above = 0;
+  Scan(tmp).ExclusiveSum(mine, above);
+  const uint32_t kt = k[t];
+  if (above < kt && kt <= above + mine) {
+    uint32_t acc = above;
+    for (int b = hi - 1; b >= hi - kPer; --b) {
+      if (acc + h[b] >= kt) {
+        thr[t] = static_cast<uint32_t>(b);
+        need[t] = kt - acc;
+        break;
+      }
+      acc += h[b];
+    }
+  }
+  __syncthreads();
+  for (int b = hi - 1; b >= hi - kPer; --b) h[b] = 0;
+  if (threadIdx.x == 0) {
+    sel_cnt[t] = 0;
+    cand_cnt[t] = 0;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    topk_collect_kernel(T* __restrict__ r, T* __restrict__ kept, const Chunk* __restrict__ chunks,
+                        uint32_t nchunks, const uint32_t* __restrict__ thr,
+                        const uint64_t* __restrict__ t_begin, const uint64_t* __restrict__ list_off,
+                        uint32_t* sel_cnt, uint32_t* __restrict__ list_idx,
+                        T* __restrict__ list_val, uint32_t* cand_cnt,
+                        typename KeyOf<T>::K* __restrict__ cand_key,
+                        uint32_t* __restrict__ cand_idx) {
+  for (uint32_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    const Chunk ch = chunks[ci];
+    const uint32_t t = ch.tensor;
+    const uint32_t tb = thr[t];
+    const uint64_t lo = list_off[t], cb = t_begin[t];
+    for (uint64_t base = ch.begin; base < ch.end; base += kThreads * kUnroll) {
+      T cv[kUnroll];
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const uint64_t i = base + q * kThreads + threadIdx.x;
+        cv[q] = i < ch.end ? r[i] : T(0);
+      }
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const uint64_t i = base + q * kThreads + threadIdx.x;
+        const bool valid = i < ch.end;
+        const uint32_t b = bin_of(cv[q]);
+        const bool take = valid && b > tb;
+        const bool cand = valid && b == tb;
+        const uint32_t ps = append_slot(take, sel_cnt + t);
+        if (take) {
+          list_idx[lo + ps] = static_cast<uint32_t>(i);
+          list_val[lo + ps] = cv[q];
+          if (kept) kept[i] = cv[q];
+          r[i] = sub_rn(cv[q], cv[q]);
+        }
+        const uint32_t pc = append_slot(cand, cand_cnt + t);
+        if (cand) {
+          cand_key[cb + pc] = KeyOf<T>::key(cv[q]);
+          cand_idx[cb + pc] = static_cast<uint32_t>(i);
+        }
+      }
+    }
+  }
+}
+
+// Finds the digit d of the current pass where the count of candidates with a
+// digit >= d first reaches need; need -= count above d.  Returns d.
+__device__ uint32_t pick_digit(uint32_t* hist, uint32_t& need, uint32_t* s_digit,
+                               uint32_t* s_need) {
+  using Scan = cub::BlockScan<uint32_t, kThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  constexpr int kPer = kDigits / kThreads;
+  const int hi = kDigits - kPer * threadIdx.x;
+  uint32_t mine = 0;
+  for (int b = hi - 1; b >= hi - kPer; --b) mine += hist[b];
+  uint32_t above = 0;
+  Scan(tmp).ExclusiveSum(mine, above);
+  if (above < need && need <= above + mine) {
+    uint32_t acc = above;
+    for (int b = hi - 1; b >= hi - kPer; --b) {
+      if (acc + hist[b] >= need) {
+        *s_digit = static_cast<uint32_t>(b);
+        *s_need = need - acc;
+        break;
+      }
+      acc += hist[b];
+    }
+  }
+  __syncthreads();
+  need = *s_need;
+  return *s_digit;
+}
+
+// One CTA per tensor: the `need` best candidates by composite (low key bits
+// desc, index asc) — an exact radix select over (key low bits, ~index).
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    topk_resolve_kernel(T* __restrict__ r, T* __restrict__ kept,
+                        const uint64_t* __restrict__ t_begin, const uint64_t* __restrict__ list_off,
+                        const uint32_t* __restrict__ sel_cnt, const uint32_t* __restrict__ need_in,
+                        const uint32_t* __restrict__ cand_cnt,
+                        const typename KeyOf<T>::K* __restrict__ cand_key,
+                        const uint32_t* __restrict__ cand_idx, uint32_t* __restrict__ list_idx,
+                        T* __restrict__ list_val) {
+  using K = typename KeyOf<T>::K;
+  constexpr int kLow = KeyOf<T>::kBits - kBinBits;  // key bits below the bin
+  __shared__ uint32_t hist[kDigits];
+  __shared__ uint32_t s_digit, s_need, s_count;
+  const uint32_t t = blockIdx.x;
+  uint32_t need = need_in[t];
+  const uint32_t m = cand_cnt[t];
+  if (need == 0) return;
+  const uint64_t cb = t_begin[t];
+  const K* ck = cand_key + cb;
+  const uint32_t* cx = cand_idx + cb;
+  const K lowmask = (K(1) << kLow) - 1;
+  uint64_t pa = 0;  // fixed prefix of the low key bits
+  uint32_t pb = 0;  // fixed prefix of ~index
+  if (need < m) {
+    // field 0: the low key bits, field 1: ~index (32 bits)
+    for (int field = 0; field < 2; ++field) {
+      int left = field == 0 ? kLow : 32;
+      while (left > 0) {
+        const int nb = left < kDigitBits ? left : kDigitBits;
+        const int shift = left - nb;
+        for (int b = threadIdx.x; b < kDigits; b += kThreads) hist[b] = 0;
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < m; e += kThreads) {
+          const uint64_t a = static_cast<uint64_t>(ck[e] & lowmask);
+          const uint32_t b = ~cx[e];
+          uint32_t digit;
+          bool match;
+          if (field == 0) {
+            match = (a >> left) == pa;
+            digit = static_cast<uint32_t>(a >> shift) & ((1u << nb) - 1u);
+          } else {
+            match = a == pa && (left == 32 ? true : (b >> left) == pb);
+            digit = (b >> shift) & ((1u << nb) - 1u);
+          }
+          if (match) atomicAdd(&hist[digit], 1u);
+        }
+        __syncthreads();
+        const uint32_t d = pick_digit(hist, need, &s_digit, &s_need);
+        if (field == 0)
+          pa = (pa << nb) | d;
+        else
+          pb = (nb == 32 ? 0u : (pb << nb)) | d;
+        left = shift;
+        __syncthreads();
+      }
+    }
+  }
+  if (threadIdx.x == 0) s_count = 0;
+  __syncthreads();
+  const uint64_t base = list_off[t] + sel_cnt[t];
+  const bool all = need_in[t] >= m;
+  // warp-uniform trip count so append_slot's ballot sees every lane
+  for (uint32_t e0 = 0; e0 < m; e0 += kThreads) {
+    const uint32_t e = e0 + threadIdx.x;
+    bool take = false;
+    if (e < m) {
+      const uint64_t a = static_cast<uint64_t>(ck[e] & lowmask);
+      const uint32_t b = ~cx[e];
+      take = all || a > pa || (a == pa && b >= pb);
+    }
+    const uint32_t slot = append_slot(take, &s_count);
+    if (take) {
+      const uint32_t i = cx[e];
+      const T c = r[i];
+      list_idx[base + slot] = i;
+      list_val[base + slot] = c;
+      if (kept) kept[i] = c;
+      r[i] = sub_rn(c, c);
+    }
+  }
+}
+
+// ------------------------------------------------------------- random-k
+
+// RandomkFilter's per-tensor stream (compress.cpp:288) or, for the standalone
+// randomk_compress, the caller's seed.
+__device__ __forceinline__ uint64_t seed_of(const RandomkArgs& A, uint32_t t) {
+  return A.raw_seed ? A.seed : mix_seed(A.seed, A.step * 0x10001ULL + t);
+}
+
+__device__ __forceinline__ uint32_t tensor_of_entry(const RandomkArgs& A, uint64_t e) {
+  return A.tensor_of[e];
+}
+
+// Draw i of tensor t: j_i = i + next_below(d - i) assuming no rejection; a
+// rejection (probability < n / 2^64 per draw) flags the tensor for the exact
+// sequential replay below.
+__global__ void randomk_draw_kernel(RandomkArgs A) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t t = tensor_of_entry(A, e);
+    const uint64_t i = e - A.list_off[t];
+    const uint64_t n = A.t_numel[t] - i;
+    const uint64_t seed = seed_of(A, t);
+    const uint64_t x = splitmix_out(seed + (i + 1) * 0x9e3779b97f4a7c15ULL);
+    const uint64_t threshold = (0ULL - n) % n;  // rng.hpp:29
+    if (x < threshold) A.reject[t] = 1;
+    A.j[e] = static_cast<uint32_t>(i + x % n);
+  }
+}
+
+// Exact replay of next_below's rejection loop for flagged tensors (one thread
+// per tensor; practically never taken).
+__global__ void randomk_replay_kernel(RandomkArgs A) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.ntensors || !A.reject[t]) return;
+  A.reject[t] = 0;
+  const uint64_t d = A.t_numel[t], lo = A.list_off[t];
+  const uint64_t k = A.list_off[t + 1] - lo;
+  uint64_t state = seed_of(A, t);
+  for (uint64_t i = 0; i < k; ++i) {
+    const uint64_t n = d - i, threshold = (0ULL - n) % n;
+    uint64_t x;
+    do {
+      state += 0x9e3779b97f4a7c15ULL;
+      x = splitmix_out(state);
+    } while (x < threshold);
+    A.j[lo + i] = static_cast<uint32_t>(i + x % n);
+  }
+}
+
+// Per-position lists of the draws that target each position.
+__global__ void randomk_link_kernel(RandomkArgs A) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t t = tensor_of_entry(A, e);
+    const uint32_t i = static_cast<uint32_t>(e - A.list_off[t]);
+    A.nxt[e] = atomicExch(&A.head[A.t_begin[t] + A.j[e]], i);
+  }
+}
+
+// last draw m < before whose target is position p (local), or kNone
+__device__ __forceinline__ uint32_t last_before(const RandomkArgs& A, uint32_t t, uint32_t p,
+                                                uint32_t before) {
+  const uint64_t lo = A.list_off[t];
+  uint32_t best = kNone;
+  for (uint32_t m = A.head[A.t_begin[t] + p]; m != kNone; m = A.nxt[lo + m])
+    if (m < before && (best == kNone || m > best)) best = m;
+  return best;
+}
+
+// prv[i] = last earlier draw with the same target; src[i] = last earlier
+// draw targeting position i itself.
+__global__ void randomk_chain_kernel(RandomkArgs A) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t t = tensor_of_entry(A, e);
+    const uint32_t i = static_cast<uint32_t>(e - A.list_off[t]);
+    A.prv[e] = last_before(A, t, A.j[e], i);
+    A.src[e] = last_before(A, t, i, i);
+  }
+}
+
+// Position i of the pool after the k swaps holds S_i = V(j_i, i), where
+// V(p, i) is p unless an earlier draw m targeted p (then W(m)), and W(m), the
+// content of position m when draw m starts, is m unless an earlier draw
+// targeted position m (then W of that draw).  kept[S] = c, r[S] = c - c.
+template <typename T>
+__global__ void randomk_gather_kernel(RandomkArgs A, T* __restrict__ r, T* __restrict__ kept,
+                                      uint32_t* __restrict__ list_idx, T* __restrict__ list_val) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t t = tensor_of_entry(A, e);
+    const uint64_t lo = A.list_off[t];
+    const uint32_t i = static_cast<uint32_t>(e - lo);
+    const uint32_t j = A.j[e];
+    uint32_t s;
+    if (j == i || A.prv[e] != kNone) {
+      uint32_t w = j == i ? i : A.prv[e];
+      while (A.src[lo + w] != kNone) w = A.src[lo + w];
+      s = w;
+    } else {
+      s = j;
+    }
+    const uint64_t flat = A.t_begin[t] + s;
+    const T c = r[flat];
+    list_idx[e] = static_cast<uint32_t>(flat);
+    list_val[e] = c;
+    if (kept) kept[flat] = c;
+    r[flat] = sub_rn(c, c);
+  }
+}
+
+__global__ void randomk_clear_kernel(RandomkArgs A) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t t = tensor_of_entry(A, e);
+    A.head[A.t_begin[t] + A.j[e]] = kNone;
+  }
+}
+
+// ------------------------------------------------------------ exchange
+
+template <typename T>
+__global__ void fp16_mean_kernel(const uint16_t* __restrict__ recv, int P, uint64_t n, T inv,
+                                 T* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    T acc = T(0);
+    for (int p = 0; p < P; ++p)
+      acc = add_rn(acc, static_cast<T>(half_to_float(recv[static_cast<uint64_t>(p) * n + i])));
+    out[i] = mul_rn(acc, inv);
+  }
+}
+
+template <typename T>
+__global__ void list_mean_aligned_kernel(const uint32_t* __restrict__ idx,
+                                         const T* __restrict__ vals, int P, uint64_t cnt, T inv,
+                                         T* __restrict__ out) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < cnt;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    T acc = T(0);
+    for (int p = 0; p < P; ++p) acc = add_rn(acc, vals[static_cast<uint64_t>(p) * cnt + e]);
+    out[idx[e]] = mul_rn(acc, inv);
+  }
+}
+
+template <typename T>
+__global__ void list_accumulate_kernel(const uint32_t* __restrict__ idx, const T* __restrict__ val,
+                                       uint64_t cnt, T* __restrict__ acc) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < cnt;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    acc[idx[e]] = add_rn(acc[idx[e]], val[e]);
+}
+
+template <typename T>
+__global__ void list_finish_kernel(const uint32_t* __restrict__ idx, uint64_t cnt, T* acc, T inv,
+                                   T* __restrict__ out, int clear) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < cnt;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (clear)
+      acc[idx[e]] = T(0);
+    else
+      out[idx[e]] = mul_rn(acc[idx[e]], inv);
+  }
+}
+
+// ------------------------------------------------------------- ordering
+
+template <typename T>
+__global__ void order_keys_kernel(const T* __restrict__ val, const uint64_t* __restrict__ p,
+                                  uint64_t cnt, typename KeyOf<T>::K* __restrict__ key) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < cnt;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    key[e] = KeyOf<T>::key(val[p[e]]);
+}
+
+// out[e] = (idx_sorted[q[e]], val[p[q[e]]]), q = identity when NULL
+template <typename T>
+__global__ void order_emit_kernel(const uint32_t* __restrict__ idx_sorted,
+                                  const uint64_t* __restrict__ p, const uint64_t* __restrict__ q,
+                                  const T* __restrict__ val, uint64_t cnt,
+                                  uint64_t* __restrict__ out_idx, T* __restrict__ out_val) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < cnt;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t f = q ? q[e] : e;
+    out_idx[e] = idx_sorted[f];
+    out_val[e] = val[p[f]];
+  }
+}
+
+__global__ void iota_kernel(uint64_t* p, uint64_t n) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    p[e] = e;
+}
+
+// Reference output order (not on the sync path; the standalone compressors
+// only): sort by index ascending, then for top-k stable-sort by |value|
+// descending, which keeps equal magnitudes in index order (the tie rule of
+// std::stable_sort in compress.cpp:123-126).  CUB radix sorts are stable.
+template <typename T>
+cudaError_t order_list_t(int kind, const uint32_t* idx, const T* val, uint64_t cnt,
+                         uint64_t* out_idx, T* out_val, cudaStream_t s) {
+  using K = typename KeyOf<T>::K;
+  if (cnt == 0) return cudaSuccess;
+  const uint64_t blocks = (cnt + kThreads - 1) / kThreads;
+  const int grid = static_cast<int>(blocks < 1024 ? blocks : 1024);
+  const int n = static_cast<int>(cnt);
+  constexpr int kKeyBits = 8 * static_cast<int>(sizeof(K));
+  uint32_t* i1 = nullptr;
+  uint64_t *p0 = nullptr, *p1 = nullptr, *q0 = nullptr, *q1 = nullptr;
+  K *k0 = nullptr, *k1 = nullptr;
+  void* tmp = nullptr;
+  size_t b1 = 0, b2 = 0;
+  cudaError_t e = cudaSuccess;
+  auto al = [&](void** ptr, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMallocAsync(ptr, bytes, s);
+  };
+  al(reinterpret_cast<void**>(&i1), cnt * 4);
+  al(reinterpret_cast<void**>(&p0), cnt * 8);
+  al(reinterpret_cast<void**>(&p1), cnt * 8);
+  al(reinterpret_cast<void**>(&q0), cnt * 8);
+  al(reinterpret_cast<void**>(&q1), cnt * 8);
+  al(reinterpret_cast<void**>(&k0), cnt * sizeof(K));
+  al(reinterpret_cast<void**>(&k1), cnt * sizeof(K));
+  if (e == cudaSuccess)
+    e = cub::DeviceRadixSort::SortPairs(nullptr, b1, idx, i1, p0, p1, n, 0, 32, s);
+  if (e == cudaSuccess)
+    e = cub::DeviceRadixSort::SortPairsDescending(nullptr, b2, k0, k1, q0, q1, n, 0, kKeyBits, s);
+  al(&tmp, b1 > b2 ? b1 : b2);
+  if (e == cudaSuccess) {
+    iota_kernel<<<grid, kThreads, 0, s>>>(p0, cnt);
+    e = cub::DeviceRadixSort::SortPairs(tmp, b1, idx, i1, p0, p1, n, 0, 32, s);
+  }
+  if (e == cudaSuccess && kind == kTopk) {
+    order_keys_kernel<T><<<grid, kThreads, 0, s>>>(val, p1, cnt, k0);
+    iota_kernel<<<grid, kThreads, 0, s>>>(q0, cnt);
+    e = cub::DeviceRadixSort::SortPairsDescending(tmp, b2, k0, k1, q0, q1, n, 0, kKeyBits, s);
+  }
+  if (e == cudaSuccess)
+    order_emit_kernel<T><<<grid, kThreads, 0, s>>>(i1, p1, kind == kTopk ? q1 : nullptr, val, cnt,
+                                                   out_idx, out_val);
+  for (void* ptr : {static_cast<void*>(i1), static_cast<void*>(p0), static_cast<void*>(p1),
+                    static_cast<void*>(q0), static_cast<void*>(q1), static_cast<void*>(k0),
+                    static_cast<void*>(k1), tmp})
+    if (ptr) cudaFreeAsync(ptr, s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
+int grid_for(uint64_t work, int sms, int per_sm) {
+  const uint64_t g = (work + kThreads - 1) / kThreads;
+  const uint64_t cap = static_cast<uint64_t>(sms) * per_sm;
+  return static_cast<int>(g < 1 ? 1 : (g < cap ? g : cap));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ launchers
+
+cudaError_t launch_dense(int dtype, int kind, const DenseArgs& a, int sms, cudaStream_t s) {
+  const int grid = static_cast<int>(a.nchunks < static_cast<uint32_t>(sms * 4) ? a.nchunks : sms * 4);
+  if (grid == 0) return cudaSuccess;
+  if (dtype == 1) {
+    switch (kind) {
+      case kIdentity: dense_kernel<double, kIdentity><<<grid, kThreads, 0, s>>>(a); break;
+      case kCovap: dense_kernel<double, kCovap><<<grid, kThreads, 0, s>>>(a); break;
+      default: dense_kernel<double, kFp16><<<grid, kThreads, 0, s>>>(a); break;
+    }
+  } else {
+    switch (kind) {
+      case kIdentity: dense_kernel<float, kIdentity><<<grid, kThreads, 0, s>>>(a); break;
+      case kCovap: dense_kernel<float, kCovap><<<grid, kThreads, 0, s>>>(a); break;
+      default: dense_kernel<float, kFp16><<<grid, kThreads, 0, s>>>(a); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uint32_t* hist,
+                              const Chunk* chunks, uint32_t nchunks, int ef, double coeff,
+                              int sms, cudaStream_t s) {
+  const int grid = static_cast<int>(nchunks < static_cast<uint32_t>(sms * 4) ? nchunks : sms * 4);
+  if (grid == 0) return cudaSuccess;
+  if (dtype == 1) {
+    if (hist)
+      compensate_kernel<double, true><<<grid, kThreads, 0, s>>>(
+          static_cast<const double*>(g), static_cast<double*>(r), static_cast<double*>(zero),
+          hist, chunks, nchunks, ef, coeff);
+    else
+      compensate_kernel<double, false><<<grid, kThreads, 0, s>>>(
+          static_cast<const double*>(g), static_cast<double*>(r), static_cast<double*>(zero),
+          hist, chunks, nchunks, ef, coeff);
+  } else {
+    const float c = static_cast<float>(coeff);
+    if (hist)
+      compensate_kernel<float, true><<<grid, kThreads, 0, s>>>(
+          static_cast<const float*>(g), static_cast<float*>(r), static_cast<float*>(zero), hist,
+          chunks, nchunks, ef, c);
+    else
+      compensate_kernel<float, false><<<grid, kThreads, 0, s>>>(
+          static_cast<const float*>(g), static_cast<float*>(r), static_cast<float*>(zero), hist,
+          chunks, nchunks, ef, c);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_threshold(uint32_t* hist, const uint32_t* k, uint32_t* thr,
+                                  uint32_t* need, uint32_t* sel_cnt, uint32_t* cand_cnt,
+                                  uint32_t ntensors, cudaStream_t s) {
+  if (ntensors == 0) return cudaSuccess;
+  topk_threshold_kernel<<<ntensors, kThreads, 0, s>>>(hist, k, thr, need, sel_cnt, cand_cnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_collect(int dtype, void* r, void* kept, const Chunk* chunks,
+                                uint32_t nchunks, const uint32_t* thr, const uint64_t* t_begin,
+                                const uint64_t* list_off, uint32_t* sel_cnt, uint32_t* list_idx,
+                                void* list_val, uint32_t* cand_cnt, void* cand_key,
+                                uint32_t* cand_idx, int sms, cudaStream_t s) {
+  const int grid = static_cast<int>(nchunks < static_cast<uint32_t>(sms * 4) ? nchunks : sms * 4);
+  if (grid == 0) return cudaSuccess;
+  if (dtype == 1)
+    topk_collect_kernel<double><<<grid, kThreads, 0, s>>>(
+        static_cast<double*>(r), static_cast<double*>(kept), chunks, nchunks, thr, t_begin,
+        list_off, sel_cnt, list_idx, static_cast<double*>(list_val), cand_cnt,
+        static_cast<uint64_t*>(cand_key), cand_idx);
+  else
+    topk_collect_kernel<float><<<grid, kThreads, 0, s>>>(
+        static_cast<float*>(r), static_cast<float*>(kept), chunks, nchunks, thr, t_begin,
+        list_off, sel_cnt, list_idx, static_cast<float*>(list_val), cand_cnt,
+        static_cast<uint32_t*>(cand_key), cand_idx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_resolve(int dtype, void* r, void* kept, const uint64_t* t_begin,
+                                const uint64_t* list_off, const uint32_t* sel_cnt,
+                                const uint32_t* need, const uint32_t* cand_cnt,
+                                const void* cand_key, const uint32_t* cand_idx,
+                                uint32_t* list_idx, void* list_val, uint32_t ntensors,
+                                cudaStream_t s) {
+  if (ntensors == 0) return cudaSuccess;
+  if (dtype == 1)
+    topk_resolve_kernel<double><<<ntensors, kThreads, 0, s>>>(
+        static_cast<double*>(r), static_cast<double*>(kept), t_begin, list_off, sel_cnt, need,
+        cand_cnt, static_cast<const uint64_t*>(cand_key), cand_idx, list_idx,
+        static_cast<double*>(list_val));
+  else
+    topk_resolve_kernel<float><<<ntensors, kThreads, 0, s>>>(
+        static_cast<float*>(r), static_cast<float*>(kept), t_begin, list_off, sel_cnt, need,
+        cand_cnt, static_cast<const uint32_t*>(cand_key), cand_idx, list_idx,
+        static_cast<float*>(list_val));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_randomk_select(const RandomkArgs& a, int sms, cudaStream_t s) {
+  if (a.total == 0) return cudaSuccess;
+  const int grid = grid_for(a.total, sms, 8);
+  randomk_draw_kernel<<<grid, kThreads, 0, s>>>(a);
+  randomk_replay_kernel<<<(a.ntensors + 63) / 64, 64, 0, s>>>(a);
+  randomk_link_kernel<<<grid, kThreads, 0, s>>>(a);
+  randomk_chain_kernel<<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_randomk_gather(int dtype, const RandomkArgs& a, void* r, void* kept,
+                                  uint32_t* list_idx, void* list_val, int sms, cudaStream_t s) {
+  if (a.total == 0) return cudaSuccess;
+  const int grid = grid_for(a.total, sms, 8);
+  if (dtype == 1)
+    randomk_gather_kernel<double><<<grid, kThreads, 0, s>>>(
+        a, static_cast<double*>(r), static_cast<double*>(kept), list_idx,
+        static_cast<double*>(list_val));
+  else
+    randomk_gather_kernel<float><<<grid, kThreads, 0, s>>>(
+        a, static_cast<float*>(r), static_cast<float*>(kept), list_idx,
+        static_cast<float*>(list_val));
+  randomk_clear_kernel<<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fp16_mean(int dtype, const uint16_t* recv, int P, uint64_t n, double inv,
+                             void* out, int sms, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int grid = grid_for(n, sms, 8);
+  if (dtype == 1)
+    fp16_mean_kernel<double><<<grid, kThreads, 0, s>>>(recv, P, n, inv, static_cast<double*>(out));
+  else
+    fp16_mean_kernel<float><<<grid, kThreads, 0, s>>>(recv, P, n, static_cast<float>(inv),
+                                                       static_cast<float*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_list_mean_aligned(int dtype, const uint32_t* idx, const void* vals, int P,
+                                     uint64_t cnt, double inv, void* out, int sms,
+                                     cudaStream_t s) {
+  if (cnt == 0) return cudaSuccess;
+  const int grid = grid_for(cnt, sms, 8);
+  if (dtype == 1)
+    list_mean_aligned_kernel<double><<<grid, kThreads, 0, s>>>(
+        idx, static_cast<const double*>(vals), P, cnt, inv, static_cast<double*>(out));
+  else
+    list_mean_aligned_kernel<float><<<grid, kThreads, 0, s>>>(
+        idx, static_cast<const float*>(vals), P, cnt, static_cast<float>(inv),
+        static_cast<float*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_list_accumulate(int dtype, const uint32_t* idx, const void* val, uint64_t cnt,
+                                   void* acc, int sms, cudaStream_t s) {
+  if (cnt == 0) return cudaSuccess;
+  const int grid = grid_for(cnt, sms, 8);
+  if (dtype == 1)
+    list_accumulate_kernel<double><<<grid, kThreads, 0, s>>>(
+        idx, static_cast<const double*>(val), cnt, static_cast<double*>(acc));
+  else
+    list_accumulate_kernel<float><<<grid, kThreads, 0, s>>>(
+        idx, static_cast<const float*>(val), cnt, static_cast<float*>(acc));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_list_finish(int dtype, const uint32_t* idx, uint64_t cnt, void* acc,
+                               double inv, void* out, int clear, int sms, cudaStream_t s) {
+  if (cnt == 0) return cudaSuccess;
+  const int grid = grid_for(cnt, sms, 8);
+  if (dtype == 1)
+    list_finish_kernel<double><<<grid, kThreads, 0, s>>>(idx, cnt, static_cast<double*>(acc), inv,
+                                                         static_cast<double*>(out), clear);
+  else
+    list_finish_kernel<float><<<grid, kThreads, 0, s>>>(idx, cnt, static_cast<float*>(acc),
+                                                        static_cast<float>(inv),
+                                                        static_cast<float*>(out), clear);
+  return cudaGetLastError();
+}
+
+cudaError_t order_list(int dtype, int kind, const uint32_t* idx, const void* val, uint64_t cnt,
+                       uint64_t* out_idx, void* out_val, cudaStream_t s) {
+  if (dtype == 1)
+    return order_list_t<double>(kind, idx, static_cast<const double*>(val), cnt, out_idx,
+                                static_cast<double*>(out_val), s);
+  return order_list_t<float>(kind, idx, static_cast<const float*>(val), cnt, out_idx,
+                             static_cast<float*>(out_val), s);
+}
+
+}  // namespace fb
+}  // namespace covapb

@@ -1,0 +1,128 @@
+// covap_feedback.h — launchers for the baseline compressors under the generic
+// error-feedback wrapper.  Internal; the boundary is
+// include/covap_c.h (covap_feedback_*, covap_topk_compress, ...).
+//
+// Reference (paths under /root/reference/proj):
+//   ErrorFeedback::step          compress.cpp:323-344
+//   IdentityFilter / CovapFilter compress.cpp:241-264
+//   TopkFilter / topk_compress   compress.cpp:119-133, 266-281
+//   RandomkFilter / randomk      compress.cpp:135-155, 283-298
+//   Fp16Filter / half bits       compress.cpp:157-236, 300-309
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace covapb {
+namespace fb {
+
+enum Kind { kIdentity = 0, kCovap = 1, kTopk = 2, kRandomk = 3, kFp16 = 4 };
+
+constexpr int kBinBits = 12;  // top-k first-level histogram: top 12 bits of |x|
+constexpr int kBins = 1 << kBinBits;
+constexpr uint32_t kNone = 0xffffffffu;
+
+// A slice of one tensor, at most kChunk elements; tensors are cut into
+// chunks so a CTA's work never straddles two tensors.
+struct Chunk {
+  uint64_t begin;
+  uint64_t end;
+  uint32_t tensor;
+  uint32_t pad;
+};
+constexpr uint64_t kChunk = 16384;
+
+// Dense filters (identity, covap, fp16): c = g (+ coeff*r); kept = f(c);
+// r = c - kept.  kept may be NULL; wire (fp16 only) receives the half bits;
+// sat counts clamped values.
+struct DenseArgs {
+  const void* g;
+  void* r;
+  void* kept;
+  uint16_t* wire;
+  unsigned long long* sat;
+  const Chunk* chunks;
+  uint32_t nchunks;
+  int ef;
+  double coeff;
+  uint64_t step;      // covap selection (compress.cpp:13-28)
+  uint32_t interval;
+  int rule;
+};
+cudaError_t launch_dense(int dtype, int kind, const DenseArgs& a, int sms, cudaStream_t s);
+
+// Compensation pass of the sparsifiers: r = c; zero[i] = 0 when zero is not
+// NULL; with hist, the per-tensor histogram of the top kBinBits of |c|.
+cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uint32_t* hist,
+                              const Chunk* chunks, uint32_t nchunks, int ef, double coeff,
+                              int sms, cudaStream_t s);
+
+// Top-k.  thr[t] = threshold bin, need[t] = elements still to take from it;
+// clears hist and the counters.
+cudaError_t launch_topk_threshold(uint32_t* hist, const uint32_t* k, uint32_t* thr,
+                                  uint32_t* need, uint32_t* sel_cnt, uint32_t* cand_cnt,
+                                  uint32_t ntensors, cudaStream_t s);
+// Elements above the threshold bin go to the list (and kept, r = c - c);
+// elements in it become candidates (cand_* at the tensor's own offset).
+cudaError_t launch_topk_collect(int dtype, void* r, void* kept, const Chunk* chunks,
+                                uint32_t nchunks, const uint32_t* thr, const uint64_t* t_begin,
+                                const uint64_t* list_off, uint32_t* sel_cnt, uint32_t* list_idx,
+                                void* list_val, uint32_t* cand_cnt, void* cand_key,
+                                uint32_t* cand_idx, int sms, cudaStream_t s);
+// Exact selection among the candidates by (|c| desc, index asc).
+cudaError_t launch_topk_resolve(int dtype, void* r, void* kept, const uint64_t* t_begin,
+                                const uint64_t* list_off, const uint32_t* sel_cnt,
+                                const uint32_t* need, const uint32_t* cand_cnt,
+                                const void* cand_key, const uint32_t* cand_idx,
+                                uint32_t* list_idx, void* list_val, uint32_t ntensors,
+                                cudaStream_t s);
+
+// Random-k: sample_without_replacement reproduced in parallel.  Entry e of
+// the list belongs to tensor tensor_of[e], draw i = e - list_off[t].
+struct RandomkArgs {
+  const uint64_t* t_begin;
+  const uint64_t* t_numel;
+  const uint64_t* list_off;
+  const uint32_t* tensor_of;  // per list entry
+  uint32_t ntensors;
+  uint64_t total;             // list entries
+  uint64_t seed;
+  uint64_t step;
+  int raw_seed;               // 1: draw from SplitMix64(seed) itself (randomk_compress)
+  uint32_t* j;                // draw targets (local)
+  uint32_t* nxt;
+  uint32_t* prv;
+  uint32_t* src;
+  uint32_t* head;             // per flat position, kNone when idle
+  int* reject;                // per tensor
+};
+cudaError_t launch_randomk_select(const RandomkArgs& a, int sms, cudaStream_t s);
+// list[e] = (flat index S_e, c); kept[S] = c; r[S] = c - c; head cleared.
+cudaError_t launch_randomk_gather(int dtype, const RandomkArgs& a, void* r, void* kept,
+                                  uint32_t* list_idx, void* list_val, int sms, cudaStream_t s);
+
+// Exchange side (the mean of the kept gradients over P ranks, trainer.cpp:402
+// and 35-47): out was zero-filled by the compensation pass.
+// fp16: out[i] = (0 + sum_p widen(recv[p*n + i])) * inv.
+cudaError_t launch_fp16_mean(int dtype, const uint16_t* recv, int P, uint64_t n, double inv,
+                             void* out, int sms, cudaStream_t s);
+// Rank-aligned lists (random-k: same indices on every rank, same order):
+// out[idx[e]] = (0 + sum_p vals[p*cnt + e]) * inv.
+cudaError_t launch_list_mean_aligned(int dtype, const uint32_t* idx, const void* vals, int P,
+                                     uint64_t cnt, double inv, void* out, int sms,
+                                     cudaStream_t s);
+// General lists (top-k): acc[idx] += val for rank p's list (call in rank order),
+// then out[idx] = acc[idx] * inv over every rank's list, then acc[idx] = 0.
+cudaError_t launch_list_accumulate(int dtype, const uint32_t* idx, const void* val, uint64_t cnt,
+                                   void* acc, int sms, cudaStream_t s);
+cudaError_t launch_list_finish(int dtype, const uint32_t* idx, uint64_t cnt, void* acc,
+                               double inv, void* out, int clear, int sms, cudaStream_t s);
+
+// Reference output order for the standalone compressors: top-k by (|x| desc,
+// index asc), random-k by index asc.  idx are positions; writes 64-bit
+// positions and values.
+cudaError_t order_list(int dtype, int kind, const uint32_t* idx, const void* val, uint64_t cnt,
+                       uint64_t* out_idx, void* out_val, cudaStream_t s);
+
+}  // namespace fb
+}  // namespace covapb

@@ -1,0 +1,596 @@
+// covap_feedback_capi.cpp — C-ABI of the baseline compressors under the
+// generic error-feedback wrapper (include/covap_c.h, covap_feedback_*;
+// SURVEY.md §8(f4)).
+//
+// Reference map (paths under /root/reference/proj):
+//   covap_feedback_create      ErrorFeedback::ErrorFeedback, compress.cpp:316-321
+//   covap_feedback_step        ErrorFeedback::step, compress.cpp:323-344, with
+//                              GradientFilter::keep, compress.cpp:241-309
+//   covap_feedback_transmitted transmitted_elements, compress.cpp:246-314; bytes
+//                              as train() counts them, trainer.cpp:396-400
+//   covap_feedback_sync_step   the non-COVAP branch of train(), trainer.cpp:387-403
+//   covap_topk_compress        topk_compress, compress.cpp:119-133
+//   covap_randomk_compress     randomk_compress, compress.cpp:135-155
+//   covap_fp16_roundtrip       fp16_roundtrip, compress.cpp:226-236
+//   covap_sparsifier_k         sparsifier_k, compress.cpp:107-116
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "covap_capi_common.hpp"
+#include "covap_feedback.h"
+#include "covap_plan.hpp"
+
+namespace fb = covapb::fb;
+
+struct covap_feedback {
+  int dtype = COVAP_F32;
+  size_t esize = 4;
+  int device = 0;
+  int sms = 148;
+  covap_ef ef{1, 0.3, 100, 0.1};
+  covap_filter filter{};
+  std::vector<uint64_t> numel, begin, k, list_off;
+  uint64_t total = 0, k_total = 0;
+  uint64_t num_steps = 0;
+  void* residual = nullptr;
+  fb::Chunk* chunks = nullptr;
+  uint32_t nchunks = 0;
+  uint64_t* d_begin = nullptr;
+  uint64_t* d_numel = nullptr;
+  uint64_t* d_list_off = nullptr;
+  unsigned long long* d_sat = nullptr;
+  // top-k
+  uint32_t* hist = nullptr;
+  uint32_t* d_k = nullptr;
+  uint32_t* thr = nullptr;
+  uint32_t* need = nullptr;
+  uint32_t* sel_cnt = nullptr;
+  uint32_t* cand_cnt = nullptr;
+  void* cand_key = nullptr;
+  uint32_t* cand_idx = nullptr;
+  void* acc = nullptr;  // rank-ordered scatter accumulator, zero between steps
+  // random-k
+  uint32_t* tensor_of = nullptr;
+  uint32_t *j = nullptr, *nxt = nullptr, *prv = nullptr, *src = nullptr, *head = nullptr;
+  int* reject = nullptr;
+  // wire
+  uint32_t* list_idx = nullptr;
+  void* list_val = nullptr;
+  uint16_t* half = nullptr;
+  // exchange scratch
+  void* recv_a = nullptr;
+  void* recv_b = nullptr;
+  uint64_t cap_a = 0, cap_b = 0;
+  std::vector<void*> owned;
+};
+
+namespace {
+
+template <typename P>
+P* dalloc(covap_feedback* f, uint64_t bytes) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<uint64_t>(bytes, 16)));
+  f->owned.push_back(p);
+  return static_cast<P*>(p);
+}
+
+void release(covap_feedback* f) {
+  if (!f) return;
+  DeviceGuard dg(f->device);
+  cudaDeviceSynchronize();
+  for (void* p : f->owned) cudaFree(p);
+  if (f->recv_a) cudaFree(f->recv_a);
+  if (f->recv_b) cudaFree(f->recv_b);
+  delete f;
+}
+
+uint64_t sparsifier_k(uint64_t d, double kf) {  // compress.cpp:107-116
+  if (d == 0) throw covap::InvalidInput("cannot sparsify an empty vector");
+  if (!(kf > 0.0) || kf > 1.0) throw covap::InvalidInput("k_fraction must be in (0, 1]");
+  const auto k = static_cast<uint64_t>(std::ceil(kf * static_cast<double>(d)));
+  return std::min(std::max<uint64_t>(k, 1), d);
+}
+
+bool sparse(const covap_feedback* f) {
+  return f->filter.kind == COVAP_FILTER_TOPK || f->filter.kind == COVAP_FILTER_RANDOMK;
+}
+
+double coeff_of(const covap_feedback* f) {
+  return f->ef.enabled ? covapb::ef_coefficient(f->num_steps, 1, f->ef.init_value,
+                                                f->ef.ascend_steps, f->ef.ascend_range)
+                       : 0.0;
+}
+
+fb::RandomkArgs randomk_args(covap_feedback* f) {
+  fb::RandomkArgs a{};
+  a.t_begin = f->d_begin;
+  a.t_numel = f->d_numel;
+  a.list_off = f->d_list_off;
+  a.tensor_of = f->tensor_of;
+  a.ntensors = static_cast<uint32_t>(f->numel.size());
+  a.total = f->k_total;
+  a.seed = f->filter.seed;
+  a.step = f->num_steps;
+  a.j = f->j;
+  a.nxt = f->nxt;
+  a.prv = f->prv;
+  a.src = f->src;
+  a.head = f->head;
+  a.reject = f->reject;
+  return a;
+}
+
+// The error-feedback step.  kept: dense kept gradient (NULL = not wanted);
+// zero: buffer to zero-fill (the sparse filters' kept or the sync output);
+// the sparse filters leave (index, value) pairs in list_idx / list_val and
+// fp16 its halves in `half` when wire is set.
+void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool wire,
+             cudaStream_t st) {
+  const int dt = f->dtype == COVAP_F64 ? 1 : 0;
+  const double coeff = coeff_of(f);
+  const uint32_t nt = static_cast<uint32_t>(f->numel.size());
+  switch (f->filter.kind) {
+    case COVAP_FILTER_IDENTITY:
+    case COVAP_FILTER_COVAP:
+    case COVAP_FILTER_FP16: {
+      fb::DenseArgs a{};
+      a.g = grad;
+      a.r = f->residual;
+      a.kept = kept;
+      a.wire = wire ? f->half : nullptr;
+      a.sat = f->d_sat;
+      a.chunks = f->chunks;
+      a.nchunks = f->nchunks;
+      a.ef = f->ef.enabled;
+      a.coeff = coeff;
+      a.step = f->num_steps;
+      a.interval = f->filter.interval;
+      a.rule = f->filter.rule;
+      CK(fb::launch_dense(dt, f->filter.kind, a, f->sms, st));
+      break;
+    }
+    case COVAP_FILTER_TOPK:
+      CK(fb::launch_compensate(dt, grad, f->residual, zero, f->hist, f->chunks, f->nchunks,
+                               f->ef.enabled, coeff, f->sms, st));
+      CK(fb::launch_topk_threshold(f->hist, f->d_k, f->thr, f->need, f->sel_cnt, f->cand_cnt, nt,
+                                   st));
+      CK(fb::launch_topk_collect(dt, f->residual, kept, f->chunks, f->nchunks, f->thr, f->d_begin,
+                                 f->d_list_off, f->sel_cnt, f->list_idx, f->list_val, f->cand_cnt,
+                                 f->cand_key, f->cand_idx, f->sms, st));
+      CK(fb::launch_topk_resolve(dt, f->residual, kept, f->d_begin, f->d_list_off, f->sel_cnt,
+                                 f->need, f->cand_cnt, f->cand_key, f->cand_idx, f->list_idx,
+                                 f->list_val, nt, st));
+      break;
+    case COVAP_FILTER_RANDOMK: {
+      CK(fb::launch_compensate(dt, grad, f->residual, zero, nullptr, f->chunks, f->nchunks,
+                               f->ef.enabled, coeff, f->sms, st));
+      const fb::RandomkArgs a = randomk_args(f);
+      CK(fb::launch_randomk_select(a, f->sms, st));
+      CK(fb::launch_randomk_gather(dt, a, f->residual, kept, f->list_idx, f->list_val, f->sms,
+                                   st));
+      break;
+    }
+    default:
+      throw covap::InvalidInput("unknown filter kind");
+  }
+  ++f->num_steps;
+}
+
+// Wire payload of one rank: a = halves (fp16) or indices (top-k), b = values.
+void wire_of(covap_feedback* f, void** a, uint64_t* ba, void** b, uint64_t* bb) {
+  *a = nullptr;
+  *b = nullptr;
+  *ba = *bb = 0;
+  switch (f->filter.kind) {
+    case COVAP_FILTER_FP16:
+      *a = f->half;
+      *ba = f->total * 2;
+      break;
+    case COVAP_FILTER_TOPK:
+      *a = f->list_idx;
+      *ba = f->k_total * 4;
+      *b = f->list_val;
+      *bb = f->k_total * f->esize;
+      break;
+    case COVAP_FILTER_RANDOMK:
+      *b = f->list_val;
+      *bb = f->k_total * f->esize;
+      break;
+    default:
+      throw covap::InvalidInput("the identity / covap filters have no sync wire (use covap_sync_step)");
+  }
+}
+
+void combine(covap_feedback* f, const void* ra, const void* rb, int P, void* out,
+             cudaStream_t st) {
+  need(P >= 1, "P must be >= 1");
+  const int dt = f->dtype == COVAP_F64 ? 1 : 0;
+  const double inv = 1.0 / static_cast<double>(P);  // trainer.cpp:44
+  switch (f->filter.kind) {
+    case COVAP_FILTER_FP16:
+      CK(fb::launch_fp16_mean(dt, static_cast<const uint16_t*>(ra), P, f->total, inv, out, f->sms,
+                              st));
+      break;
+    case COVAP_FILTER_RANDOMK:
+      CK(fb::launch_list_mean_aligned(dt, f->list_idx, rb, P, f->k_total, inv, out, f->sms, st));
+      break;
+    case COVAP_FILTER_TOPK: {
+      if (P == 1) {
+        CK(fb::launch_list_mean_aligned(dt, static_cast<const uint32_t*>(ra), rb, 1, f->k_total,
+                                        inv, out, f->sms, st));
+        break;
+      }
+      const auto* idx = static_cast<const uint32_t*>(ra);
+      const auto* val = static_cast<const char*>(rb);
+      for (int p = 0; p < P; ++p)  // rank order (trainer.cpp:41-43)
+        CK(fb::launch_list_accumulate(dt, idx + static_cast<uint64_t>(p) * f->k_total,
+                                      val + static_cast<uint64_t>(p) * f->k_total * f->esize,
+                                      f->k_total, f->acc, f->sms, st));
+      const uint64_t all = static_cast<uint64_t>(P) * f->k_total;
+      CK(fb::launch_list_finish(dt, idx, all, f->acc, inv, out, 0, f->sms, st));
+      CK(fb::launch_list_finish(dt, idx, all, f->acc, inv, out, 1, f->sms, st));
+      break;
+    }
+    default:
+      throw covap::InvalidInput("the identity / covap filters have no sync wire (use covap_sync_step)");
+  }
+}
+
+void grow(void** p, uint64_t* cap, uint64_t bytes) {
+  if (bytes <= *cap) return;
+  if (*p) CK(cudaFree(*p));
+  *p = nullptr;
+  CK(cudaMalloc(p, bytes));
+  *cap = bytes;
+}
+
+}  // namespace
+
+extern "C" {
+
+covap_status covap_sparsifier_k(uint64_t d, double k_fraction, uint64_t* k) {
+  return guarded([&] {
+    need(k != nullptr, "k must not be NULL");
+    *k = sparsifier_k(d, k_fraction);
+  });
+}
+
+covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int dtype,
+                                   const covap_ef* schedule, const covap_filter* filter,
+                                   int device, covap_feedback** out) {
+  covap_feedback* f = nullptr;
+  const covap_status st = guarded([&] {
+    need(out != nullptr && filter != nullptr, "NULL argument");
+    need(n_tensors > 0 && numels != nullptr, "need at least one tensor");
+    need(dtype == COVAP_F32 || dtype == COVAP_F64, "dtype must be COVAP_F32 or COVAP_F64");
+    need(filter->kind >= COVAP_FILTER_IDENTITY && filter->kind <= COVAP_FILTER_FP16,
+         "unknown filter kind");
+    if (filter->kind == COVAP_FILTER_COVAP) need(filter->interval >= 1, "interval must be >= 1");
+    if (schedule && schedule->enabled) need(schedule->ascend_steps >= 1, "ascend_steps must be >= 1");
+    f = new covap_feedback;
+    f->dtype = dtype;
+    f->esize = dtype == COVAP_F64 ? 8 : 4;
+    f->device = device;
+    f->filter = *filter;
+    if (schedule) f->ef = *schedule;
+    f->numel.assign(numels, numels + n_tensors);
+    for (uint64_t n : f->numel) {
+      f->begin.push_back(f->total);
+      f->total += n;
+    }
+    need(f->total < 0xffffffffull, "at most 2^32 - 1 elements");
+    if (sparse(f)) {
+      f->list_off.push_back(0);
+      for (uint64_t n : f->numel) {
+        f->k.push_back(sparsifier_k(n, filter->k_fraction));
+        f->list_off.push_back(f->list_off.back() + f->k.back());
+      }
+      f->k_total = f->list_off.back();
+    }
+    DeviceGuard dg(device);
+    CK(cudaDeviceGetAttribute(&f->sms, cudaDevAttrMultiProcessorCount, device));
+    std::vector<fb::Chunk> ch;
+    for (size_t t = 0; t < n_tensors; ++t)
+      for (uint64_t b = f->begin[t]; b < f->begin[t] + f->numel[t]; b += fb::kChunk)
+        ch.push_back({b, std::min(b + fb::kChunk, f->begin[t] + f->numel[t]),
+                      static_cast<uint32_t>(t), 0});
+    f->nchunks = static_cast<uint32_t>(ch.size());
+    f->residual = dalloc<void>(f, f->total * f->esize);
+    CK(cudaMemset(f->residual, 0, std::max<uint64_t>(f->total, 1) * f->esize));
+    f->chunks = dalloc<fb::Chunk>(f, ch.size() * sizeof(fb::Chunk));
+    CK(cudaMemcpy(f->chunks, ch.data(), ch.size() * sizeof(fb::Chunk), cudaMemcpyHostToDevice));
+    f->d_begin = dalloc<uint64_t>(f, n_tensors * 8);
+    f->d_numel = dalloc<uint64_t>(f, n_tensors * 8);
+    CK(cudaMemcpy(f->d_begin, f->begin.data(), n_tensors * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(f->d_numel, f->numel.data(), n_tensors * 8, cudaMemcpyHostToDevice));
+    f->d_sat = dalloc<unsigned long long>(f, 8);
+    CK(cudaMemset(f->d_sat, 0, 8));
+    if (filter->kind == COVAP_FILTER_FP16) f->half = dalloc<uint16_t>(f, f->total * 2);
+    if (sparse(f)) {
+      f->d_list_off = dalloc<uint64_t>(f, (n_tensors + 1) * 8);
+      CK(cudaMemcpy(f->d_list_off, f->list_off.data(), (n_tensors + 1) * 8,
+                    cudaMemcpyHostToDevice));
+      f->list_idx = dalloc<uint32_t>(f, f->k_total * 4);
+      f->list_val = dalloc<void>(f, f->k_total * f->esize);
+    }
+    if (filter->kind == COVAP_FILTER_TOPK) {
+      f->hist = dalloc<uint32_t>(f, n_tensors * fb::kBins * 4);
+      CK(cudaMemset(f->hist, 0, n_tensors * fb::kBins * 4));
+      std::vector<uint32_t> k32(f->k.begin(), f->k.end());
+      f->d_k = dalloc<uint32_t>(f, n_tensors * 4);
+      CK(cudaMemcpy(f->d_k, k32.data(), n_tensors * 4, cudaMemcpyHostToDevice));
+      f->thr = dalloc<uint32_t>(f, n_tensors * 4);
+      f->need = dalloc<uint32_t>(f, n_tensors * 4);
+      f->sel_cnt = dalloc<uint32_t>(f, n_tensors * 4);
+      f->cand_cnt = dalloc<uint32_t>(f, n_tensors * 4);
+      f->cand_key = dalloc<void>(f, f->total * f->esize);
+      f->cand_idx = dalloc<uint32_t>(f, f->total * 4);
+      f->acc = dalloc<void>(f, f->total * f->esize);
+      CK(cudaMemset(f->acc, 0, std::max<uint64_t>(f->total, 1) * f->esize));
+    }
+    if (filter->kind == COVAP_FILTER_RANDOMK) {
+      std::vector<uint32_t> owner(f->k_total);
+      for (size_t t = 0; t < n_tensors; ++t)
+        std::fill(owner.begin() + f->list_off[t], owner.begin() + f->list_off[t + 1],
+                  static_cast<uint32_t>(t));
+      f->tensor_of = dalloc<uint32_t>(f, f->k_total * 4);
+      CK(cudaMemcpy(f->tensor_of, owner.data(), f->k_total * 4, cudaMemcpyHostToDevice));
+      f->j = dalloc<uint32_t>(f, f->k_total * 4);
+      f->nxt = dalloc<uint32_t>(f, f->k_total * 4);
+      f->prv = dalloc<uint32_t>(f, f->k_total * 4);
+      f->src = dalloc<uint32_t>(f, f->k_total * 4);
+      f->head = dalloc<uint32_t>(f, f->total * 4);
+      CK(cudaMemset(f->head, 0xff, std::max<uint64_t>(f->total, 4) * 4));
+      f->reject = dalloc<int>(f, n_tensors * 4);
+      CK(cudaMemset(f->reject, 0, n_tensors * 4));
+    }
+    CK(cudaDeviceSynchronize());
+    *out = f;
+  });
+  if (st != COVAP_OK && f) {
+    try {
+      release(f);
+    } catch (...) {
+    }
+  }
+  return st;
+}
+
+void covap_feedback_destroy(covap_feedback* f) {
+  try {
+    release(f);
+  } catch (...) {
+  }
+}
+
+covap_status covap_feedback_residual(covap_feedback* f, void** p, uint64_t* n) {
+  return guarded([&] {
+    need(f && p, "NULL argument");
+    *p = f->residual;
+    if (n) *n = f->total;
+  });
+}
+
+covap_status covap_feedback_get_step(const covap_feedback* f, uint64_t* s) {
+  return guarded([&] {
+    need(f && s, "NULL argument");
+    *s = f->num_steps;
+  });
+}
+
+covap_status covap_feedback_set_step(covap_feedback* f, uint64_t s) {
+  return guarded([&] {
+    need(f != nullptr, "NULL argument");
+    f->num_steps = s;
+  });
+}
+
+covap_status covap_feedback_reset(covap_feedback* f, void* stream) {
+  return guarded([&] {
+    need(f != nullptr, "NULL argument");
+    DeviceGuard dg(f->device);
+    CK(cudaMemsetAsync(f->residual, 0, f->total * f->esize, as_stream(stream)));
+    f->num_steps = 0;
+  });
+}
+
+covap_status covap_feedback_step(covap_feedback* f, const void* grad, void* kept, void* stream) {
+  return guarded([&] {
+    need(f && grad && kept, "NULL argument");
+    DeviceGuard dg(f->device);
+    ef_step(f, grad, kept, kept, false, as_stream(stream));
+  });
+}
+
+covap_status covap_feedback_transmitted(const covap_feedback* f, uint64_t step, uint64_t* elems,
+                                        uint64_t* bytes) {
+  return guarded([&] {
+    need(f != nullptr, "NULL argument");
+    uint64_t e = 0, b = 0;
+    switch (f->filter.kind) {
+      case COVAP_FILTER_COVAP: {
+        const auto keep = covapb::select(step, f->filter.interval, f->numel.size(), f->filter.rule);
+        for (size_t t = 0; t < keep.size(); ++t)
+          if (keep[t]) e += f->numel[t];
+        b = e * 4;
+        break;
+      }
+      case COVAP_FILTER_TOPK:
+      case COVAP_FILTER_RANDOMK:
+        e = f->k_total;
+        b = e * 8;  // index + value pairs (trainer.cpp:398-400)
+        break;
+      case COVAP_FILTER_FP16:
+        e = f->total;
+        b = e * 2;
+        break;
+      default:
+        e = f->total;
+        b = e * 4;
+    }
+    if (elems) *elems = e;
+    if (bytes) *bytes = b;
+  });
+}
+
+covap_status covap_feedback_saturations(covap_feedback* f, uint64_t* count, void* stream) {
+  return guarded([&] {
+    need(f && count, "NULL argument");
+    DeviceGuard dg(f->device);
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, f->d_sat, 8, cudaMemcpyDeviceToHost, as_stream(stream)));
+    CK(cudaStreamSynchronize(as_stream(stream)));
+    *count = v;
+  });
+}
+
+covap_status covap_feedback_pack(covap_feedback* f, const void* grad, void* out, void* stream) {
+  return guarded([&] {
+    need(f && grad, "NULL argument");
+    need(!sparse(f) || out != nullptr, "out must not be NULL for the sparse filters");
+    need(f->filter.kind >= COVAP_FILTER_TOPK, "the identity / covap filters have no sync wire");
+    DeviceGuard dg(f->device);
+    ef_step(f, grad, nullptr, sparse(f) ? out : nullptr, true, as_stream(stream));
+  });
+}
+
+covap_status covap_feedback_wire(covap_feedback* f, void** a, uint64_t* ba, void** b,
+                                 uint64_t* bb) {
+  return guarded([&] {
+    need(f && a && ba && b && bb, "NULL argument");
+    wire_of(f, a, ba, b, bb);
+  });
+}
+
+covap_status covap_feedback_combine(covap_feedback* f, const void* ra, const void* rb, int P,
+                                    void* out, void* stream) {
+  return guarded([&] {
+    need(f && out, "NULL argument");
+    DeviceGuard dg(f->device);
+    combine(f, ra, rb, P, out, as_stream(stream));
+  });
+}
+
+covap_status covap_feedback_sync_step(covap_feedback* f, covap_comm* comm, const void* grad,
+                                      void* out, void* stream) {
+  return guarded([&] {
+    need(f && grad && out, "NULL argument");
+    need(f->filter.kind >= COVAP_FILTER_TOPK,
+         "the identity / covap filters have no sync wire (use covap_sync_step)");
+    DeviceGuard dg(f->device);
+    const cudaStream_t st = as_stream(stream);
+    ef_step(f, grad, nullptr, sparse(f) ? out : nullptr, true, st);
+    void *a, *b;
+    uint64_t ba, bb;
+    wire_of(f, &a, &ba, &b, &bb);
+    const int P = world(comm);
+    if (P == 1) {
+      combine(f, a, b, 1, out, st);
+      return;
+    }
+    grow(&f->recv_a, &f->cap_a, ba * P);
+    grow(&f->recv_b, &f->cap_b, bb * P);
+    NK(ncclGroupStart());
+    if (ba) NK(ncclAllGather(a, f->recv_a, ba, ncclUint8, comm->nccl, st));
+    if (bb) NK(ncclAllGather(b, f->recv_b, bb, ncclUint8, comm->nccl, st));
+    NK(ncclGroupEnd());
+    combine(f, f->recv_a, f->recv_b, P, out, st);
+  });
+}
+
+covap_status covap_topk_compress(int device, int dtype, const void* x, uint64_t d,
+                                 double k_fraction, uint64_t* indices, void* values, uint64_t* k,
+                                 void* stream) {
+  covap_feedback* f = nullptr;
+  const covap_filter flt{COVAP_FILTER_TOPK, 1, 0, k_fraction, 0};
+  const covap_ef off{0, 0.0, 1, 0.0};
+  covap_status st = guarded([&] { sparsifier_k(d, k_fraction); });
+  if (st != COVAP_OK) return st;
+  st = covap_feedback_create(&d, 1, dtype, &off, &flt, device, &f);
+  if (st != COVAP_OK) return st;
+  st = guarded([&] {
+    need(x && indices && values && k, "NULL argument");
+    DeviceGuard dg(device);
+    const cudaStream_t s = as_stream(stream);
+    ef_step(f, x, nullptr, nullptr, true, s);
+    CK(fb::order_list(dtype == COVAP_F64 ? 1 : 0, fb::kTopk, f->list_idx, f->list_val, f->k_total,
+                      indices, values, s));
+    CK(cudaStreamSynchronize(s));
+    *k = f->k_total;
+  });
+  covap_feedback_destroy(f);
+  return st;
+}
+
+covap_status covap_randomk_compress(int device, int dtype, const void* x, uint64_t d,
+                                    double k_fraction, uint64_t seed, uint64_t* indices,
+                                    void* values, uint64_t* k, void* stream) {
+  covap_feedback* f = nullptr;
+  // randomk_compress draws from SplitMix64(seed) directly; the filter's
+  // per-tensor seed is mix_seed(seed', step*0x10001 + t).  Drive the kernels
+  // with that seed through a one-tensor state whose draws use `seed` as is.
+  const covap_filter flt{COVAP_FILTER_RANDOMK, 1, 0, k_fraction, 0};
+  const covap_ef off{0, 0.0, 1, 0.0};
+  covap_status st = guarded([&] { sparsifier_k(d, k_fraction); });
+  if (st != COVAP_OK) return st;
+  st = covap_feedback_create(&d, 1, dtype, &off, &flt, device, &f);
+  if (st != COVAP_OK) return st;
+  st = guarded([&] {
+    need(x && indices && values && k, "NULL argument");
+    DeviceGuard dg(device);
+    const cudaStream_t s = as_stream(stream);
+    const int dt = dtype == COVAP_F64 ? 1 : 0;
+    CK(fb::launch_compensate(dt, x, f->residual, nullptr, nullptr, f->chunks, f->nchunks, 0, 0.0,
+                             f->sms, s));
+    fb::RandomkArgs a = randomk_args(f);
+    a.raw_seed = 1;
+    a.seed = seed;
+    CK(fb::launch_randomk_select(a, f->sms, s));
+    CK(fb::launch_randomk_gather(dt, a, f->residual, nullptr, f->list_idx, f->list_val, f->sms, s));
+    CK(fb::order_list(dt, fb::kRandomk, f->list_idx, f->list_val, f->k_total, indices, values, s));
+    CK(cudaStreamSynchronize(s));
+    *k = f->k_total;
+  });
+  covap_feedback_destroy(f);
+  return st;
+}
+
+covap_status covap_fp16_roundtrip(int device, int dtype, const void* x, uint64_t n, void* out,
+                                  uint64_t* saturations, void* stream) {
+  covap_feedback* f = nullptr;
+  const covap_filter flt{COVAP_FILTER_FP16, 1, 0, 0.0, 0};
+  const covap_ef off{0, 0.0, 1, 0.0};
+  if (n == 0) {
+    if (saturations) *saturations = 0;
+    return COVAP_OK;
+  }
+  covap_status st = covap_feedback_create(&n, 1, dtype, &off, &flt, device, &f);
+  if (st != COVAP_OK) return st;
+  st = guarded([&] {
+    need(x && out, "NULL argument");
+    DeviceGuard dg(device);
+    const cudaStream_t s = as_stream(stream);
+    fb::DenseArgs a{};
+    a.g = x;
+    a.r = nullptr;
+    a.kept = out;
+    a.sat = f->d_sat;
+    a.chunks = f->chunks;
+    a.nchunks = f->nchunks;
+    a.ef = 0;
+    CK(fb::launch_dense(dtype == COVAP_F64 ? 1 : 0, COVAP_FILTER_FP16, a, f->sms, s));
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, f->d_sat, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (saturations) *saturations = v;
+  });
+  covap_feedback_destroy(f);
+  return st;
+}
+
+}  // extern "C"
