@@ -145,6 +145,108 @@ CompressedUpdate covap_compress(const GradientSet& gradients, CompressorState& s
 GradientSet covap_decompress(const CompressedUpdate& update,
                              const std::vector<std::uint64_t>& numels);
 
+// ------------------------------------------------------------------ baseline compressors
+// (compress.hpp:66-164), on the GPU (covap_feedback.cu).
+
+struct SparseSelection {
+  std::vector<std::size_t> indices;
+  std::vector<double> values;  // aligned with indices
+};
+
+// ceil(k_fraction * d) entries of largest magnitude; ties keep the lower index.
+SparseSelection topk_compress(std::span<const double> x, double k_fraction);
+// ceil(k_fraction * d) indices sampled uniformly without replacement from
+// SplitMix64(seed), ascending.
+SparseSelection randomk_compress(std::span<const double> x, double k_fraction, std::uint64_t seed);
+// Nearest half-precision value, widened back; clamps to +-65504 and counts.
+TensorVec fp16_roundtrip(std::span<const double> x, std::uint64_t* saturation_count = nullptr);
+std::uint16_t half_bits_from_float(float value, bool* saturated = nullptr);
+float float_from_half_bits(std::uint16_t bits);
+
+// A dense view of a compressor (compress.hpp:95-102).  The built-in filters
+// below run on the device; descriptor() names the kernel.  A user-defined
+// subclass may override keep() / transmitted_elements() for direct calls;
+// ErrorFeedback runs only the built-in filters (InvalidInput otherwise).
+class GradientFilter {
+ public:
+  virtual ~GradientFilter() = default;
+  virtual GradientSet keep(const GradientSet& gradients, std::uint64_t step) const;
+  virtual std::uint64_t transmitted_elements(const GradientSet& gradients,
+                                             std::uint64_t step) const;
+  // kind < 0: not a built-in filter.
+  virtual covap_filter descriptor() const { return covap_filter{-1, 1, 0, 0.0, 0}; }
+};
+
+class IdentityFilter final : public GradientFilter {
+ public:
+  covap_filter descriptor() const override { return covap_filter{COVAP_FILTER_IDENTITY, 1, 0, 0.0, 0}; }
+};
+
+class CovapFilter final : public GradientFilter {
+ public:
+  CovapFilter(std::uint32_t interval, SelectionRule rule = SelectionRule::kMatchStep)
+      : interval_(interval), rule_(rule) {}
+  covap_filter descriptor() const override {
+    return covap_filter{COVAP_FILTER_COVAP, interval_, rule_ == SelectionRule::kPlusStep ? 1 : 0,
+                        0.0, 0};
+  }
+
+ private:
+  std::uint32_t interval_;
+  SelectionRule rule_;
+};
+
+class TopkFilter final : public GradientFilter {
+ public:
+  explicit TopkFilter(double k_fraction) : k_fraction_(k_fraction) {}
+  covap_filter descriptor() const override { return covap_filter{COVAP_FILTER_TOPK, 1, 0, k_fraction_, 0}; }
+
+ private:
+  double k_fraction_;
+};
+
+class RandomkFilter final : public GradientFilter {
+ public:
+  RandomkFilter(double k_fraction, std::uint64_t seed) : k_fraction_(k_fraction), seed_(seed) {}
+  covap_filter descriptor() const override {
+    return covap_filter{COVAP_FILTER_RANDOMK, 1, 0, k_fraction_, seed_};
+  }
+
+ private:
+  double k_fraction_;
+  std::uint64_t seed_;
+};
+
+class Fp16Filter final : public GradientFilter {
+ public:
+  covap_filter descriptor() const override { return covap_filter{COVAP_FILTER_FP16, 1, 0, 0.0, 0}; }
+};
+
+// Residual accumulation around any built-in filter (compress.hpp:151-164):
+// G += coeff * residuals before filtering, residuals = G - kept afterwards.
+// Value semantics as in the reference (residuals live on the host between
+// steps); the step itself runs in the device kernels.
+class ErrorFeedback {
+ public:
+  ErrorFeedback(const std::vector<std::uint64_t>& numels, EfSchedule schedule);
+  ~ErrorFeedback();
+  ErrorFeedback(const ErrorFeedback&) = delete;
+  ErrorFeedback& operator=(const ErrorFeedback&) = delete;
+
+  GradientSet step(const GradientSet& gradients, const GradientFilter& filter);
+
+  const GradientSet& residuals() const { return residuals_; }
+  std::uint64_t num_steps() const { return num_steps_; }
+
+ private:
+  struct Device;
+  std::vector<std::uint64_t> numels_;
+  GradientSet residuals_;
+  EfSchedule schedule_;
+  std::uint64_t num_steps_ = 0;
+  std::unique_ptr<Device> dev_;
+};
+
 // ------------------------------------------------------------------ trainer
 // (0 + v_0 + ... + v_{P-1}) * (1/P) in worker order, on the GPU.
 std::vector<double> allreduce_mean(const std::vector<std::vector<double>>& per_worker);

@@ -420,6 +420,13 @@ covap_status covap_randomk_compress(int device, int dtype, const void* x, uint64
                                     void* values, uint64_t* k, void* stream);
 covap_status covap_fp16_roundtrip(int device, int dtype, const void* x, uint64_t n, void* out,
                                   uint64_t* saturations, void* stream);
+/* half_bits_from_float / float_from_half_bits (compress.cpp:157-224) over
+ * device vectors: encode takes f32 (dtype COVAP_F32) or f64 values (narrowed
+ * to float first, as fp16_roundtrip does); decode widens to float. */
+covap_status covap_fp16_encode(int device, int dtype, const void* x, uint64_t n, uint16_t* bits,
+                               uint64_t* saturations, void* stream);
+covap_status covap_fp16_decode(int device, const uint16_t* bits, uint64_t n, float* out,
+                               void* stream);
 
 /* ------------------------------------------------------ harness kernels -- */
 

@@ -139,6 +139,8 @@ _SIGS = {
     "covap_topk_compress": (None, [i32, i32, vp, u64, f64, vp, vp, u64p, vp]),
     "covap_randomk_compress": (None, [i32, i32, vp, u64, f64, u64, vp, vp, u64p, vp]),
     "covap_fp16_roundtrip": (None, [i32, i32, vp, u64, vp, u64p, vp]),
+    "covap_fp16_encode": (None, [i32, i32, vp, u64, vp, u64p, vp]),
+    "covap_fp16_decode": (None, [i32, vp, u64, vp, vp]),
     "covap_stream_key": (u64, [u64, u64, u64]),
     "covap_generate": (None, [vp, u64, i32, u64, i32, u64, vp]),
     "covap_spin": (None, [f64, i32, vp]),

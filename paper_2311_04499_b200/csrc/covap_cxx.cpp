@@ -503,6 +503,206 @@ std::vector<double> allreduce_mean(const std::vector<std::vector<double>>& per_w
   return out;
 }
 
+// ------------------------------------------------------------------ baseline compressors (§8(f4))
+
+namespace {
+
+std::vector<uint64_t> numels_of(const GradientSet& g) {
+  std::vector<uint64_t> n;
+  for (const auto& t : g) n.push_back(t.size());
+  return n;
+}
+
+std::vector<double> flatten(const GradientSet& g, uint64_t total) {
+  std::vector<double> flat;
+  flat.reserve(total);
+  for (const auto& t : g) flat.insert(flat.end(), t.begin(), t.end());
+  return flat;
+}
+
+GradientSet unflatten(const std::vector<double>& flat, const std::vector<uint64_t>& numels) {
+  GradientSet out;
+  uint64_t off = 0;
+  for (uint64_t n : numels) {
+    out.emplace_back(flat.begin() + off, flat.begin() + off + n);
+    off += n;
+  }
+  return out;
+}
+
+struct FeedbackHandle {
+  covap_feedback* f = nullptr;
+  ~FeedbackHandle() {
+    if (f) covap_feedback_destroy(f);
+  }
+};
+
+SparseSelection sparse_select(std::span<const double> x, double k_fraction, bool topk,
+                              std::uint64_t seed) {
+  uint64_t k = 0;
+  check(covap_sparsifier_k(x.size(), k_fraction, &k));
+  b200::DevBuf dx(x.size() * 8), di(x.size() * 8), dv(x.size() * 8);
+  check(covap_memcpy(dx.p, x.data(), x.size() * 8, 0, nullptr));
+  uint64_t got = 0;
+  if (topk)
+    check(covap_topk_compress(0, COVAP_F64, dx.p, x.size(), k_fraction, static_cast<uint64_t*>(di.p),
+                              dv.p, &got, nullptr));
+  else
+    check(covap_randomk_compress(0, COVAP_F64, dx.p, x.size(), k_fraction, seed,
+                                 static_cast<uint64_t*>(di.p), dv.p, &got, nullptr));
+  std::vector<uint64_t> idx(got);
+  SparseSelection out;
+  out.values.resize(got);
+  check(covap_memcpy(idx.data(), di.p, got * 8, 1, nullptr));
+  check(covap_memcpy(out.values.data(), dv.p, got * 8, 1, nullptr));
+  check(covap_stream_synchronize(nullptr));
+  out.indices.assign(idx.begin(), idx.end());
+  return out;
+}
+
+}  // namespace
+
+SparseSelection topk_compress(std::span<const double> x, double k_fraction) {
+  return sparse_select(x, k_fraction, true, 0);
+}
+
+SparseSelection randomk_compress(std::span<const double> x, double k_fraction,
+                                 std::uint64_t seed) {
+  return sparse_select(x, k_fraction, false, seed);
+}
+
+TensorVec fp16_roundtrip(std::span<const double> x, std::uint64_t* saturation_count) {
+  TensorVec out(x.size());
+  if (x.empty()) return out;
+  b200::DevBuf dx(x.size() * 8), dy(x.size() * 8);
+  check(covap_memcpy(dx.p, x.data(), x.size() * 8, 0, nullptr));
+  uint64_t sat = 0;
+  check(covap_fp16_roundtrip(0, COVAP_F64, dx.p, x.size(), dy.p, &sat, nullptr));
+  check(covap_memcpy(out.data(), dy.p, x.size() * 8, 1, nullptr));
+  check(covap_stream_synchronize(nullptr));
+  if (saturation_count) *saturation_count += sat;
+  return out;
+}
+
+std::uint16_t half_bits_from_float(float value, bool* saturated) {
+  b200::DevBuf dx(4), dh(2);
+  check(covap_memcpy(dx.p, &value, 4, 0, nullptr));
+  uint64_t sat = 0;
+  check(covap_fp16_encode(0, COVAP_F32, dx.p, 1, static_cast<uint16_t*>(dh.p), &sat, nullptr));
+  std::uint16_t h = 0;
+  check(covap_memcpy(&h, dh.p, 2, 1, nullptr));
+  check(covap_stream_synchronize(nullptr));
+  if (sat && saturated) *saturated = true;
+  return h;
+}
+
+float float_from_half_bits(std::uint16_t bits) {
+  b200::DevBuf dh(2), dx(4);
+  check(covap_memcpy(dh.p, &bits, 2, 0, nullptr));
+  check(covap_fp16_decode(0, static_cast<const uint16_t*>(dh.p), 1, static_cast<float*>(dx.p),
+                          nullptr));
+  float v = 0.0f;
+  check(covap_memcpy(&v, dx.p, 4, 1, nullptr));
+  check(covap_stream_synchronize(nullptr));
+  return v;
+}
+
+// GradientFilter::keep for the built-in filters: one error-feedback step
+// with compensation off (c = g), at `step`, on the device.
+GradientSet GradientFilter::keep(const GradientSet& g, std::uint64_t step) const {
+  const covap_filter d = descriptor();
+  if (d.kind < 0) throw InvalidInput("keep() is not implemented by this filter");
+  const auto numels = numels_of(g);
+  if (numels.empty()) return {};
+  uint64_t total = 0;
+  for (auto n : numels) total += n;
+  const covap_ef off{0, 0.0, 1, 0.0};
+  FeedbackHandle h;
+  check(covap_feedback_create(numels.data(), numels.size(), COVAP_F64, &off, &d, 0, &h.f));
+  check(covap_feedback_set_step(h.f, step));
+  b200::DevBuf dg(total * 8), dk(total * 8);
+  const auto flat = flatten(g, total);
+  check(covap_memcpy(dg.p, flat.data(), total * 8, 0, nullptr));
+  check(covap_feedback_step(h.f, dg.p, dk.p, nullptr));
+  std::vector<double> kept(total);
+  check(covap_memcpy(kept.data(), dk.p, total * 8, 1, nullptr));
+  check(covap_stream_synchronize(nullptr));
+  return unflatten(kept, numels);
+}
+
+std::uint64_t GradientFilter::transmitted_elements(const GradientSet& g,
+                                                   std::uint64_t step) const {
+  const covap_filter d = descriptor();
+  if (d.kind < 0) throw InvalidInput("transmitted_elements() is not implemented by this filter");
+  const auto numels = numels_of(g);
+  if (numels.empty()) return 0;
+  const covap_ef off{0, 0.0, 1, 0.0};
+  FeedbackHandle h;
+  check(covap_feedback_create(numels.data(), numels.size(), COVAP_F64, &off, &d, 0, &h.f));
+  uint64_t e = 0;
+  check(covap_feedback_transmitted(h.f, step, &e, nullptr));
+  return e;
+}
+
+// The device state behind one ErrorFeedback, rebuilt when the filter changes.
+struct ErrorFeedback::Device {
+  covap_filter filter{};
+  FeedbackHandle h;
+  std::unique_ptr<b200::DevBuf> grad, kept;
+};
+
+ErrorFeedback::ErrorFeedback(const std::vector<std::uint64_t>& numels, EfSchedule schedule)
+    : numels_(numels), schedule_(schedule) {
+  residuals_.reserve(numels.size());
+  for (std::uint64_t n : numels) residuals_.emplace_back(n, 0.0);
+}
+
+ErrorFeedback::~ErrorFeedback() = default;
+
+GradientSet ErrorFeedback::step(const GradientSet& gradients, const GradientFilter& filter) {
+  if (gradients.size() != residuals_.size())
+    throw InvalidState("gradient tensor count does not match error-feedback state");
+  for (size_t t = 0; t < gradients.size(); ++t)
+    if (gradients[t].size() != residuals_[t].size())
+      throw InvalidState("gradient shape mismatch at tensor " + std::to_string(t));
+  const covap_filter d = filter.descriptor();
+  if (d.kind < 0) throw InvalidInput("ErrorFeedback on the device runs the built-in filters");
+  if (numels_.empty()) {
+    ++num_steps_;
+    return {};
+  }
+  uint64_t total = 0;
+  for (auto n : numels_) total += n;
+  const bool same = dev_ && dev_->filter.kind == d.kind && dev_->filter.interval == d.interval &&
+                    dev_->filter.rule == d.rule && dev_->filter.k_fraction == d.k_fraction &&
+                    dev_->filter.seed == d.seed;
+  if (!same) {
+    auto dv = std::make_unique<Device>();
+    dv->filter = d;
+    const covap_ef ef = b200::ef_of(schedule_);
+    check(covap_feedback_create(numels_.data(), numels_.size(), COVAP_F64, &ef, &d, 0, &dv->h.f));
+    dv->grad = std::make_unique<b200::DevBuf>(total * 8);
+    dv->kept = std::make_unique<b200::DevBuf>(total * 8);
+    dev_ = std::move(dv);
+  }
+  covap_feedback* f = dev_->h.f;
+  void* res = nullptr;
+  check(covap_feedback_residual(f, &res, nullptr));
+  const auto g = flatten(gradients, total);
+  const auto r = flatten(residuals_, total);
+  check(covap_memcpy(dev_->grad->p, g.data(), total * 8, 0, nullptr));
+  check(covap_memcpy(res, r.data(), total * 8, 0, nullptr));
+  check(covap_feedback_set_step(f, num_steps_));
+  check(covap_feedback_step(f, dev_->grad->p, dev_->kept->p, nullptr));
+  std::vector<double> kept(total), rnew(total);
+  check(covap_memcpy(kept.data(), dev_->kept->p, total * 8, 1, nullptr));
+  check(covap_memcpy(rnew.data(), res, total * 8, 1, nullptr));
+  check(covap_stream_synchronize(nullptr));
+  residuals_ = unflatten(rnew, numels_);
+  ++num_steps_;
+  return unflatten(kept, numels_);
+}
+
 double ccr(double comm_ms, double comp_ms) {
   double c = 0.0;
   check(covap_ccr(comm_ms, comp_ms, &c));

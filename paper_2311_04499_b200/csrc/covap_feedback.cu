@@ -611,6 +611,13 @@ __global__ void list_finish_kernel(const uint32_t* __restrict__ idx, uint64_t cn
   }
 }
 
+__global__ void fp16_decode_kernel(const uint16_t* __restrict__ bits, uint64_t n,
+                                   float* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = half_to_float(bits[i]);
+}
+
 // ------------------------------------------------------------- ordering
 
 template <typename T>
@@ -877,6 +884,13 @@ cudaError_t launch_list_finish(int dtype, const uint32_t* idx, uint64_t cnt, voi
     list_finish_kernel<float><<<grid, kThreads, 0, s>>>(idx, cnt, static_cast<float*>(acc),
                                                         static_cast<float>(inv),
                                                         static_cast<float*>(out), clear);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fp16_decode(const uint16_t* bits, uint64_t n, float* out, int sms,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  fp16_decode_kernel<<<grid_for(n, sms, 8), kThreads, 0, s>>>(bits, n, out);
   return cudaGetLastError();
 }
 

@@ -118,6 +118,10 @@ cudaError_t launch_list_accumulate(int dtype, const uint32_t* idx, const void* v
 cudaError_t launch_list_finish(int dtype, const uint32_t* idx, uint64_t cnt, void* acc,
                                double inv, void* out, int clear, int sms, cudaStream_t s);
 
+// float_from_half_bits over a vector (compress.cpp:207-224).
+cudaError_t launch_fp16_decode(const uint16_t* bits, uint64_t n, float* out, int sms,
+                               cudaStream_t s);
+
 // Reference output order for the standalone compressors: top-k by (|x| desc,
 // index asc), random-k by index asc.  idx are positions; writes 64-bit
 // positions and values.

@@ -594,3 +594,49 @@ covap_status covap_fp16_roundtrip(int device, int dtype, const void* x, uint64_t
 }
 
 }  // extern "C"
+
+extern "C" {
+
+covap_status covap_fp16_encode(int device, int dtype, const void* x, uint64_t n, uint16_t* bits,
+                               uint64_t* saturations, void* stream) {
+  if (n == 0) {
+    if (saturations) *saturations = 0;
+    return COVAP_OK;
+  }
+  covap_feedback* f = nullptr;
+  const covap_filter flt{COVAP_FILTER_FP16, 1, 0, 0.0, 0};
+  const covap_ef off{0, 0.0, 1, 0.0};
+  covap_status st = covap_feedback_create(&n, 1, dtype, &off, &flt, device, &f);
+  if (st != COVAP_OK) return st;
+  st = guarded([&] {
+    need(x && bits, "NULL argument");
+    DeviceGuard dg(device);
+    const cudaStream_t s = as_stream(stream);
+    fb::DenseArgs a{};
+    a.g = x;
+    a.wire = bits;
+    a.sat = f->d_sat;
+    a.chunks = f->chunks;
+    a.nchunks = f->nchunks;
+    CK(fb::launch_dense(dtype == COVAP_F64 ? 1 : 0, COVAP_FILTER_FP16, a, f->sms, s));
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, f->d_sat, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (saturations) *saturations = v;
+  });
+  covap_feedback_destroy(f);
+  return st;
+}
+
+covap_status covap_fp16_decode(int device, const uint16_t* bits, uint64_t n, float* out,
+                               void* stream) {
+  return guarded([&] {
+    need(n == 0 || (bits && out), "NULL argument");
+    DeviceGuard dg(device);
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CK(fb::launch_fp16_decode(bits, n, out, sms, as_stream(stream)));
+  });
+}
+
+}  // extern "C"

@@ -3,10 +3,10 @@ test_model.cpp, compiled unchanged by tests/cxx/Makefile) against the B200
 library's drop-in C++ headers (include/covap/) and libcovap_cxx.so.
 
 Skipped by name: the cases that exercise components outside the hot path
-(Top-k / Random-k / fp16 compressors, the generic
-error-feedback wrapper, compute-time split, JSON I/O).  Every other case of
-the two files must pass: the planner/selection/EF ones on CPU, the
-covap_compress / covap_decompress ones on the GPU (fp64 kernels).
+(compute-time split, JSON I/O).  Every other case of the two files must pass:
+the planner/selection/EF ones on CPU; covap_compress / covap_decompress and
+the baseline compressors under the error-feedback wrapper (Top-k, Random-k,
+fp16, §8(f4)) on the GPU (fp64 kernels).
 """
 import os
 import subprocess
@@ -18,14 +18,6 @@ from conftest import ROOT
 BIN = os.path.join(ROOT, "tests", "cxx", "_build", "ref_unit_tests")
 
 OUT_OF_SCOPE = [
-    "largest magnitudes win with ties to the lower index",
-    "no same-size selection beats the magnitude selection",
-    "random selection is reproducible and of exact size",
-    "random selection is uniform over seeds",
-    "half precision round trip",
-    "half precision conversion is idempotent",
-    "shared feedback wrapper conserves mass for every scheme",
-    "feedback wrapper with the tensor filter matches the fused compressor",
     "compute time split is proportional to elements",
     "declared layer times win over proportional split",
     "model JSON round trip",
@@ -59,6 +51,15 @@ DEVICE = [
     "decompression embeds payload and zero-fills",
     "round trip matches the direct filter at any phase",
     "transmitted mass plus residuals conserves the gradient sum",
+    # baseline compressors + ErrorFeedback (covap_feedback.cu)
+    "largest magnitudes win with ties to the lower index",
+    "no same-size selection beats the magnitude selection",
+    "random selection is reproducible and of exact size",
+    "random selection is uniform over seeds",
+    "half precision round trip",
+    "half precision conversion is idempotent",
+    "shared feedback wrapper conserves mass for every scheme",
+    "feedback wrapper with the tensor filter matches the fused compressor",
 ]
 
 
