@@ -18,6 +18,8 @@
 // contraction disabled (__fmul_rn / __fadd_rn / __fsub_rn), so the fp64
 // instantiation is bit-exact against the reference and the fp32 one against
 // the same sequence in single precision (the tests' fp32 restatement).
+#include <cuda_fp16.h>
+
 #include <cub/cub.cuh>
 
 #include "covap_feedback.h"
@@ -28,8 +30,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kUnroll = 8;
-constexpr int kDigitBits = 11;
-constexpr int kDigits = 1 << kDigitBits;
 
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
@@ -60,44 +60,24 @@ __device__ __forceinline__ uint32_t bin_of(T c) {
   return static_cast<uint32_t>(KeyOf<T>::key(c) >> (KeyOf<T>::kBits - kBinBits));
 }
 
-// half_bits_from_float (compress.cpp:157-205): round to nearest even,
-// saturate to +-65504, NaN -> 0x7e00, below 2^-24 -> signed zero.
+// half_bits_from_float (compress.cpp:157-205).  The reference rounds to
+// nearest even on the normal and subnormal half grids, which is what the
+// hardware conversion (cvt.rn.f16.f32) does for |x| in [2^-24, 65504]; its
+// three departures from IEEE are patched explicitly: NaN -> 0x7e00,
+// |x| > 65504 (inf included) -> +-65504 and counted as saturated (IEEE
+// would round 65504 < |x| < 65520 down and give inf above), and
+// |x| < 2^-24 -> signed zero (IEEE rounds (2^-25, 2^-24) up).
 __device__ __forceinline__ uint16_t half_bits(float value, bool& saturated) {
   const uint32_t bits = __float_as_uint(value);
   const uint32_t sign = (bits >> 16) & 0x8000u;
-  const uint32_t abs_bits = bits & 0x7fffffffu;
-  if (abs_bits > 0x7f800000u) return static_cast<uint16_t>(sign | 0x7e00u);
-  if (__uint_as_float(abs_bits) > 65504.0f) {
+  const uint32_t a = bits & 0x7fffffffu;
+  if (a > 0x7f800000u) return static_cast<uint16_t>(sign | 0x7e00u);
+  if (a > 0x477fe000u) {  // 65504.0f
     saturated = true;
     return static_cast<uint16_t>(sign | 0x7bffu);
   }
-  const int32_t e = static_cast<int32_t>((abs_bits >> 23) & 0xff) - 127;
-  uint32_t mant = abs_bits & 0x7fffffu;
-  if (e < -24) return static_cast<uint16_t>(sign);
-  if (e < -14) {
-    mant |= 0x800000u;
-    const uint32_t shift = static_cast<uint32_t>(-14 - e) + 13;
-    const uint32_t hm = mant >> shift;
-    const uint32_t rest = mant & ((1u << shift) - 1);
-    const uint32_t halfway = 1u << (shift - 1);
-    const uint32_t rounded = hm + ((rest > halfway || (rest == halfway && (hm & 1u))) ? 1u : 0u);
-    return static_cast<uint16_t>(sign | rounded);
-  }
-  uint32_t he = static_cast<uint32_t>(e + 15);
-  uint32_t hm = mant >> 13;
-  const uint32_t rest = mant & 0x1fffu;
-  if (rest > 0x1000u || (rest == 0x1000u && (hm & 1u))) {
-    ++hm;
-    if (hm == 0x400u) {
-      hm = 0;
-      ++he;
-    }
-  }
-  if (he >= 31) {
-    saturated = true;
-    return static_cast<uint16_t>(sign | 0x7bffu);
-  }
-  return static_cast<uint16_t>(sign | (he << 10) | hm);
+  if (a < 0x33800000u) return static_cast<uint16_t>(sign);  // 2^-24
+  return __half_as_ushort(__float2half_rn(value));
 }
 
 // float_from_half_bits (compress.cpp:207-224).
@@ -159,36 +139,74 @@ __global__ void __launch_bounds__(kThreads) dense_kernel(DenseArgs A) {
       const uint64_t phase = A.step % A.interval, rem = ch.tensor % A.interval;
       sel = A.rule ? ((rem + phase) % A.interval == 0) : (rem == phase);
     }
-    for (uint64_t base = ch.begin; base < ch.end; base += kThreads * kUnroll) {
-      T gv[kUnroll], rv[kUnroll];
+    // kept = f(c), residual = compensated - kept (compress.cpp:339-341)
+    auto one = [&](T c, T& k, T& res, uint16_t& h) {
+      if (KIND == kFp16) {
+        bool s = false;
+        h = half_bits(static_cast<float>(c), s);
+        nsat += s ? 1 : 0;
+        k = static_cast<T>(half_to_float(h));
+      } else if (KIND == kCovap) {
+        k = sel ? c : T(0);
+      } else {
+        k = c;
+      }
+      res = sub_rn(c, k);
+    };
+    if (ch.pad == 0) {
+      // 16-byte-aligned body chunk: kVec vectors per thread in flight
+      using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+      constexpr int W = 16 / static_cast<int>(sizeof(T));
+      constexpr int kVec = 4;
+      const uint32_t v1 = static_cast<uint32_t>(ch.end / W);
+      const V* g4 = reinterpret_cast<const V*>(g);
+      V* r4 = reinterpret_cast<V*>(r);
+      V* k4 = reinterpret_cast<V*>(kept);
+      for (uint32_t vb = static_cast<uint32_t>(ch.begin / W) + threadIdx.x; vb < v1;
+           vb += kThreads * kVec) {
+        V gv[kVec], rv[kVec];
 #pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
-        const uint64_t i = base + q * kThreads + threadIdx.x;
-        if (i < ch.end) {
-          gv[q] = g[i];
-          rv[q] = A.ef ? r[i] : T(0);
+        for (int u = 0; u < kVec; ++u) {
+          const uint32_t v = vb + u * kThreads;
+          if (v < v1) {
+            gv[u] = g4[v];
+            rv[u] = A.ef ? r4[v] : V{};
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) {
+          const uint32_t v = vb + u * kThreads;
+          if (v >= v1) continue;
+          V kv, nr;
+          uint16_t hv[W];
+          const T* gs = reinterpret_cast<const T*>(&gv[u]);
+          const T* rs = reinterpret_cast<const T*>(&rv[u]);
+          T* ks = reinterpret_cast<T*>(&kv);
+          T* ns = reinterpret_cast<T*>(&nr);
+#pragma unroll
+          for (int w = 0; w < W; ++w) one(compensate(gs[w], rs[w], coeff, A.ef), ks[w], ns[w], hv[w]);
+          if (kept) k4[v] = kv;
+          if (r) r4[v] = nr;
+          if (KIND == kFp16 && A.wire) {
+            if (W == 4)
+              reinterpret_cast<uint2*>(A.wire)[v] =
+                  make_uint2(hv[0] | (uint32_t(hv[1]) << 16), hv[2 % W] | (uint32_t(hv[3 % W]) << 16));
+            else
+              reinterpret_cast<uint32_t*>(A.wire)[v] = hv[0] | (uint32_t(hv[1 % W]) << 16);
+          }
         }
       }
-#pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
-        const uint64_t i = base + q * kThreads + threadIdx.x;
-        if (i >= ch.end) continue;
-        const T c = compensate(gv[q], rv[q], coeff, A.ef);
-        T k;
-        if (KIND == kFp16) {
-          bool s = false;
-          const uint16_t h = half_bits(static_cast<float>(c), s);
-          nsat += s ? 1 : 0;
-          k = static_cast<T>(half_to_float(h));
-          if (A.wire) A.wire[i] = h;
-        } else if (KIND == kCovap) {
-          k = sel ? c : T(0);
-        } else {
-          k = c;
-        }
-        if (kept) kept[i] = k;
-        if (r) r[i] = sub_rn(c, k);  // residual = compensated - kept (compress.cpp:339-341)
-      }
+      continue;
+    }
+    for (uint64_t base = ch.begin; base < ch.end; base += kThreads) {
+      const uint64_t i = base + threadIdx.x;
+      if (i >= ch.end) continue;
+      T k, res;
+      uint16_t h = 0;
+      one(compensate(g[i], A.ef ? r[i] : T(0), coeff, A.ef), k, res, h);
+      if (kept) kept[i] = k;
+      if (r) r[i] = res;
+      if (KIND == kFp16 && A.wire) A.wire[i] = h;
     }
   }
   if (KIND == kFp16 && A.sat) {
@@ -254,136 +272,344 @@ __global__ void __launch_bounds__(kThreads)
 
 // --------------------------------------------------------------- top-k
 
-// One CTA per tensor: the bin holding the k-th largest |c|.
-__global__ void __launch_bounds__(kThreads)
-    topk_threshold_kernel(uint32_t* hist, const uint32_t* k, uint32_t* thr, uint32_t* need,
-                          uint32_t* sel_cnt, uint32_t* cand_cnt) {
+// Exact per-tensor top-k by (|c| desc, index asc) in three levels:
+//   1. compensate: histogram of the top kBinBits of |c|; threshold: the bin
+//      b1 holding the k-th largest and need1, the count still to take from it
+//   2. collect: |c| above b1 -> list; in b1 -> candidates + histogram of the
+//      next kDigitBits; threshold: digit d2 and need2; filter2: candidates
+//      above d2 -> list, at d2 -> second-level candidates
+//   3. final: exact radix select among the second-level candidates over (the
+//      remaining key bits, ~index) — a handful of elements on real gradients.
+// Appends reserve list slots once per CTA per tile (block scan + one atomic).
+
+template <typename T>
+constexpr int kShift2 = KeyOf<T>::kBits - kBinBits - kDigitBits;  // level-2 digit position
+
+template <typename T>
+__device__ __forceinline__ uint32_t digit2_of(typename KeyOf<T>::K key) {
+  return static_cast<uint32_t>(key >> kShift2<T>) & (kDigits - 1);
+}
+
+// Block-wide: the bin where the count of elements in bins >= it first
+// reaches need (thread j owns BINS/kThreads bins, highest first).  The
+// crossing thread writes *s_bin / *s_need; ends with a barrier.
+template <int BINS>
+__device__ __forceinline__ void crossing(const uint32_t* h, uint32_t need, uint32_t* s_bin,
+                                         uint32_t* s_need) {
   using Scan = cub::BlockScan<uint32_t, kThreads>;
   __shared__ typename Scan::TempStorage tmp;
-  constexpr int kPer = kBins / kThreads;
-  const uint32_t t = blockIdx.x;
-  uint32_t* h = hist + static_cast<uint64_t>(t) * kBins;
-  // thread j owns bins [kBins - kPer*(j+1), kBins - kPer*j): highest first
-  const int hi = kBins - kPer * threadIdx.x;
+  constexpr int kPer = BINS / kThreads;
+  const int hi = BINS - kPer * threadIdx.x;
   uint32_t mine = 0;
   for (int b = hi - 1; b >= hi - kPer; --b) mine += h[b];
   uint32_t above = 0;
   Scan(tmp).ExclusiveSum(mine, above);
-  const uint32_t kt = k[t];
-  if (above < kt && kt <= above + mine) {
+  if (above < need && need <= above + mine) {
     uint32_t acc = above;
     for (int b = hi - 1; b >= hi - kPer; --b) {
-      if (acc + h[b] >= kt) {
-        thr[t] = static_cast<uint32_t>(b);
-        need[t] = kt - acc;
+      if (acc + h[b] >= need) {
+        *s_bin = static_cast<uint32_t>(b);
+        *s_need = need - acc;
         break;
       }
       acc += h[b];
     }
   }
   __syncthreads();
-  for (int b = hi - 1; b >= hi - kPer; --b) h[b] = 0;
-  if (threadIdx.x == 0) {
-    sel_cnt[t] = 0;
-    cand_cnt[t] = 0;
-  }
 }
 
-template <typename T>
+// One CTA per tensor (levels 1 and 2): bin / need from the tensor's
+// histogram, which is cleared for the next step; resets two counters.
+template <int BINS>
 __global__ void __launch_bounds__(kThreads)
-    topk_collect_kernel(T* __restrict__ r, T* __restrict__ kept, const Chunk* __restrict__ chunks,
-                        uint32_t nchunks, const uint32_t* __restrict__ thr,
-                        const uint64_t* __restrict__ t_begin, const uint64_t* __restrict__ list_off,
-                        uint32_t* sel_cnt, uint32_t* __restrict__ list_idx,
-                        T* __restrict__ list_val, uint32_t* cand_cnt,
-                        typename KeyOf<T>::K* __restrict__ cand_key,
-                        uint32_t* __restrict__ cand_idx) {
-  for (uint32_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
-    const Chunk ch = chunks[ci];
-    const uint32_t t = ch.tensor;
-    const uint32_t tb = thr[t];
-    const uint64_t lo = list_off[t], cb = t_begin[t];
-    for (uint64_t base = ch.begin; base < ch.end; base += kThreads * kUnroll) {
-      T cv[kUnroll];
-#pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
-        const uint64_t i = base + q * kThreads + threadIdx.x;
-        cv[q] = i < ch.end ? r[i] : T(0);
-      }
-#pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
-        const uint64_t i = base + q * kThreads + threadIdx.x;
-        const bool valid = i < ch.end;
-        const uint32_t b = bin_of(cv[q]);
-        const bool take = valid && b > tb;
-        const bool cand = valid && b == tb;
-        const uint32_t ps = append_slot(take, sel_cnt + t);
-        if (take) {
-          list_idx[lo + ps] = static_cast<uint32_t>(i);
-          list_val[lo + ps] = cv[q];
-          if (kept) kept[i] = cv[q];
-          r[i] = sub_rn(cv[q], cv[q]);
-        }
-        const uint32_t pc = append_slot(cand, cand_cnt + t);
-        if (cand) {
-          cand_key[cb + pc] = KeyOf<T>::key(cv[q]);
-          cand_idx[cb + pc] = static_cast<uint32_t>(i);
-        }
-      }
-    }
+    topk_threshold_kernel(uint32_t* hist, const uint32_t* need_in, uint32_t* bin_out,
+                          uint32_t* need_out, uint32_t* reset0, uint32_t* reset1) {
+  __shared__ uint32_t s_bin, s_need;
+  const uint32_t t = blockIdx.x;
+  uint32_t* h = hist + static_cast<uint64_t>(t) * BINS;
+  crossing<BINS>(h, need_in[t], &s_bin, &s_need);
+  if (threadIdx.x == 0) {
+    bin_out[t] = s_bin;
+    need_out[t] = s_need;
+    if (reset0) reset0[t] = 0;
+    if (reset1) reset1[t] = 0;
   }
+  for (int b = threadIdx.x; b < BINS; b += kThreads) h[b] = 0;
 }
 
-// Finds the digit d of the current pass where the count of candidates with a
-// digit >= d first reaches need; need -= count above d.  Returns d.
-__device__ uint32_t pick_digit(uint32_t* hist, uint32_t& need, uint32_t* s_digit,
-                               uint32_t* s_need) {
+// Block-wide slot reservation in two lists: thread counts na, nb (< 2^16
+// per block); returns the thread's first slot in each.  One atomic per list.
+__device__ __forceinline__ void block_reserve(uint32_t na, uint32_t nb, uint32_t* ca,
+                                              uint32_t* cb, uint32_t& sa, uint32_t& sb) {
   using Scan = cub::BlockScan<uint32_t, kThreads>;
   __shared__ typename Scan::TempStorage tmp;
-  constexpr int kPer = kDigits / kThreads;
-  const int hi = kDigits - kPer * threadIdx.x;
-  uint32_t mine = 0;
-  for (int b = hi - 1; b >= hi - kPer; --b) mine += hist[b];
-  uint32_t above = 0;
-  Scan(tmp).ExclusiveSum(mine, above);
-  if (above < need && need <= above + mine) {
-    uint32_t acc = above;
-    for (int b = hi - 1; b >= hi - kPer; --b) {
-      if (acc + hist[b] >= need) {
-        *s_digit = static_cast<uint32_t>(b);
-        *s_need = need - acc;
-        break;
-      }
-      acc += hist[b];
-    }
+  __shared__ uint32_t s_base[2];
+  uint32_t pre = 0, tot = 0;
+  Scan(tmp).ExclusiveSum(na | (nb << 16), pre, tot);
+  if (threadIdx.x == 0) {
+    s_base[0] = (tot & 0xffffu) ? atomicAdd(ca, tot & 0xffffu) : 0u;
+    s_base[1] = (tot >> 16) ? atomicAdd(cb, tot >> 16) : 0u;
   }
   __syncthreads();
-  need = *s_need;
-  return *s_digit;
+  sa = s_base[0] + (pre & 0xffffu);
+  sb = s_base[1] + (pre >> 16);
+  __syncthreads();
 }
 
-// One CTA per tensor: the `need` best candidates by composite (low key bits
-// desc, index asc) — an exact radix select over (key low bits, ~index).
+// Per-warp staging of (index, payload) pairs appended by ballot, written to
+// a global list 32 at a time with one atomic per 32 entries: no block
+// barriers on the streaming path, and no contention on the list counters.
+template <typename V, uint32_t RING = 64>
+struct WarpStage {
+  uint32_t* idx;  // shared ring of RING entries
+  V* val;
+  uint32_t n = 0, done = 0;  // appended / written, warp-uniform
+
+  __device__ __forceinline__ void push(bool p, uint32_t i, V v) {
+    const unsigned m = __ballot_sync(0xffffffffu, p);
+    if (p) {
+      const uint32_t s = (n + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))) & (RING - 1);
+      idx[s] = i;
+      val[s] = v;
+    }
+    n += __popc(m);
+    __syncwarp();
+  }
+  __device__ __forceinline__ void put(uint32_t slot, uint32_t i, V v) {
+    idx[slot & (RING - 1)] = i;
+    val[slot & (RING - 1)] = v;
+  }
+  // Writes full groups of 32 (all = true: everything pending).
+  __device__ __forceinline__ void flush(uint32_t* counter, uint32_t* gidx, V* gval, uint64_t off,
+                                        bool all) {
+    const uint32_t lane = threadIdx.x & 31;
+    while (n - done >= 32 || (all && n > done)) {
+      const uint32_t c = n - done < 32 ? n - done : 32;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(counter, c);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (lane < c) {
+        const uint32_t s = (done + lane) & (RING - 1);
+        gidx[off + base + lane] = idx[s];
+        gval[off + base + lane] = val[s];
+      }
+      done += c;
+      __syncwarp();
+    }
+  }
+};
+
+constexpr int kWarps = kThreads / 32;
+// collect: elements per lane per warp iteration (1 KB of c per warp; 2 KB
+// measured slower on VGG-16: 259 -> 387 us, register-limited occupancy)
 template <typename T>
-__global__ void __launch_bounds__(kThreads)
-    topk_resolve_kernel(T* __restrict__ r, T* __restrict__ kept,
-                        const uint64_t* __restrict__ t_begin, const uint64_t* __restrict__ list_off,
-                        const uint32_t* __restrict__ sel_cnt, const uint32_t* __restrict__ need_in,
-                        const uint32_t* __restrict__ cand_cnt,
-                        const typename KeyOf<T>::K* __restrict__ cand_key,
-                        const uint32_t* __restrict__ cand_idx, uint32_t* __restrict__ list_idx,
-                        T* __restrict__ list_val) {
+constexpr int kCollectUnroll = 32 / static_cast<int>(sizeof(T));
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
   using K = typename KeyOf<T>::K;
-  constexpr int kLow = KeyOf<T>::kBits - kBinBits;  // key bits below the bin
+  constexpr int kU = kCollectUnroll<T>;
+  constexpr int kG = 32 / static_cast<int>(sizeof(T));  // staged per lane per group
+  constexpr uint32_t kRing = 32 * kG;  // one group always fits after a flush
+  __shared__ uint32_t hist2[kDigits];
+  __shared__ uint32_t s_ti[kWarps][kRing], s_ci[kWarps][kRing];
+  __shared__ T s_tv[kWarps][kRing];
+  __shared__ K s_ck[kWarps][kRing];
+  T* __restrict__ r = static_cast<T*>(A.r);
+  T* __restrict__ kept = static_cast<T*>(A.kept);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpStage<T, kRing> take{s_ti[warp], s_tv[warp]};
+  WarpStage<K, kRing> cand{s_ci[warp], s_ck[warp]};
+  for (int b = threadIdx.x; b < kDigits; b += kThreads) hist2[b] = 0;
+  __syncthreads();
+  uint32_t cur = kNone;
+  auto flush_hist = [&]() {
+    __syncthreads();
+    uint32_t* dst = A.hist2 + static_cast<uint64_t>(cur) * kDigits;
+    for (int b = threadIdx.x; b < kDigits; b += kThreads) {
+      const uint32_t v = hist2[b];
+      if (v) {
+        atomicAdd(dst + b, v);
+        hist2[b] = 0;
+      }
+    }
+    __syncthreads();
+  };
+  constexpr uint32_t kSpan = 32 * kU;  // elements per warp iteration
+  for (uint32_t ci = blockIdx.x; ci < A.nchunks; ci += gridDim.x) {
+    const Chunk ch = A.chunks[ci];
+    const uint32_t t = ch.tensor;
+    if (t != cur) {
+      if (cur != kNone) flush_hist();
+      cur = t;
+    }
+    const uint32_t b1 = A.thr[t];
+    const uint64_t lo = A.list_off[t], cb = A.t_begin[t];
+    // 32-bit flat indices (the state checks N < 2^32).  Body chunks are
+    // 16-byte aligned (covap_feedback_create cuts every tensor's unaligned
+    // head and tail into chunks of their own, flagged scalar), so a lane loads
+    // kU / W vectors: element q of the lane is vector (q / W), lane (q % W).
+    constexpr int W = 16 / static_cast<int>(sizeof(T));
+    const bool vec = ch.pad == 0;
+    const uint32_t cbeg = static_cast<uint32_t>(ch.begin), cend = static_cast<uint32_t>(ch.end);
+    const uint32_t span = vec ? kSpan : 32u;  // scalar chunks: one element per lane
+    for (uint32_t base = cbeg + warp * span; base < cend; base += kWarps * span) {
+      T cv[kU];
+      uint32_t ix[kU];
+      uint32_t valid = 0;
+      if (vec) {
+        using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+#pragma unroll
+        for (int j = 0; j < kU / W; ++j) {
+          const uint32_t e0 = base + (j * 32 + lane) * W;
+          V x;
+          if (e0 < cend) {
+            x = *reinterpret_cast<const V*>(r + e0);
+            valid |= ((1u << W) - 1u) << (j * W);
+          } else {
+            x = V{};
+          }
+          const T* xs = reinterpret_cast<const T*>(&x);
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            cv[j * W + w] = xs[w];
+            ix[j * W + w] = e0 + w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+          ix[q] = base + lane;
+          cv[q] = T(0);
+        }
+        if (base + lane < cend) {
+          cv[0] = r[base + lane];
+          valid = 1u;
+        }
+      }
+      uint32_t mt = 0, mc = 0;
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        if (!((valid >> q) & 1u)) continue;
+        const uint32_t b = bin_of(cv[q]);
+        if (b > b1) {
+          mt |= 1u << q;
+          if (kept) kept[ix[q]] = cv[q];
+          r[ix[q]] = sub_rn(cv[q], cv[q]);
+        } else if (b == b1) {
+          mc |= 1u << q;
+          atomicAdd(&hist2[digit2_of<T>(KeyOf<T>::key(cv[q]))], 1u);
+        }
+      }
+      if (!__any_sync(0xffffffffu, mt | mc)) continue;
+      // Stage in groups of kG elements per lane (kG * 32 <= kRing): a warp
+      // scan of the per-lane counts (takes low 16 bits, candidates high).
+#pragma unroll
+      for (int g0 = 0; g0 < kU; g0 += kG) {
+        const uint32_t gt = (mt >> g0) & ((1u << kG) - 1u), gc = (mc >> g0) & ((1u << kG) - 1u);
+        const uint32_t mine = __popc(gt) | (__popc(gc) << 16);
+        uint32_t inc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+        if (tot == 0) continue;
+        const uint32_t ex = inc - mine, nt = tot & 0xffffu, nc = tot >> 16;
+        if (take.n - take.done + nt > kRing)
+          take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, true);
+        if (cand.n - cand.done + nc > kRing)
+          cand.flush(A.cand_cnt + t, A.cand_idx, static_cast<K*>(A.cand_key), cb, true);
+        uint32_t st = take.n + (ex & 0xffffu), sc = cand.n + (ex >> 16);
+        if (gt | gc) {
+#pragma unroll
+          for (int q = 0; q < kG; ++q) {
+            if ((gt >> q) & 1u) take.put(st++, ix[g0 + q], cv[g0 + q]);
+            if ((gc >> q) & 1u) cand.put(sc++, ix[g0 + q], KeyOf<T>::key(cv[g0 + q]));
+          }
+        }
+        take.n += nt;
+        cand.n += nc;
+        __syncwarp();
+        take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, false);
+        cand.flush(A.cand_cnt + t, A.cand_idx, static_cast<K*>(A.cand_key), cb, false);
+      }
+    }
+    take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, true);
+    cand.flush(A.cand_cnt + t, A.cand_idx, static_cast<K*>(A.cand_key), cb, true);
+  }
+  if (cur != kNone) flush_hist();
+}
+
+// Level-1 candidates above d2 are taken, those at d2 go on to the final
+// selection.  Every warp strides over every tensor's candidates, so the work
+// is balanced however unevenly the candidates fall.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) topk_filter2_kernel(TopkArgs A) {
+  using K = typename KeyOf<T>::K;
+  __shared__ uint32_t s_ti[kWarps][64], s_ci[kWarps][64];
+  __shared__ T s_tv[kWarps][64];
+  __shared__ K s_ck[kWarps][64];
+  T* __restrict__ r = static_cast<T*>(A.r);
+  T* __restrict__ kept = static_cast<T*>(A.kept);
+  const K* __restrict__ ck = static_cast<const K*>(A.cand_key);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpStage<T> take{s_ti[warp], s_tv[warp]};
+  WarpStage<K> next{s_ci[warp], s_ck[warp]};
+  const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  for (uint32_t t = 0; t < A.ntensors; ++t) {
+    const uint32_t m = A.cand_cnt[t], d2 = A.thr2[t];
+    const uint64_t lo = A.list_off[t], cb = A.t_begin[t];
+    for (uint32_t e0 = gw * 32; e0 < m; e0 += nw * 32) {
+      const uint32_t e = e0 + lane;
+      bool tk = false, nx = false;
+      K key = 0;
+      uint32_t i = 0;
+      T c = T(0);
+      if (e < m) {
+        key = ck[cb + e];
+        i = A.cand_idx[cb + e];
+        const uint32_t d = digit2_of<T>(key);
+        tk = d > d2;
+        nx = d == d2;
+        if (tk) {
+          c = r[i];
+          if (kept) kept[i] = c;
+          r[i] = sub_rn(c, c);
+        }
+      }
+      take.push(tk, i, c);
+      next.push(nx, i, key);
+      take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, false);
+      next.flush(A.cand2_cnt + t, A.cand2_idx, static_cast<K*>(A.cand2_key), cb, false);
+    }
+    take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, true);
+    next.flush(A.cand2_cnt + t, A.cand2_idx, static_cast<K*>(A.cand2_key), cb, true);
+  }
+}
+
+// One CTA per tensor: the need2 best second-level candidates by composite
+// (remaining key bits desc, index asc) — an exact radix select over
+// (key low bits, ~index), then their emission.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) topk_final_kernel(TopkArgs A) {
+  using K = typename KeyOf<T>::K;
+  constexpr int kLow = kShift2<T>;  // key bits below the level-2 digit
   __shared__ uint32_t hist[kDigits];
   __shared__ uint32_t s_digit, s_need, s_count;
+  T* __restrict__ r = static_cast<T*>(A.r);
+  T* __restrict__ kept = static_cast<T*>(A.kept);
+  T* __restrict__ list_val = static_cast<T*>(A.list_val);
+  uint32_t* __restrict__ list_idx = A.list_idx;
   const uint32_t t = blockIdx.x;
-  uint32_t need = need_in[t];
-  const uint32_t m = cand_cnt[t];
+  const uint32_t need0 = A.need2[t];
+  uint32_t need = need0;
+  const uint32_t m = A.cand2_cnt[t];
   if (need == 0) return;
-  const uint64_t cb = t_begin[t];
-  const K* ck = cand_key + cb;
-  const uint32_t* cx = cand_idx + cb;
+  const uint64_t cb = A.t_begin[t];
+  const K* ck = static_cast<const K*>(A.cand2_key) + cb;
+  const uint32_t* cx = A.cand2_idx + cb;
   const K lowmask = (K(1) << kLow) - 1;
   uint64_t pa = 0;  // fixed prefix of the low key bits
   uint32_t pb = 0;  // fixed prefix of ~index
@@ -411,7 +637,9 @@ __global__ void __launch_bounds__(kThreads)
           if (match) atomicAdd(&hist[digit], 1u);
         }
         __syncthreads();
-        const uint32_t d = pick_digit(hist, need, &s_digit, &s_need);
+        crossing<kDigits>(hist, need, &s_digit, &s_need);
+        const uint32_t d = s_digit;
+        need = s_need;
         if (field == 0)
           pa = (pa << nb) | d;
         else
@@ -423,8 +651,8 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (threadIdx.x == 0) s_count = 0;
   __syncthreads();
-  const uint64_t base = list_off[t] + sel_cnt[t];
-  const bool all = need_in[t] >= m;
+  const uint64_t base = A.list_off[t] + A.sel_cnt[t];
+  const bool all = need0 >= m;
   // warp-uniform trip count so append_slot's ballot sees every lane
   for (uint32_t e0 = 0; e0 < m; e0 += kThreads) {
     const uint32_t e = e0 + threadIdx.x;
@@ -554,6 +782,7 @@ __global__ void randomk_gather_kernel(RandomkArgs A, T* __restrict__ r, T* __res
     list_val[e] = c;
     if (kept) kept[flat] = c;
     r[flat] = sub_rn(c, c);
+    A.head[A.t_begin[t] + j] = kNone;  // the chain kernel is done with the lists
   }
 }
 
@@ -567,15 +796,44 @@ __global__ void randomk_clear_kernel(RandomkArgs A) {
 
 // ------------------------------------------------------------ exchange
 
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store8(double* p, const double (&v)[8]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) reinterpret_cast<double2*>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
+}
+
 template <typename T>
 __global__ void fp16_mean_kernel(const uint16_t* __restrict__ recv, int P, uint64_t n, T inv,
                                  T* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    T acc = T(0);
+  // 8 halves (16 B) per thread per rank when the rows stay 16-byte aligned
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nvec = (n % 8 == 0) ? n / 8 : 0;
+  for (uint64_t v = tid; v < nvec; v += stride) {
+    T acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = T(0);
+    for (int p = 0; p < P; ++p) {
+      const uint4 w = reinterpret_cast<const uint4*>(recv + static_cast<uint64_t>(p) * n)[v];
+      const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint16_t h = static_cast<uint16_t>(u[q >> 1] >> (16 * (q & 1)));
+        acc[q] = add_rn(acc[q], static_cast<T>(half_to_float(h)));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = mul_rn(acc[q], inv);
+    store8(out + v * 8, acc);
+  }
+  for (uint64_t i = nvec * 8 + tid; i < n; i += stride) {
+    T a = T(0);
     for (int p = 0; p < P; ++p)
-      acc = add_rn(acc, static_cast<T>(half_to_float(recv[static_cast<uint64_t>(p) * n + i])));
-    out[i] = mul_rn(acc, inv);
+      a = add_rn(a, static_cast<T>(half_to_float(recv[static_cast<uint64_t>(p) * n + i])));
+    out[i] = mul_rn(a, inv);
   }
 }
 
@@ -759,52 +1017,23 @@ cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uin
   return cudaGetLastError();
 }
 
-cudaError_t launch_topk_threshold(uint32_t* hist, const uint32_t* k, uint32_t* thr,
-                                  uint32_t* need, uint32_t* sel_cnt, uint32_t* cand_cnt,
-                                  uint32_t ntensors, cudaStream_t s) {
-  if (ntensors == 0) return cudaSuccess;
-  topk_threshold_kernel<<<ntensors, kThreads, 0, s>>>(hist, k, thr, need, sel_cnt, cand_cnt);
+template <typename T>
+cudaError_t launch_topk_t(const TopkArgs& a, int sms, cudaStream_t s) {
+  if (a.ntensors == 0) return cudaSuccess;
+  const int grid = static_cast<int>(a.nchunks < static_cast<uint32_t>(sms * 4) ? a.nchunks
+                                                                             : sms * 4);
+  topk_threshold_kernel<kBins><<<a.ntensors, kThreads, 0, s>>>(a.hist1, a.k, a.thr, a.need,
+                                                               a.sel_cnt, a.cand_cnt);
+  if (grid > 0) topk_collect_kernel<T><<<grid, kThreads, 0, s>>>(a);
+  topk_threshold_kernel<kDigits><<<a.ntensors, kThreads, 0, s>>>(a.hist2, a.need, a.thr2, a.need2,
+                                                                 a.cand2_cnt, nullptr);
+  topk_filter2_kernel<T><<<sms * 2, kThreads, 0, s>>>(a);
+  topk_final_kernel<T><<<a.ntensors, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_topk_collect(int dtype, void* r, void* kept, const Chunk* chunks,
-                                uint32_t nchunks, const uint32_t* thr, const uint64_t* t_begin,
-                                const uint64_t* list_off, uint32_t* sel_cnt, uint32_t* list_idx,
-                                void* list_val, uint32_t* cand_cnt, void* cand_key,
-                                uint32_t* cand_idx, int sms, cudaStream_t s) {
-  const int grid = static_cast<int>(nchunks < static_cast<uint32_t>(sms * 4) ? nchunks : sms * 4);
-  if (grid == 0) return cudaSuccess;
-  if (dtype == 1)
-    topk_collect_kernel<double><<<grid, kThreads, 0, s>>>(
-        static_cast<double*>(r), static_cast<double*>(kept), chunks, nchunks, thr, t_begin,
-        list_off, sel_cnt, list_idx, static_cast<double*>(list_val), cand_cnt,
-        static_cast<uint64_t*>(cand_key), cand_idx);
-  else
-    topk_collect_kernel<float><<<grid, kThreads, 0, s>>>(
-        static_cast<float*>(r), static_cast<float*>(kept), chunks, nchunks, thr, t_begin,
-        list_off, sel_cnt, list_idx, static_cast<float*>(list_val), cand_cnt,
-        static_cast<uint32_t*>(cand_key), cand_idx);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_topk_resolve(int dtype, void* r, void* kept, const uint64_t* t_begin,
-                                const uint64_t* list_off, const uint32_t* sel_cnt,
-                                const uint32_t* need, const uint32_t* cand_cnt,
-                                const void* cand_key, const uint32_t* cand_idx,
-                                uint32_t* list_idx, void* list_val, uint32_t ntensors,
-                                cudaStream_t s) {
-  if (ntensors == 0) return cudaSuccess;
-  if (dtype == 1)
-    topk_resolve_kernel<double><<<ntensors, kThreads, 0, s>>>(
-        static_cast<double*>(r), static_cast<double*>(kept), t_begin, list_off, sel_cnt, need,
-        cand_cnt, static_cast<const uint64_t*>(cand_key), cand_idx, list_idx,
-        static_cast<double*>(list_val));
-  else
-    topk_resolve_kernel<float><<<ntensors, kThreads, 0, s>>>(
-        static_cast<float*>(r), static_cast<float*>(kept), t_begin, list_off, sel_cnt, need,
-        cand_cnt, static_cast<const uint32_t*>(cand_key), cand_idx, list_idx,
-        static_cast<float*>(list_val));
-  return cudaGetLastError();
+cudaError_t launch_topk(int dtype, const TopkArgs& a, int sms, cudaStream_t s) {
+  return dtype == 1 ? launch_topk_t<double>(a, sms, s) : launch_topk_t<float>(a, sms, s);
 }
 
 cudaError_t launch_randomk_select(const RandomkArgs& a, int sms, cudaStream_t s) {
@@ -829,7 +1058,6 @@ cudaError_t launch_randomk_gather(int dtype, const RandomkArgs& a, void* r, void
     randomk_gather_kernel<float><<<grid, kThreads, 0, s>>>(
         a, static_cast<float*>(r), static_cast<float*>(kept), list_idx,
         static_cast<float*>(list_val));
-  randomk_clear_kernel<<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -57,25 +57,39 @@ cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uin
                               const Chunk* chunks, uint32_t nchunks, int ef, double coeff,
                               int sms, cudaStream_t s);
 
-// Top-k.  thr[t] = threshold bin, need[t] = elements still to take from it;
-// clears hist and the counters.
-cudaError_t launch_topk_threshold(uint32_t* hist, const uint32_t* k, uint32_t* thr,
-                                  uint32_t* need, uint32_t* sel_cnt, uint32_t* cand_cnt,
-                                  uint32_t ntensors, cudaStream_t s);
-// Elements above the threshold bin go to the list (and kept, r = c - c);
-// elements in it become candidates (cand_* at the tensor's own offset).
-cudaError_t launch_topk_collect(int dtype, void* r, void* kept, const Chunk* chunks,
-                                uint32_t nchunks, const uint32_t* thr, const uint64_t* t_begin,
-                                const uint64_t* list_off, uint32_t* sel_cnt, uint32_t* list_idx,
-                                void* list_val, uint32_t* cand_cnt, void* cand_key,
-                                uint32_t* cand_idx, int sms, cudaStream_t s);
-// Exact selection among the candidates by (|c| desc, index asc).
-cudaError_t launch_topk_resolve(int dtype, void* r, void* kept, const uint64_t* t_begin,
-                                const uint64_t* list_off, const uint32_t* sel_cnt,
-                                const uint32_t* need, const uint32_t* cand_cnt,
-                                const void* cand_key, const uint32_t* cand_idx,
-                                uint32_t* list_idx, void* list_val, uint32_t ntensors,
-                                cudaStream_t s);
+// Top-k after the compensation pass filled hist1: the k[t] largest |c| of
+// every tensor (ties to the lower index) go to list_idx / list_val at
+// list_off[t] (and kept, r = c - c).  Three levels: 4096-bin histogram,
+// 2048-bin histogram of the threshold bin's candidates, exact radix select
+// among the survivors.  Candidate arrays are indexed at the tensor's begin.
+constexpr int kDigitBits = 11;
+constexpr int kDigits = 1 << kDigitBits;
+struct TopkArgs {
+  void* r;
+  void* kept;
+  const Chunk* chunks;
+  uint32_t nchunks;
+  uint32_t ntensors;
+  const uint64_t* t_begin;
+  const uint64_t* list_off;
+  const uint32_t* k;
+  uint32_t* hist1;  // ntensors x kBins, zero between steps
+  uint32_t* hist2;  // ntensors x kDigits, zero between steps
+  uint32_t* thr;
+  uint32_t* need;
+  uint32_t* thr2;
+  uint32_t* need2;
+  uint32_t* sel_cnt;
+  uint32_t* cand_cnt;
+  uint32_t* cand2_cnt;
+  void* cand_key;
+  uint32_t* cand_idx;
+  void* cand2_key;
+  uint32_t* cand2_idx;
+  uint32_t* list_idx;
+  void* list_val;
+};
+cudaError_t launch_topk(int dtype, const TopkArgs& a, int sms, cudaStream_t s);
 
 // Random-k: sample_without_replacement reproduced in parallel.  Entry e of
 // the list belongs to tensor tensor_of[e], draw i = e - list_off[t].

@@ -53,11 +53,19 @@ struct covap_feedback {
   uint32_t* cand_cnt = nullptr;
   void* cand_key = nullptr;
   uint32_t* cand_idx = nullptr;
+  uint32_t* hist2 = nullptr;
+  uint32_t* thr2 = nullptr;
+  uint32_t* need2 = nullptr;
+  uint32_t* cand2_cnt = nullptr;
+  void* cand2_key = nullptr;
+  uint32_t* cand2_idx = nullptr;
   void* acc = nullptr;  // rank-ordered scatter accumulator, zero between steps
   // random-k
   uint32_t* tensor_of = nullptr;
   uint32_t *j = nullptr, *nxt = nullptr, *prv = nullptr, *src = nullptr, *head = nullptr;
   int* reject = nullptr;
+  cudaStream_t side = nullptr;  // index sampling, concurrent with the compensation pass
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // wire
   uint32_t* list_idx = nullptr;
   void* list_val = nullptr;
@@ -84,6 +92,9 @@ void release(covap_feedback* f) {
   DeviceGuard dg(f->device);
   cudaDeviceSynchronize();
   for (void* p : f->owned) cudaFree(p);
+  if (f->ev_fork) cudaEventDestroy(f->ev_fork);
+  if (f->ev_join) cudaEventDestroy(f->ev_join);
+  if (f->side) cudaStreamDestroy(f->side);
   if (f->recv_a) cudaFree(f->recv_a);
   if (f->recv_b) cudaFree(f->recv_b);
   delete f;
@@ -154,23 +165,47 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       CK(fb::launch_dense(dt, f->filter.kind, a, f->sms, st));
       break;
     }
-    case COVAP_FILTER_TOPK:
+    case COVAP_FILTER_TOPK: {
       CK(fb::launch_compensate(dt, grad, f->residual, zero, f->hist, f->chunks, f->nchunks,
                                f->ef.enabled, coeff, f->sms, st));
-      CK(fb::launch_topk_threshold(f->hist, f->d_k, f->thr, f->need, f->sel_cnt, f->cand_cnt, nt,
-                                   st));
-      CK(fb::launch_topk_collect(dt, f->residual, kept, f->chunks, f->nchunks, f->thr, f->d_begin,
-                                 f->d_list_off, f->sel_cnt, f->list_idx, f->list_val, f->cand_cnt,
-                                 f->cand_key, f->cand_idx, f->sms, st));
-      CK(fb::launch_topk_resolve(dt, f->residual, kept, f->d_begin, f->d_list_off, f->sel_cnt,
-                                 f->need, f->cand_cnt, f->cand_key, f->cand_idx, f->list_idx,
-                                 f->list_val, nt, st));
+      fb::TopkArgs a{};
+      a.r = f->residual;
+      a.kept = kept;
+      a.chunks = f->chunks;
+      a.nchunks = f->nchunks;
+      a.ntensors = nt;
+      a.t_begin = f->d_begin;
+      a.list_off = f->d_list_off;
+      a.k = f->d_k;
+      a.hist1 = f->hist;
+      a.hist2 = f->hist2;
+      a.thr = f->thr;
+      a.need = f->need;
+      a.thr2 = f->thr2;
+      a.need2 = f->need2;
+      a.sel_cnt = f->sel_cnt;
+      a.cand_cnt = f->cand_cnt;
+      a.cand2_cnt = f->cand2_cnt;
+      a.cand_key = f->cand_key;
+      a.cand_idx = f->cand_idx;
+      a.cand2_key = f->cand2_key;
+      a.cand2_idx = f->cand2_idx;
+      a.list_idx = f->list_idx;
+      a.list_val = f->list_val;
+      CK(fb::launch_topk(dt, a, f->sms, st));
       break;
+    }
     case COVAP_FILTER_RANDOMK: {
+      // The sampled indices depend only on (seed, step, t): they are drawn on
+      // a side stream while the compensation pass streams the gradient.
+      const fb::RandomkArgs a = randomk_args(f);
+      CK(cudaEventRecord(f->ev_fork, st));
+      CK(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
+      CK(fb::launch_randomk_select(a, f->sms, f->side));
+      CK(cudaEventRecord(f->ev_join, f->side));
       CK(fb::launch_compensate(dt, grad, f->residual, zero, nullptr, f->chunks, f->nchunks,
                                f->ef.enabled, coeff, f->sms, st));
-      const fb::RandomkArgs a = randomk_args(f);
-      CK(fb::launch_randomk_select(a, f->sms, st));
+      CK(cudaStreamWaitEvent(st, f->ev_join, 0));
       CK(fb::launch_randomk_gather(dt, a, f->residual, kept, f->list_idx, f->list_val, f->sms,
                                    st));
       break;
@@ -294,11 +329,19 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
     }
     DeviceGuard dg(device);
     CK(cudaDeviceGetAttribute(&f->sms, cudaDevAttrMultiProcessorCount, device));
+    // Chunks never straddle tensors; a tensor's 16-byte-unaligned head and
+    // tail get chunks of their own flagged scalar (pad = 1), so every other
+    // chunk can be streamed with 16-byte vectors.
     std::vector<fb::Chunk> ch;
-    for (size_t t = 0; t < n_tensors; ++t)
-      for (uint64_t b = f->begin[t]; b < f->begin[t] + f->numel[t]; b += fb::kChunk)
-        ch.push_back({b, std::min(b + fb::kChunk, f->begin[t] + f->numel[t]),
-                      static_cast<uint32_t>(t), 0});
+    const uint64_t W = 16 / f->esize;
+    for (size_t t = 0; t < n_tensors; ++t) {
+      const uint64_t b = f->begin[t], e = b + f->numel[t];
+      const uint64_t ab = std::min(e, (b + W - 1) / W * W), ae = std::max(ab, e / W * W);
+      const auto tt = static_cast<uint32_t>(t);
+      if (ab > b) ch.push_back({b, ab, tt, 1});
+      for (uint64_t x = ab; x < ae; x += fb::kChunk) ch.push_back({x, std::min(x + fb::kChunk, ae), tt, 0});
+      if (e > ae) ch.push_back({ae, e, tt, 1});
+    }
     f->nchunks = static_cast<uint32_t>(ch.size());
     f->residual = dalloc<void>(f, f->total * f->esize);
     CK(cudaMemset(f->residual, 0, std::max<uint64_t>(f->total, 1) * f->esize));
@@ -330,6 +373,13 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
       f->cand_cnt = dalloc<uint32_t>(f, n_tensors * 4);
       f->cand_key = dalloc<void>(f, f->total * f->esize);
       f->cand_idx = dalloc<uint32_t>(f, f->total * 4);
+      f->hist2 = dalloc<uint32_t>(f, n_tensors * fb::kDigits * 4);
+      CK(cudaMemset(f->hist2, 0, n_tensors * fb::kDigits * 4));
+      f->thr2 = dalloc<uint32_t>(f, n_tensors * 4);
+      f->need2 = dalloc<uint32_t>(f, n_tensors * 4);
+      f->cand2_cnt = dalloc<uint32_t>(f, n_tensors * 4);
+      f->cand2_key = dalloc<void>(f, f->total * f->esize);
+      f->cand2_idx = dalloc<uint32_t>(f, f->total * 4);
       f->acc = dalloc<void>(f, f->total * f->esize);
       CK(cudaMemset(f->acc, 0, std::max<uint64_t>(f->total, 1) * f->esize));
     }
@@ -348,6 +398,9 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
       CK(cudaMemset(f->head, 0xff, std::max<uint64_t>(f->total, 4) * 4));
       f->reject = dalloc<int>(f, n_tensors * 4);
       CK(cudaMemset(f->reject, 0, n_tensors * 4));
+      CK(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming));
     }
     CK(cudaDeviceSynchronize());
     *out = f;
