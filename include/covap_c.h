@@ -158,6 +158,9 @@ covap_status covap_state_set_step(covap_state* state, uint64_t num_steps);
  * (NCCL over the 1-rank communicator when one is given) -> K2 instead, the
  * exact multi-rank code path — used to test that path on one GPU. */
 covap_status covap_state_set_fused(covap_state* state, int fuse_single_rank);
+/* covap_sync_step_host's chunk schedule: chunks ramp geometrically from
+ * ramp_min_elems (>= 8192) up to the body chunk at both ends (default 1 Mi). */
+covap_status covap_state_set_host_ramp(covap_state* state, uint64_t ramp_min_elems);
 /* Zero the residual arena (stream-ordered). */
 covap_status covap_state_reset(covap_state* state, void* stream);
 

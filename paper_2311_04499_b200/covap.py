@@ -408,6 +408,10 @@ class CompressorState:
         """One rank: fused K1F pass (default) or the multi-rank K1 -> C1 -> K2 path."""
         L.lib().covap_state_set_fused(self._h, 1 if fuse_single_rank else 0)
 
+    def set_host_ramp(self, ramp_min_elems: int):
+        """Smallest chunk of sync_host's geometric ramp at both ends of the step."""
+        L.lib().covap_state_set_host_ramp(self._h, int(ramp_min_elems))
+
     def reset(self, stream=None):
         L.lib().covap_state_reset(self._h, _stream_ptr(stream, self.device))
 

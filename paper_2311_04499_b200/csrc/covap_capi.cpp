@@ -56,6 +56,7 @@ struct covap_state {
   std::vector<uint8_t> tl_mode;                 // per bucket: 0 fused, 1 covap, 2 dense
   std::vector<uint8_t> timed;                   // bucket had a collective in the last step
   bool fuse_single_rank = true;                 // P = 1: run K1F instead of K1 -> C1 -> K2
+  uint64_t ramp_min = 1u << 20;                 // host pipeline: smallest ramp chunk (elements)
 };
 
 namespace covapb {
@@ -443,6 +444,13 @@ covap_status covap_state_set_fused(covap_state* s, int fuse_single_rank) {
   });
 }
 
+covap_status covap_state_set_host_ramp(covap_state* s, uint64_t ramp_min_elems) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    s->ramp_min = std::max<uint64_t>(ramp_min_elems, 8192);
+  });
+}
+
 covap_status covap_state_reset(covap_state* s, void* stream) {
   return guarded([&] {
     need(s != nullptr, "NULL state");
@@ -612,8 +620,9 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
     const uint64_t n = s->plan.dtotal;
     const size_t es = s->esize;
     // Chunk boundaries (multiples of 8192 elements): C-sized chunks in the
-    // middle, ramping C/4, C/2 at both ends so the first H2D and the last
-    // D2H — the parts no other copy overlaps — are short.
+    // middle, ramping geometrically (C/2^k, ..., C/4, C/2, from ramp_min
+    // elements) at both ends so the first H2D and the last D2H — the parts
+    // no other copy overlaps — are short.
     // Default C = max(4 Mi, N / 32): measured best for ResNet-50 (4 Mi) and
     // BERT-large (~10 Mi) on B200 PCIe (profiles/r1_design_study.md).
     uint64_t chunk = std::max<uint64_t>(
@@ -621,15 +630,22 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
     chunk = (chunk + 8191) / 8192 * 8192;
     std::vector<uint64_t> cuts{0};
     if (n >= 3 * chunk) {
-      const uint64_t q = chunk / 4 / 8192 * 8192, h = chunk / 2 / 8192 * 8192;
-      cuts.push_back(q);
-      cuts.push_back(q + h);
-      const uint64_t mid_end = n - q - h;
-      const uint64_t m = (mid_end - (q + h) + chunk - 1) / chunk;
-      for (uint64_t i = 1; i < m; ++i)
-        cuts.push_back((q + h) + ((mid_end - (q + h)) * i / m) / 8192 * 8192);
-      cuts.push_back(mid_end);
-      cuts.push_back(n - q);
+      std::vector<uint64_t> ramp;  // C/2, C/4, ... down to ramp_min
+      for (uint64_t c = chunk / 2; c >= s->ramp_min && c >= 8192; c /= 2) ramp.push_back(c / 8192 * 8192);
+      if (ramp.empty()) ramp.push_back(chunk / 2 / 8192 * 8192);
+      uint64_t head = 0;
+      for (size_t i = ramp.size(); i-- > 0;) {
+        head += ramp[i];
+        cuts.push_back(head);
+      }
+      const uint64_t mid_end = n - head;
+      const uint64_t m = (mid_end - head + chunk - 1) / chunk;
+      for (uint64_t i = 1; i < m; ++i) cuts.push_back(head + ((mid_end - head) * i / m) / 8192 * 8192);
+      uint64_t tail = mid_end;
+      for (size_t i = 0; i < ramp.size(); ++i) {
+        cuts.push_back(tail);
+        tail += ramp[i];
+      }
     } else {
       for (uint64_t a = chunk; a < n; a += chunk) cuts.push_back(a);
     }

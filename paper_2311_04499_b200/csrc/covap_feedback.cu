@@ -405,22 +405,77 @@ constexpr int kWarps = kThreads / 32;
 template <typename T>
 constexpr int kCollectUnroll = 32 / static_cast<int>(sizeof(T));
 
+// Per-warp ring fed lane by lane: a lane with a hit claims a slot with a
+// shared-memory atomic (hits are ~1% of elements, so the common path is one
+// compare per element and no warp-wide scan); the warp drains full groups of
+// 32 to the global list at the end of each iteration.  A claim that finds the
+// ring full (only when most elements are hits) goes straight to the global
+// list with its own atomic.  List order is irrelevant downstream.
+template <typename V, uint32_t RING>
+struct LaneRing {
+  uint32_t* idx;       // shared, RING entries
+  V* val;
+  uint32_t* n;         // shared claim counter of this warp
+  uint32_t done = 0;   // drained (warp-uniform)
+
+  __device__ __forceinline__ void claim(uint32_t i, V v, uint32_t* gcnt, uint32_t* gidx, V* gval,
+                                        uint64_t off) {
+    const uint32_t slot = atomicAdd(n, 1u);
+    if (slot - done < RING) {
+      idx[slot & (RING - 1)] = i;
+      val[slot & (RING - 1)] = v;
+    } else {
+      const uint32_t g = atomicAdd(gcnt, 1u);
+      gidx[off + g] = i;
+      gval[off + g] = v;
+    }
+  }
+  // Warp-collective: drain groups of 32 (all: everything pending).
+  __device__ __forceinline__ void drain(uint32_t* gcnt, uint32_t* gidx, V* gval, uint64_t off,
+                                        bool all) {
+    const uint32_t lane = threadIdx.x & 31;
+    __syncwarp();
+    uint32_t m = *n;
+    if (m - done > RING) {  // overflowed claims were written directly
+      m = done + RING;
+      __syncwarp();
+      if (lane == 0) *n = m;
+    }
+    while (m - done >= 32 || (all && m > done)) {
+      const uint32_t c = m - done < 32 ? m - done : 32;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(gcnt, c);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (lane < c) {
+        const uint32_t s = (done + lane) & (RING - 1);
+        gidx[off + base + lane] = idx[s];
+        gval[off + base + lane] = val[s];
+      }
+      done += c;
+    }
+    __syncwarp();
+  }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
   using K = typename KeyOf<T>::K;
   constexpr int kU = kCollectUnroll<T>;
-  constexpr int kG = 32 / static_cast<int>(sizeof(T));  // staged per lane per group
-  constexpr uint32_t kRing = 32 * kG;  // one group always fits after a flush
+  constexpr uint32_t kRing = 128;
   __shared__ uint32_t hist2[kDigits];
   __shared__ uint32_t s_ti[kWarps][kRing], s_ci[kWarps][kRing];
   __shared__ T s_tv[kWarps][kRing];
   __shared__ K s_ck[kWarps][kRing];
+  __shared__ uint32_t s_n[kWarps][2];
   T* __restrict__ r = static_cast<T*>(A.r);
   T* __restrict__ kept = static_cast<T*>(A.kept);
+  T* __restrict__ list_val = static_cast<T*>(A.list_val);
+  K* __restrict__ cand_key = static_cast<K*>(A.cand_key);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpStage<T, kRing> take{s_ti[warp], s_tv[warp]};
-  WarpStage<K, kRing> cand{s_ci[warp], s_ck[warp]};
+  LaneRing<T, kRing> take{s_ti[warp], s_tv[warp], &s_n[warp][0]};
+  LaneRing<K, kRing> cand{s_ci[warp], s_ck[warp], &s_n[warp][1]};
   for (int b = threadIdx.x; b < kDigits; b += kThreads) hist2[b] = 0;
+  if (lane < 2) s_n[warp][lane] = 0;
   __syncthreads();
   uint32_t cur = kNone;
   auto flush_hist = [&]() {
@@ -443,101 +498,63 @@ __global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
       if (cur != kNone) flush_hist();
       cur = t;
     }
+    // bin > b1: taken (key >= k_take); bin == b1: candidate (key >= k_cand)
     const uint32_t b1 = A.thr[t];
+    const K k_cand = static_cast<K>(b1) << (KeyOf<T>::kBits - kBinBits);
+    const K k_take = static_cast<K>(b1 + 1) << (KeyOf<T>::kBits - kBinBits);
     const uint64_t lo = A.list_off[t], cb = A.t_begin[t];
+    uint32_t* sel_cnt = A.sel_cnt + t;
+    uint32_t* cand_cnt = A.cand_cnt + t;
+    auto hit = [&](uint32_t i, T c) {  // key >= k_cand
+      const K key = KeyOf<T>::key(c);
+      if (key >= k_take) {
+        take.claim(i, c, sel_cnt, A.list_idx, list_val, lo);
+        if (kept) kept[i] = c;
+        r[i] = sub_rn(c, c);
+      } else {
+        cand.claim(i, key, cand_cnt, A.cand_idx, cand_key, cb);
+        atomicAdd(&hist2[digit2_of<T>(key)], 1u);
+      }
+    };
     // 32-bit flat indices (the state checks N < 2^32).  Body chunks are
     // 16-byte aligned (covap_feedback_create cuts every tensor's unaligned
     // head and tail into chunks of their own, flagged scalar), so a lane loads
     // kU / W vectors: element q of the lane is vector (q / W), lane (q % W).
     constexpr int W = 16 / static_cast<int>(sizeof(T));
-    const bool vec = ch.pad == 0;
     const uint32_t cbeg = static_cast<uint32_t>(ch.begin), cend = static_cast<uint32_t>(ch.end);
-    const uint32_t span = vec ? kSpan : 32u;  // scalar chunks: one element per lane
-    for (uint32_t base = cbeg + warp * span; base < cend; base += kWarps * span) {
-      T cv[kU];
-      uint32_t ix[kU];
-      uint32_t valid = 0;
-      if (vec) {
-        using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    if (ch.pad == 0) {
+      using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+      for (uint32_t base = cbeg + warp * kSpan; base < cend; base += kWarps * kSpan) {
+        V x[kU / W];
 #pragma unroll
         for (int j = 0; j < kU / W; ++j) {
           const uint32_t e0 = base + (j * 32 + lane) * W;
-          V x;
-          if (e0 < cend) {
-            x = *reinterpret_cast<const V*>(r + e0);
-            valid |= ((1u << W) - 1u) << (j * W);
-          } else {
-            x = V{};
-          }
-          const T* xs = reinterpret_cast<const T*>(&x);
+          x[j] = e0 < cend ? *reinterpret_cast<const V*>(r + e0) : V{};
+        }
 #pragma unroll
-          for (int w = 0; w < W; ++w) {
-            cv[j * W + w] = xs[w];
-            ix[j * W + w] = e0 + w;
-          }
-        }
-      } else {
+        for (int j = 0; j < kU / W; ++j) {
+          const uint32_t e0 = base + (j * 32 + lane) * W;
+          const T* xs = reinterpret_cast<const T*>(&x[j]);
 #pragma unroll
-        for (int q = 0; q < kU; ++q) {
-          ix[q] = base + lane;
-          cv[q] = T(0);
+          for (int w = 0; w < W; ++w)
+            if (KeyOf<T>::key(xs[w]) >= k_cand && e0 < cend) hit(e0 + w, xs[w]);
         }
-        if (base + lane < cend) {
-          cv[0] = r[base + lane];
-          valid = 1u;
-        }
+        take.drain(sel_cnt, A.list_idx, list_val, lo, false);
+        cand.drain(cand_cnt, A.cand_idx, cand_key, cb, false);
       }
-      uint32_t mt = 0, mc = 0;
-#pragma unroll
-      for (int q = 0; q < kU; ++q) {
-        if (!((valid >> q) & 1u)) continue;
-        const uint32_t b = bin_of(cv[q]);
-        if (b > b1) {
-          mt |= 1u << q;
-          if (kept) kept[ix[q]] = cv[q];
-          r[ix[q]] = sub_rn(cv[q], cv[q]);
-        } else if (b == b1) {
-          mc |= 1u << q;
-          atomicAdd(&hist2[digit2_of<T>(KeyOf<T>::key(cv[q]))], 1u);
+    } else {  // scalar chunk: one element per lane
+      for (uint32_t base = cbeg + warp * 32; base < cend; base += kWarps * 32) {
+        const uint32_t e = base + lane;
+        if (e < cend) {
+          const T c = r[e];
+          if (KeyOf<T>::key(c) >= k_cand) hit(e, c);
         }
-      }
-      if (!__any_sync(0xffffffffu, mt | mc)) continue;
-      // Stage in groups of kG elements per lane (kG * 32 <= kRing): a warp
-      // scan of the per-lane counts (takes low 16 bits, candidates high).
-#pragma unroll
-      for (int g0 = 0; g0 < kU; g0 += kG) {
-        const uint32_t gt = (mt >> g0) & ((1u << kG) - 1u), gc = (mc >> g0) & ((1u << kG) - 1u);
-        const uint32_t mine = __popc(gt) | (__popc(gc) << 16);
-        uint32_t inc = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += y;
-        }
-        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-        if (tot == 0) continue;
-        const uint32_t ex = inc - mine, nt = tot & 0xffffu, nc = tot >> 16;
-        if (take.n - take.done + nt > kRing)
-          take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, true);
-        if (cand.n - cand.done + nc > kRing)
-          cand.flush(A.cand_cnt + t, A.cand_idx, static_cast<K*>(A.cand_key), cb, true);
-        uint32_t st = take.n + (ex & 0xffffu), sc = cand.n + (ex >> 16);
-        if (gt | gc) {
-#pragma unroll
-          for (int q = 0; q < kG; ++q) {
-            if ((gt >> q) & 1u) take.put(st++, ix[g0 + q], cv[g0 + q]);
-            if ((gc >> q) & 1u) cand.put(sc++, ix[g0 + q], KeyOf<T>::key(cv[g0 + q]));
-          }
-        }
-        take.n += nt;
-        cand.n += nc;
-        __syncwarp();
-        take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, false);
-        cand.flush(A.cand_cnt + t, A.cand_idx, static_cast<K*>(A.cand_key), cb, false);
+        take.drain(sel_cnt, A.list_idx, list_val, lo, false);
+        cand.drain(cand_cnt, A.cand_idx, cand_key, cb, false);
       }
     }
-    take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, true);
-    cand.flush(A.cand_cnt + t, A.cand_idx, static_cast<K*>(A.cand_key), cb, true);
+    take.drain(sel_cnt, A.list_idx, list_val, lo, true);
+    cand.drain(cand_cnt, A.cand_idx, cand_key, cb, true);
   }
   if (cur != kNone) flush_hist();
 }

@@ -1,4 +1,4 @@
-"""PCIe and host-pipeline chunk-size probe (not product code)."""
+"""PCIe and host-pipeline chunk-schedule probe (not product code)."""
 import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import torch
@@ -30,5 +30,10 @@ for name in ("resnet50", "bert_large"):
     hin = torch.empty(n, pin_memory=True); hout = torch.empty(n, pin_memory=True)
     sync = covap.CovapSync(plan, None, torch.float32, 0)
     for chunk in (1 << 21, 1 << 22, 1 << 23, 3 << 22):
-        ms = t(lambda: sync.sync_host(hin, hout, chunk_elems=chunk), reps=5 if name == "bert_large" else 10)
-        print(f"{name} chunk {chunk >> 20 if chunk >= 1<<20 else chunk/(1<<20)} Mi: {ms:.3f} ms -> e2e {4*n/ms/1e6:.1f} GB/s")
+        for ramp in (1 << 20, 1 << 18, 1 << 16, 1 << 14):
+            if ramp >= chunk // 2 and ramp != 1 << 20:
+                continue
+            sync.state.set_host_ramp(ramp)
+            ms = t(lambda: sync.sync_host(hin, hout, chunk_elems=chunk), reps=5 if name == "bert_large" else 10)
+            print(f"{name} chunk {chunk / (1 << 20):g} Mi ramp_min {ramp / (1 << 10):g} Ki: {ms:.3f} ms -> e2e {4*n/ms/1e6:.1f} GB/s",
+                  flush=True)
