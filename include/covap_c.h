@@ -357,7 +357,7 @@ typedef struct covap_feedback covap_feedback;
 /* ErrorFeedback(numels, schedule) with its filter; residuals zero.
  * InvalidInput: empty tensor list or an empty tensor for top-k / random-k
  * (sparsifier_k, compress.cpp:109), k_fraction outside (0, 1], K < 1, more
- * than 2^32 - 1 elements. */
+ * than 2^32 - 1 elements, more than 49152 tensors for top-k. */
 covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int dtype,
                                    const covap_ef* schedule, const covap_filter* filter,
                                    int device, covap_feedback** out);

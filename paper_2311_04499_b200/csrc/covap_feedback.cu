@@ -402,8 +402,14 @@ struct WarpStage {
 constexpr int kWarps = kThreads / 32;
 // collect: elements per lane per warp iteration (1 KB of c per warp; 2 KB
 // measured slower on VGG-16: 259 -> 387 us, register-limited occupancy)
+#ifndef COVAP_COLLECT_BYTES  // bytes of c per lane per warp iteration
+#define COVAP_COLLECT_BYTES 32
+#endif
+#ifndef COVAP_COLLECT_CTAS  // collect CTAs per SM
+#define COVAP_COLLECT_CTAS 4
+#endif
 template <typename T>
-constexpr int kCollectUnroll = 32 / static_cast<int>(sizeof(T));
+constexpr int kCollectUnroll = COVAP_COLLECT_BYTES / static_cast<int>(sizeof(T));
 
 // Per-warp ring fed lane by lane: a lane with a hit claims a slot with a
 // shared-memory atomic (hits are ~1% of elements, so the common path is one
@@ -560,49 +566,105 @@ __global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
 }
 
 // Level-1 candidates above d2 are taken, those at d2 go on to the final
-// selection.  Every warp strides over every tensor's candidates, so the work
-// is balanced however unevenly the candidates fall.
+// selection.  The candidates of all tensors form one flat index space (the
+// CTA scans cand_cnt into shared memory), so the work is balanced however
+// unevenly the candidates fall and no tensor waits for another.  The pass is
+// latency-bound (a dependent key -> r[i] gather per taken candidate), so every
+// lane keeps kF2 candidates in flight and the grid fills the SMs.  Appends are
+// warp-aggregated per tensor (one atomic per tensor present in the warp).
+constexpr int kF2 = 4;
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) topk_filter2_kernel(TopkArgs A) {
   using K = typename KeyOf<T>::K;
-  __shared__ uint32_t s_ti[kWarps][64], s_ci[kWarps][64];
-  __shared__ T s_tv[kWarps][64];
-  __shared__ K s_ck[kWarps][64];
+  using Scan = cub::BlockScan<uint32_t, kThreads>;
+  extern __shared__ uint32_t s_pre[];  // ntensors + 1 (kTopkMaxTensors bounds it)
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t s_carry;
   T* __restrict__ r = static_cast<T*>(A.r);
   T* __restrict__ kept = static_cast<T*>(A.kept);
+  T* __restrict__ list_val = static_cast<T*>(A.list_val);
   const K* __restrict__ ck = static_cast<const K*>(A.cand_key);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpStage<T> take{s_ti[warp], s_tv[warp]};
-  WarpStage<K> next{s_ci[warp], s_ck[warp]};
-  const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
-  for (uint32_t t = 0; t < A.ntensors; ++t) {
-    const uint32_t m = A.cand_cnt[t], d2 = A.thr2[t];
-    const uint64_t lo = A.list_off[t], cb = A.t_begin[t];
-    for (uint32_t e0 = gw * 32; e0 < m; e0 += nw * 32) {
-      const uint32_t e = e0 + lane;
-      bool tk = false, nx = false;
-      K key = 0;
-      uint32_t i = 0;
-      T c = T(0);
-      if (e < m) {
-        key = ck[cb + e];
-        i = A.cand_idx[cb + e];
-        const uint32_t d = digit2_of<T>(key);
-        tk = d > d2;
-        nx = d == d2;
-        if (tk) {
-          c = r[i];
-          if (kept) kept[i] = c;
-          r[i] = sub_rn(c, c);
+  K* __restrict__ ck2 = static_cast<K*>(A.cand2_key);
+  const uint32_t nt = A.ntensors;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t b0 = 0; b0 < nt; b0 += kThreads) {  // exclusive prefix of cand_cnt
+    const uint32_t t = b0 + threadIdx.x;
+    const uint32_t v = t < nt ? A.cand_cnt[t] : 0u;
+    uint32_t ex = 0, tot = 0;
+    Scan(tmp).ExclusiveSum(v, ex, tot);
+    if (t < nt) s_pre[t] = s_carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) s_pre[nt] = s_carry;
+  __syncthreads();
+  const uint32_t total = s_pre[nt];
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5), nw = gridDim.x * kWarps;
+  for (uint32_t base = gw * 32 * kF2; base < total; base += nw * 32 * kF2) {
+    uint32_t tq[kF2], iq[kF2];
+    K kq[kF2];
+    bool vq[kF2];
+#pragma unroll
+    for (int q = 0; q < kF2; ++q) {  // issue every lane's key / index loads first
+      const uint32_t e = base + q * 32 + lane;
+      vq[q] = e < total;
+      uint32_t lo = 0, hi = nt;  // tensor t with s_pre[t] <= e < s_pre[t + 1]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_pre[mid] <= e) lo = mid; else hi = mid;
+      }
+      tq[q] = lo;
+      const uint64_t at = A.t_begin[lo] + (e - s_pre[lo]);
+      kq[q] = vq[q] ? ck[at] : K(0);
+      iq[q] = vq[q] ? A.cand_idx[at] : 0u;
+    }
+    T cq[kF2];
+    bool tk[kF2], nx[kF2];
+#pragma unroll
+    for (int q = 0; q < kF2; ++q) {  // then the gathers of the taken values
+      const uint32_t d = digit2_of<T>(kq[q]), d2 = vq[q] ? A.thr2[tq[q]] : 0u;
+      tk[q] = vq[q] && d > d2;
+      nx[q] = vq[q] && d == d2;
+      cq[q] = tk[q] ? r[iq[q]] : T(0);
+    }
+#pragma unroll
+    for (int q = 0; q < kF2; ++q) {
+      if (tk[q]) {
+        if (kept) kept[iq[q]] = cq[q];
+        r[iq[q]] = sub_rn(cq[q], cq[q]);
+      }
+      // warp-aggregated appends, one round per tensor present in this slot
+      unsigned pending = __ballot_sync(0xffffffffu, tk[q] || nx[q]);
+      while (pending) {
+        const uint32_t t = __shfl_sync(0xffffffffu, tq[q], __ffs(pending) - 1);
+        const bool mine = tq[q] == t;
+        const unsigned mt = __ballot_sync(0xffffffffu, mine && tk[q]);
+        const unsigned mn = __ballot_sync(0xffffffffu, mine && nx[q]);
+        pending &= ~(mt | mn);
+        uint32_t bt = 0, bn = 0;
+        if (lane == 0) {
+          if (mt) bt = atomicAdd(A.sel_cnt + t, static_cast<uint32_t>(__popc(mt)));
+          if (mn) bn = atomicAdd(A.cand2_cnt + t, static_cast<uint32_t>(__popc(mn)));
+        }
+        bt = __shfl_sync(0xffffffffu, bt, 0);
+        bn = __shfl_sync(0xffffffffu, bn, 0);
+        if (mine && tk[q]) {
+          const uint64_t at = A.list_off[t] + bt + __popc(mt & lt);
+          A.list_idx[at] = iq[q];
+          list_val[at] = cq[q];
+        }
+        if (mine && nx[q]) {
+          const uint64_t at = A.t_begin[t] + bn + __popc(mn & lt);
+          A.cand2_idx[at] = iq[q];
+          ck2[at] = kq[q];
         }
       }
-      take.push(tk, i, c);
-      next.push(nx, i, key);
-      take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, false);
-      next.flush(A.cand2_cnt + t, A.cand2_idx, static_cast<K*>(A.cand2_key), cb, false);
     }
-    take.flush(A.sel_cnt + t, A.list_idx, static_cast<T*>(A.list_val), lo, true);
-    next.flush(A.cand2_cnt + t, A.cand2_idx, static_cast<K*>(A.cand2_key), cb, true);
   }
 }
 
@@ -1037,14 +1099,21 @@ cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uin
 template <typename T>
 cudaError_t launch_topk_t(const TopkArgs& a, int sms, cudaStream_t s) {
   if (a.ntensors == 0) return cudaSuccess;
-  const int grid = static_cast<int>(a.nchunks < static_cast<uint32_t>(sms * 4) ? a.nchunks
-                                                                             : sms * 4);
+  const uint32_t cap = static_cast<uint32_t>(sms * COVAP_COLLECT_CTAS);
+  const int grid = static_cast<int>(a.nchunks < cap ? a.nchunks : cap);
   topk_threshold_kernel<kBins><<<a.ntensors, kThreads, 0, s>>>(a.hist1, a.k, a.thr, a.need,
                                                                a.sel_cnt, a.cand_cnt);
   if (grid > 0) topk_collect_kernel<T><<<grid, kThreads, 0, s>>>(a);
   topk_threshold_kernel<kDigits><<<a.ntensors, kThreads, 0, s>>>(a.hist2, a.need, a.thr2, a.need2,
                                                                  a.cand2_cnt, nullptr);
-  topk_filter2_kernel<T><<<sms * 2, kThreads, 0, s>>>(a);
+  const uint32_t pre_bytes = (a.ntensors + 1) * 4;
+  if (pre_bytes > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(topk_filter2_kernel<T>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(pre_bytes));
+    if (e != cudaSuccess) return e;
+  }
+  topk_filter2_kernel<T><<<sms * 4, kThreads, pre_bytes, s>>>(a);
   topk_final_kernel<T><<<a.ntensors, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }

@@ -63,6 +63,8 @@ cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uin
 // 2048-bin histogram of the threshold bin's candidates, exact radix select
 // among the survivors.  Candidate arrays are indexed at the tensor's begin.
 constexpr int kDigitBits = 11;
+// The level-2 pass keeps a prefix over the tensors in shared memory.
+constexpr uint64_t kTopkMaxTensors = 49152;
 constexpr int kDigits = 1 << kDigitBits;
 struct TopkArgs {
   void* r;

@@ -306,6 +306,8 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
     need(filter->kind >= COVAP_FILTER_IDENTITY && filter->kind <= COVAP_FILTER_FP16,
          "unknown filter kind");
     if (filter->kind == COVAP_FILTER_COVAP) need(filter->interval >= 1, "interval must be >= 1");
+    if (filter->kind == COVAP_FILTER_TOPK)
+      need(n_tensors <= fb::kTopkMaxTensors, "top-k: at most 49152 tensors per state");
     if (schedule && schedule->enabled) need(schedule->ascend_steps >= 1, "ascend_steps must be >= 1");
     f = new covap_feedback;
     f->dtype = dtype;

@@ -160,11 +160,11 @@ int main(int argc, char** argv) {
   printf("n=%llu (%.1f MB per direction), %d SMs\n", (unsigned long long)c.n, mb, sms);
   float t;
   t = time_it(c.s0, 10, ce_h2d, &c);
-  printf("ce_h2d   %.3f ms  %.1f GB/s\n", t, mb / t / 1e3);
+  printf("ce_h2d   %.3f ms  %.1f GB/s\n", t, mb / t);
   t = time_it(c.s0, 10, ce_d2h, &c);
-  printf("ce_d2h   %.3f ms  %.1f GB/s\n", t, mb / t / 1e3);
+  printf("ce_d2h   %.3f ms  %.1f GB/s\n", t, mb / t);
   t = time_it(c.s0, 10, ce_both, &c);
-  printf("ce_both  %.3f ms  %.1f GB/s per direction\n", t, mb / t / 1e3);
+  printf("ce_both  %.3f ms  %.1f GB/s per direction\n", t, mb / t);
   const char* names[] = {"zc_h2d", "zc_d2h", "zc_both", "zc_k1f"};
   for (int mode = 0; mode < 4; ++mode) {
     for (int mult : {1, 2, 4, 8}) {
@@ -175,8 +175,37 @@ int main(int argc, char** argv) {
         t = time_it(c.s0, 10, run_kernel, &c);
         CK(cudaGetLastError());
         printf("%-8s grid %4d unroll %d  %.3f ms  %.1f GB/s per direction\n", names[mode], c.grid, u, t,
-               mb / t / 1e3);
+               mb / t);
       }
+    }
+  }
+  // hybrid: copy engines move a fraction f of both directions while a
+  // zero-copy kernel on a third stream moves the rest (host -> host via SMs)
+  {
+    cudaStream_t s2;
+    CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    cudaEvent_t a, b, j1, j2;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventCreateWithFlags(&j1, cudaEventDisableTiming); cudaEventCreateWithFlags(&j2, cudaEventDisableTiming);
+    for (double f : {1.0, 0.95, 0.9, 0.85, 0.8, 0.7}) {
+      const uint64_t nce = (uint64_t)(c.n * f) / 1024 * 1024, nzc = c.n - nce;
+      float best = 1e9;
+      for (int rep = 0; rep < 8; ++rep) {
+        cudaDeviceSynchronize();
+        cudaEventRecord(a, c.s0);
+        cudaStreamWaitEvent(c.s1, a, 0);
+        cudaStreamWaitEvent(s2, a, 0);
+        cudaMemcpyAsync(c.d_a, c.h_in, nce * 4, cudaMemcpyHostToDevice, c.s0);
+        cudaMemcpyAsync(c.h_out, c.d_b, nce * 4, cudaMemcpyDeviceToHost, c.s1);
+        if (nzc) copy_kernel<1><<<sms, 256, 0, s2>>>((const float4*)(c.h_in + nce), (float4*)(c.h_out + nce), nzc / 4);
+        cudaEventRecord(j1, c.s1); cudaEventRecord(j2, s2);
+        cudaStreamWaitEvent(c.s0, j1, 0); cudaStreamWaitEvent(c.s0, j2, 0);
+        cudaEventRecord(b, c.s0);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+      }
+      printf("hybrid f=%.2f  %.3f ms  (%.1f GB/s per direction)\n", f, best, mb / best);
     }
   }
   // correctness of the zero-copy k1f path: out = g + 0.5 * 0 = g
