@@ -118,6 +118,14 @@ __device__ __forceinline__ uint32_t append_slot(bool pred, uint32_t* counter) {
   return base + static_cast<uint32_t>(__popc(mask & ((1u << lane) - 1u)));
 }
 
+// The kept value as written to `kept`: itself, or — when kept is one rank's
+// synchronised output — allreduce_mean's (0.0 + x) * (1/1) (trainer.cpp:41-45),
+// which only turns -0 into +0.
+template <typename T>
+__device__ __forceinline__ T kept_value(T c, int mean) {
+  return mean ? add_rn(T(0), c) : c;
+}
+
 template <typename T>
 __device__ __forceinline__ T compensate(T g, T r, T coeff, int ef) {
   return ef ? add_rn(g, mul_rn(coeff, r)) : g;  // compress.cpp:332-336
@@ -185,7 +193,11 @@ __global__ void __launch_bounds__(kThreads) dense_kernel(DenseArgs A) {
           T* ns = reinterpret_cast<T*>(&nr);
 #pragma unroll
           for (int w = 0; w < W; ++w) one(compensate(gs[w], rs[w], coeff, A.ef), ks[w], ns[w], hv[w]);
-          if (kept) k4[v] = kv;
+          if (kept) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) ks[w] = kept_value(ks[w], A.kept_mean);
+            k4[v] = kv;
+          }
           if (r) r4[v] = nr;
           if (KIND == kFp16 && A.wire) {
             if (W == 4)
@@ -204,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) dense_kernel(DenseArgs A) {
       T k, res;
       uint16_t h = 0;
       one(compensate(g[i], A.ef ? r[i] : T(0), coeff, A.ef), k, res, h);
-      if (kept) kept[i] = k;
+      if (kept) kept[i] = kept_value(k, A.kept_mean);
       if (r) r[i] = res;
       if (KIND == kFp16 && A.wire) A.wire[i] = h;
     }
@@ -515,7 +527,7 @@ __global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
       const K key = KeyOf<T>::key(c);
       if (key >= k_take) {
         take.claim(i, c, sel_cnt, A.list_idx, list_val, lo);
-        if (kept) kept[i] = c;
+        if (kept) kept[i] = kept_value(c, A.kept_mean);
         r[i] = sub_rn(c, c);
       } else {
         cand.claim(i, key, cand_cnt, A.cand_idx, cand_key, cb);
@@ -635,7 +647,7 @@ __global__ void __launch_bounds__(kThreads) topk_filter2_kernel(TopkArgs A) {
 #pragma unroll
     for (int q = 0; q < kF2; ++q) {
       if (tk[q]) {
-        if (kept) kept[iq[q]] = cq[q];
+        if (kept) kept[iq[q]] = kept_value(cq[q], A.kept_mean);
         r[iq[q]] = sub_rn(cq[q], cq[q]);
       }
       // warp-aggregated appends, one round per tensor present in this slot
@@ -747,7 +759,7 @@ __global__ void __launch_bounds__(kThreads) topk_final_kernel(TopkArgs A) {
       const T c = r[i];
       list_idx[base + slot] = i;
       list_val[base + slot] = c;
-      if (kept) kept[i] = c;
+      if (kept) kept[i] = kept_value(c, A.kept_mean);
       r[i] = sub_rn(c, c);
     }
   }
@@ -840,7 +852,8 @@ __global__ void randomk_chain_kernel(RandomkArgs A) {
 // targeted position m (then W of that draw).  kept[S] = c, r[S] = c - c.
 template <typename T>
 __global__ void randomk_gather_kernel(RandomkArgs A, T* __restrict__ r, T* __restrict__ kept,
-                                      uint32_t* __restrict__ list_idx, T* __restrict__ list_val) {
+                                      int kept_mean, uint32_t* __restrict__ list_idx,
+                                      T* __restrict__ list_val) {
   for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
        e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t t = tensor_of_entry(A, e);
@@ -859,7 +872,7 @@ __global__ void randomk_gather_kernel(RandomkArgs A, T* __restrict__ r, T* __res
     const T c = r[flat];
     list_idx[e] = static_cast<uint32_t>(flat);
     list_val[e] = c;
-    if (kept) kept[flat] = c;
+    if (kept) kept[flat] = kept_value(c, kept_mean);
     r[flat] = sub_rn(c, c);
     A.head[A.t_begin[t] + j] = kNone;  // the chain kernel is done with the lists
   }
@@ -1133,16 +1146,17 @@ cudaError_t launch_randomk_select(const RandomkArgs& a, int sms, cudaStream_t s)
 }
 
 cudaError_t launch_randomk_gather(int dtype, const RandomkArgs& a, void* r, void* kept,
-                                  uint32_t* list_idx, void* list_val, int sms, cudaStream_t s) {
+                                  int kept_mean, uint32_t* list_idx, void* list_val, int sms,
+                                  cudaStream_t s) {
   if (a.total == 0) return cudaSuccess;
   const int grid = grid_for(a.total, sms, 8);
   if (dtype == 1)
     randomk_gather_kernel<double><<<grid, kThreads, 0, s>>>(
-        a, static_cast<double*>(r), static_cast<double*>(kept), list_idx,
+        a, static_cast<double*>(r), static_cast<double*>(kept), kept_mean, list_idx,
         static_cast<double*>(list_val));
   else
     randomk_gather_kernel<float><<<grid, kThreads, 0, s>>>(
-        a, static_cast<float*>(r), static_cast<float*>(kept), list_idx,
+        a, static_cast<float*>(r), static_cast<float*>(kept), kept_mean, list_idx,
         static_cast<float*>(list_val));
   return cudaGetLastError();
 }

@@ -39,6 +39,7 @@ struct DenseArgs {
   const void* g;
   void* r;
   void* kept;
+  int kept_mean;      // kept receives allreduce_mean's (0 + k) * 1 (one rank's sync output)
   uint16_t* wire;
   unsigned long long* sat;
   const Chunk* chunks;
@@ -69,6 +70,7 @@ constexpr int kDigits = 1 << kDigitBits;
 struct TopkArgs {
   void* r;
   void* kept;
+  int kept_mean;      // as DenseArgs::kept_mean
   const Chunk* chunks;
   uint32_t nchunks;
   uint32_t ntensors;
@@ -115,7 +117,8 @@ struct RandomkArgs {
 cudaError_t launch_randomk_select(const RandomkArgs& a, int sms, cudaStream_t s);
 // list[e] = (flat index S_e, c); kept[S] = c; r[S] = c - c; head cleared.
 cudaError_t launch_randomk_gather(int dtype, const RandomkArgs& a, void* r, void* kept,
-                                  uint32_t* list_idx, void* list_val, int sms, cudaStream_t s);
+                                  int kept_mean, uint32_t* list_idx, void* list_val, int sms,
+                                  cudaStream_t s);
 
 // Exchange side (the mean of the kept gradients over P ranks, trainer.cpp:402
 // and 35-47): out was zero-filled by the compensation pass.

@@ -141,7 +141,7 @@ fb::RandomkArgs randomk_args(covap_feedback* f) {
 // the sparse filters leave (index, value) pairs in list_idx / list_val and
 // fp16 its halves in `half` when wire is set.
 void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool wire,
-             cudaStream_t st) {
+             cudaStream_t st, bool kept_mean = false) {
   const int dt = f->dtype == COVAP_F64 ? 1 : 0;
   const double coeff = coeff_of(f);
   const uint32_t nt = static_cast<uint32_t>(f->numel.size());
@@ -153,6 +153,7 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       a.g = grad;
       a.r = f->residual;
       a.kept = kept;
+      a.kept_mean = kept_mean ? 1 : 0;
       a.wire = wire ? f->half : nullptr;
       a.sat = f->d_sat;
       a.chunks = f->chunks;
@@ -171,6 +172,7 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       fb::TopkArgs a{};
       a.r = f->residual;
       a.kept = kept;
+      a.kept_mean = kept_mean ? 1 : 0;
       a.chunks = f->chunks;
       a.nchunks = f->nchunks;
       a.ntensors = nt;
@@ -206,7 +208,8 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       CK(fb::launch_compensate(dt, grad, f->residual, zero, nullptr, f->chunks, f->nchunks,
                                f->ef.enabled, coeff, f->sms, st));
       CK(cudaStreamWaitEvent(st, f->ev_join, 0));
-      CK(fb::launch_randomk_gather(dt, a, f->residual, kept, f->list_idx, f->list_val, f->sms,
+      CK(fb::launch_randomk_gather(dt, a, f->residual, kept, kept_mean ? 1 : 0, f->list_idx,
+                                   f->list_val, f->sms,
                                    st));
       break;
     }
@@ -539,15 +542,17 @@ covap_status covap_feedback_sync_step(covap_feedback* f, covap_comm* comm, const
          "the identity / covap filters have no sync wire (use covap_sync_step)");
     DeviceGuard dg(f->device);
     const cudaStream_t st = as_stream(stream);
+    const int P = world(comm);
+    if (P == 1) {
+      // One rank: the mean is (0 + kept) * 1, so the filter writes it straight
+      // into out (zero-filled first for the sparsifiers) and no wire is built.
+      ef_step(f, grad, out, sparse(f) ? out : nullptr, false, st, true);
+      return;
+    }
     ef_step(f, grad, nullptr, sparse(f) ? out : nullptr, true, st);
     void *a, *b;
     uint64_t ba, bb;
     wire_of(f, &a, &ba, &b, &bb);
-    const int P = world(comm);
-    if (P == 1) {
-      combine(f, a, b, 1, out, st);
-      return;
-    }
     grow(&f->recv_a, &f->cap_a, ba * P);
     grow(&f->recv_b, &f->cap_b, bb * P);
     NK(ncclGroupStart());
@@ -606,7 +611,8 @@ covap_status covap_randomk_compress(int device, int dtype, const void* x, uint64
     a.raw_seed = 1;
     a.seed = seed;
     CK(fb::launch_randomk_select(a, f->sms, s));
-    CK(fb::launch_randomk_gather(dt, a, f->residual, nullptr, f->list_idx, f->list_val, f->sms, s));
+    CK(fb::launch_randomk_gather(dt, a, f->residual, nullptr, 0, f->list_idx, f->list_val, f->sms,
+                                 s));
     CK(fb::order_list(dt, fb::kRandomk, f->list_idx, f->list_val, f->k_total, indices, values, s));
     CK(cudaStreamSynchronize(s));
     *k = f->k_total;
