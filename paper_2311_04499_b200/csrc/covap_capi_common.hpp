@@ -93,11 +93,16 @@ inline covap_status guarded(F&& body) {
   }
 }
 
-// Restores the caller's current device on scope exit.
+// Restores the caller's current device on scope exit (no device switch, and
+// so no extra runtime calls, when the caller is already on dev).
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
     if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev == dev) {
+      prev = -1;
+      return;
+    }
     CK(cudaSetDevice(dev));
   }
   ~DeviceGuard() {

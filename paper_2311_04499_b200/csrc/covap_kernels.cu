@@ -39,6 +39,11 @@
 #include "covap_internal.h"
 
 namespace covapb {
+#ifdef COVAP_K2_TRACE
+// Diagnostic build only: per-CTA K2 timeline (start, end ns; full / none /
+// mixed tile counts; ns spent waiting on the load barrier).
+__device__ unsigned long long g_k2_trace[1024 * 6];
+#endif
 namespace {
 
 // Pipeline shape (defaults = the measured best on B200, see DESIGN.md §3;
@@ -442,6 +447,10 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   __shared__ __align__(8) uint64_t bar[NS];
 
   pdl_launch_dependents();
+#ifdef COVAP_K2_TRACE
+  unsigned long long tr_t0, tr_wait = 0, tr_full = 0, tr_none = 0, tr_mixed = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_t0));
+#endif
   const uint64_t a16 = (A.a + W - 1) / W * W;
   const uint64_t b16 = A.b / W * W;
   if (a16 >= b16) {
@@ -496,48 +505,109 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
     const TileSel sel = classify<T>(A.runs, A.nruns, e0, e1);
     if (sel.cls == kNone) {  // zero fill (compress.cpp:91); SGD: nothing to do
       if (!SGD && threadIdx.x == 0) bulk_store(A.out + e0, zero, n * sizeof(T));
+#ifdef COVAP_K2_TRACE
+      ++tr_none;
+#endif
       continue;
     }
     if (sel.cls == kMixed) {
-      // Tiles that straddle a shard boundary: per element, all of a
-      // thread's recv loads issued before any use (coalesced across the
-      // warp), so the tile costs about one memory latency, not one per
-      // element.  The runs table is L1-resident.
-      constexpr int kPer = TE / kThreads;
-      static_assert(kPer <= 32, "selection mask is 32 bits");
-      T vals[kPer];
-      uint32_t hit = 0;
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const uint32_t i = threadIdx.x + q * kThreads;
-        vals[q] = T(0);
-        if (i < n) {
-          const uint64_t e = e0 + i;
-          int j = sel.j;
-          while (j < A.nruns && A.runs[j].end <= e) ++j;
-          if (j < A.nruns && A.runs[j].begin <= e) {
-            vals[q] = A.recv[A.runs[j].dst + (e - A.runs[j].begin)];
-            hit |= 1u << q;
+#ifdef COVAP_K2_TRACE
+      ++tr_mixed;
+#endif
+      // Tiles that straddle a shard boundary: walked as segments, each
+      // wholly selected (out = scale(recv), straight from global) or wholly
+      // unselected (zero fill / untouched); the block handles one segment at
+      // a time with 16-byte vectors — recv and out line up modulo 16 bytes
+      // whenever dst == begin (mod W), which the planner guarantees — and
+      // batches its loads so a segment costs about one memory latency.
+      // (A per-element path here made these few tiles the critical path:
+      // ~5 us each, scripts/k2_trace.py.)
+      int j = sel.j;
+      uint64_t pos = e0;
+      while (pos < e1) {
+        const bool in_run = j < A.nruns && A.runs[j].begin <= pos;
+        const uint64_t end = in_run ? min(e1, A.runs[j].end)
+                                    : (j < A.nruns ? min(e1, A.runs[j].begin) : e1);
+        if (in_run) {
+          const T* src = A.recv + A.runs[j].dst + (pos - A.runs[j].begin);
+          T* dst = A.out + pos;
+          const uint64_t len = end - pos;
+          const uint64_t mis = (reinterpret_cast<uintptr_t>(dst) / sizeof(T)) % W;
+          const uint64_t head = (len < (W - mis) % W ? len : (W - mis) % W);
+          const bool aligned = ((reinterpret_cast<uintptr_t>(src) / sizeof(T)) % W) == mis;
+          const uint64_t nv = aligned ? (len - head) / W : 0;
+          const uint64_t body_end = aligned ? head + nv * W : 0;
+          // scalar head and tail (the whole segment when misaligned)
+          auto scalar = [&](uint64_t i0, uint64_t i1) {
+            for (uint64_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
+              const T u = scale_of(src[i], A.inv, A.mean);
+              dst[i] = SGD ? sgd(dst[i], A.lr, u) : u;
+            }
+          };
+          if (aligned) {
+            scalar(0, head);
+            scalar(body_end, len);
+          } else {
+            scalar(0, len);
           }
-        }
-      }
+          const V* sv = reinterpret_cast<const V*>(src + head);
+          V* dv = reinterpret_cast<V*>(dst + head);
+          constexpr int kB = 4;  // vectors in flight per thread
+          for (uint64_t v0 = 0; v0 < nv; v0 += kB * kThreads) {
+            V x[kB];
 #pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const uint32_t i = threadIdx.x + q * kThreads;
-        if (i >= n) continue;
-        const bool h = (hit >> q) & 1u;
-        if (!SGD)
-          A.out[e0 + i] = h ? scale_of(vals[q], A.inv, A.mean) : T(0);
-        else if (h)
-          A.out[e0 + i] = sgd(A.out[e0 + i], A.lr, scale_of(vals[q], A.inv, A.mean));
+            for (int q = 0; q < kB; ++q) {
+              const uint64_t v = v0 + q * kThreads + threadIdx.x;
+              if (v < nv) x[q] = sv[v];
+            }
+#pragma unroll
+            for (int q = 0; q < kB; ++q) {
+              const uint64_t v = v0 + q * kThreads + threadIdx.x;
+              if (v >= nv) continue;
+              V y = x[q];
+#pragma unroll
+              for (int w = 0; w < static_cast<int>(W); ++w) lane(y, w) = scale_of(lane(y, w), A.inv, A.mean);
+              if (SGD) {
+                const V p = dv[v];
+#pragma unroll
+                for (int w = 0; w < static_cast<int>(W); ++w) lane(y, w) = sgd(lane(p, w), A.lr, lane(y, w));
+              }
+              dv[v] = y;
+            }
+          }
+          ++j;
+        } else if (!SGD) {  // zero fill; tiles are 16-byte aligned, segments need not be
+          T* dst = A.out + pos;
+          const uint64_t len = end - pos;
+          const uint64_t mis = (reinterpret_cast<uintptr_t>(dst) / sizeof(T)) % W;
+          const uint64_t head = (len < (W - mis) % W ? len : (W - mis) % W);
+          const uint64_t nv = (len - head) / W;
+          for (uint64_t i = threadIdx.x; i < head; i += kThreads) dst[i] = T(0);
+          for (uint64_t i = head + nv * W + threadIdx.x; i < len; i += kThreads) dst[i] = T(0);
+          V z;
+#pragma unroll
+          for (int w = 0; w < static_cast<int>(W); ++w) lane(z, w) = T(0);
+          V* dv = reinterpret_cast<V*>(dst + head);
+          for (uint64_t v = threadIdx.x; v < nv; v += kThreads) dv[v] = z;
+        }
+        pos = end;
       }
       continue;
     }
     const int s = static_cast<int>(qc % NS);
     T* st = stage + (qc & 1) * TE;
+#ifdef COVAP_K2_TRACE
+    unsigned long long tw0, tw1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw0));
+    ++tr_full;
+#endif
     if (threadIdx.x == 0) bulk_wait_read<1>();
     mbar_wait(&bar[s], static_cast<uint32_t>((qc / NS) & 1));
     __syncthreads();
+#ifdef COVAP_K2_TRACE
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw1));
+    tr_wait += tw1 - tw0;
+#endif
     const V* xv = reinterpret_cast<const V*>(in + s * kSlotTiles * TE);
     const V* pv = reinterpret_cast<const V*>(in + (s * kSlotTiles + 1) * TE);
     V* sv = reinterpret_cast<V*>(st);
@@ -564,6 +634,14 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   if (threadIdx.x == 0) {
     bulk_commit();
     bulk_wait_all();
+#ifdef COVAP_K2_TRACE
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (blockIdx.x < 1024) {
+      unsigned long long* o = g_k2_trace + blockIdx.x * 6;
+      o[0] = tr_t0; o[1] = t1; o[2] = tr_full; o[3] = tr_none; o[4] = tr_mixed; o[5] = tr_wait;
+    }
+#endif
   }
 }
 
@@ -849,4 +927,10 @@ uint64_t stream_key(uint64_t seed, uint64_t rank, uint64_t step) {
   return host_mix_seed(host_mix_seed(seed, 0x100 + rank), step);
 }
 
+#ifdef COVAP_K2_TRACE
+extern "C" int covap_debug_k2_trace(unsigned long long* host, int nblocks) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_k2_trace, sizeof(unsigned long long) * 6 *
+                                                                     static_cast<size_t>(nblocks)));
+}
+#endif
 }  // namespace covapb

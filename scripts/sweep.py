@@ -46,6 +46,40 @@ while mb <= a.max_mb:
         st = covap.CompressorState(plan, torch.float32, 0)
         cycles = max(1, min(64, int(2e9 // (16 * n * 4)) // K + 1))
         res = {}
+
+        def one(mode, g):
+            if mode == "k1f":
+                st.filter_unpack(g, out)
+            elif mode == "k1":
+                st.filter_pack(g)
+            else:
+                st.unpack(out, 1.0, True)
+            st.step_end()
+
+        # Kernel-only time: one K-cycle (every phase once) captured in a CUDA
+        # graph and replayed, so the host launch path (Python -> ctypes ->
+        # C-ABI, ~10 us per call) cannot starve the GPU at small sizes.
+        graph_ms = {}
+        cap = torch.cuda.Stream()
+        for mode in ("k1f", "k1", "k2"):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(cap):
+                one(mode, grads[0])  # warm-up outside capture (attributes, first launch)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(gr, stream=cap):
+                    for k in range(K):
+                        one(mode, grads[k % ng])
+            reps = max(3, cycles)
+            gr.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()  # replay() launches on the current stream
+            for _ in range(reps):
+                gr.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            graph_ms[mode] = e0.elapsed_time(e1) / (reps * K)
+            del gr
         for mode in ("k1f", "k1", "k2"):
             for _ in range(K):  # warm-up cycle
                 st.filter_unpack(grads[0], out) if mode == "k1f" else (
@@ -72,25 +106,31 @@ while mb <= a.max_mb:
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / (cycles * K)
-            res[mode] = (ms, byts / (cycles * K) / (ms * 1e-3) / 1e9)
+            gb = byts / (cycles * K) / 1e9
+            res[mode] = (ms, gb / (ms * 1e-3), graph_ms[mode], gb / (graph_ms[mode] * 1e-3))
         rows.append((mb, K, n, res))
-        print(mb, K, {k: (round(v[0] * 1e3, 1), round(v[1])) for k, v in res.items()}, flush=True)
+        print(mb, K, {k: tuple(round(x, 4) for x in v) for k, v in res.items()}, flush=True)
         del st, plan
     del grads, out
     torch.cuda.empty_cache()
     mb *= 2
 
 lines = ["# Synthetic bucket sweep (BASELINE config 5), one B200\n",
-         "16 equal buckets of B MB (N = 16 B / 4 fp32 elements), S = N/K.  Back-to-back "
-         f"launches over whole K-cycles; fraction of the measured {peak} GB/s copy peak.  "
-         "K1F = fused single-rank sync (16N bytes); K1 = filter_pack (12N + 4S); "
-         "K2 = unpack (4N + 4S).\n",
-         "| bucket | K | N (M elems) | K1F µs | K1F frac | K1 µs | K1 frac | K2 µs | K2 frac |",
-         "|---|---|---|---|---|---|---|---|---|"]
+         "16 equal buckets of B MB (N = 16 B / 4 fp32 elements), S = N/K.  Fraction of the "
+         f"measured {peak} GB/s copy peak.  K1F = fused single-rank sync (16N bytes); "
+         "K1 = filter_pack (12N + 4S); K2 = unpack (4N + 4S).  *graph*: one K-cycle "
+         "captured in a CUDA graph and replayed (kernel time); *eager*: the same launches "
+         "issued one by one from Python through the C-ABI (includes the host launch path, "
+         "which dominates below ~8 MB buckets).\n",
+         "| bucket | K | N (M elems) | K1F µs graph | K1F frac graph | K1F frac eager | K1 µs graph | "
+         "K1 frac graph | K1 frac eager | K2 µs graph | K2 frac graph | K2 frac eager |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|"]
 for mb, K, n, res in rows:
-    lines.append(f"| {mb} MB | {K} | {n / 1e6:.1f} | {res['k1f'][0] * 1e3:.1f} | "
-                 f"{res['k1f'][1] / peak:.3f} | {res['k1'][0] * 1e3:.1f} | {res['k1'][1] / peak:.3f} | "
-                 f"{res['k2'][0] * 1e3:.1f} | {res['k2'][1] / peak:.3f} |")
+    c = []
+    for m in ("k1f", "k1", "k2"):
+        ms, gbs, gms, ggbs = res[m]
+        c += [f"{gms * 1e3:.1f}", f"{ggbs / peak:.3f}", f"{gbs / peak:.3f}"]
+    lines.append(f"| {mb} MB | {K} | {n / 1e6:.1f} | " + " | ".join(c) + " |")
 os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
 with open(a.out, "w") as f:
     f.write("\n".join(lines) + "\n")
