@@ -400,9 +400,69 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
         sv[v] = x;
       }
     } else {
+      // Tile straddling a shard boundary: segments wholly selected or wholly
+      // unselected, each written by the block with 16-byte vectors between
+      // scalar edges (the tile itself is 16-byte aligned; segments need not be).
       int j = sel.j;
-      for (uint32_t i = threadIdx.x; i < n; i += kThreads)
-        element<T, OP>(A, j, e0 + i, gs[i], A.ef ? rs[i] : T(0));
+      uint64_t pos = e0;
+      while (pos < e1) {
+        const bool in_run = j < A.nruns && A.runs[j].begin <= pos;
+        const uint64_t end = in_run ? min(e1, A.runs[j].end)
+                                    : (j < A.nruns ? min(e1, A.runs[j].begin) : e1);
+        const uint64_t len = end - pos, i0 = pos - e0;
+        const uint64_t head = (W - pos % W) % W < len ? (W - pos % W) % W : len;
+        const uint64_t nv = (len - head) / W;
+        // send slot of element e (OP 0); vectors need dst == begin (mod W)
+        T* send_at = (OP == 0 && in_run) ? A.send + A.runs[j].dst - A.runs[j].begin : nullptr;
+        const bool vec_ok = !(OP == 0 && in_run) || (A.runs[j].dst - A.runs[j].begin) % W == 0;
+        auto one = [&](uint64_t i) {  // element pos + i
+          const uint64_t e = pos + i;
+          const T c = A.ef ? add_rn(gs[i0 + i], mul_rn(A.coeff, rs[i0 + i])) : gs[i0 + i];
+          if (in_run) {
+            if (OP == 0) send_at[e] = c;
+            else if (OP == 1) A.out[e] = scale_of(c, A.inv, 1);
+            else A.out[e] = sgd(A.out[e], A.lr, scale_of(c, A.inv, 1));
+            A.r[e] = T(0);
+          } else {
+            A.r[e] = c;
+            if (OP == 1) A.out[e] = T(0);
+          }
+        };
+        const uint64_t body = vec_ok ? nv : 0;
+        for (uint64_t i = threadIdx.x; i < head; i += kThreads) one(i);
+        for (uint64_t i = head + body * W + threadIdx.x; i < len; i += kThreads) one(i);
+        for (uint64_t v = threadIdx.x; v < body; v += kThreads) {
+          const uint64_t i = head + v * W, e = pos + i;
+          V x = *reinterpret_cast<const V*>(gs + i0 + i);
+          if (A.ef) {
+            const V y = *reinterpret_cast<const V*>(rs + i0 + i);
+#pragma unroll
+            for (int q = 0; q < static_cast<int>(W); ++q)
+              lane(x, q) = add_rn(lane(x, q), mul_rn(A.coeff, lane(y, q)));
+          }
+          V z;
+#pragma unroll
+          for (int q = 0; q < static_cast<int>(W); ++q) lane(z, q) = T(0);
+          if (in_run) {
+            if (OP == 0) {
+              *reinterpret_cast<V*>(send_at + e) = x;
+            } else {
+              V o = OP == 3 ? *reinterpret_cast<const V*>(A.out + e) : z;
+#pragma unroll
+              for (int q = 0; q < static_cast<int>(W); ++q)
+                lane(o, q) = OP == 1 ? scale_of(lane(x, q), A.inv, 1)
+                                     : sgd(lane(o, q), A.lr, scale_of(lane(x, q), A.inv, 1));
+              *reinterpret_cast<V*>(A.out + e) = o;
+            }
+            *reinterpret_cast<V*>(A.r + e) = z;
+          } else {
+            *reinterpret_cast<V*>(A.r + e) = x;
+            if (OP == 1) *reinterpret_cast<V*>(A.out + e) = z;
+          }
+        }
+        if (in_run) ++j;
+        pos = end;
+      }
     }
     fence_async_smem();
     __syncthreads();
