@@ -61,6 +61,8 @@ tpath = os.path.join(P, "dram_traffic.json")
 if os.path.exists(tpath):
     traffic = json.load(open(tpath))
 for rep in sorted(glob.glob(os.path.join(G, "prof_*.ncu-rep"))):
+    if os.path.basename(rep)[5:].split("_")[0] not in ("r50", "bert", "vgg"):
+        continue  # other studies' captures (f4, K2 traces) are summarised by hand
     name = os.path.basename(rep)[5:-8]
     lines.append(f"\n## {name}\n")
     lines.append("| kernel | µs | DRAM read MB | DRAM write MB | DRAM % peak | SM % | warps active % | regs | grid | dyn smem KB |")
