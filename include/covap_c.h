@@ -300,9 +300,20 @@ covap_status covap_peer_attach_local(covap_peer** peers, int nranks);
 /* max_ctas: cap the collective's grid (0 = one CTA per SM); timeout_s: bound
  * of every spin-wait (0 = keep). */
 covap_status covap_peer_set_limits(covap_peer* peer, int max_ctas, double timeout_s);
-/* fused = 1 (default): the collective's last phase reads the reduced slices
- * straight from their owners and writes the synchronised gradient (C1 + K2 in
- * one kernel); fused = 0: all-gather into the local send buffer, then K2. */
+/* mode (named "fused" for compatibility):
+ *   1 (default)  K1 kernel, then the collective whose last phase reads the
+ *                reduced slices straight from their owners and writes the
+ *                synchronised gradient (C1 + K2 in one kernel);
+ *   0            K1, collective with an all-gather into the local send
+ *                buffer, then K2;
+ *   2            the whole step as ONE kernel per rank: K1 packs the send
+ *                buffer chunk by chunk (16 Ki elements) and publishes each
+ *                chunk; the chunk's owner (chunk mod P) reduces it in rank
+ *                order as soon as every rank published it; every rank
+ *                unpacks each reduced chunk from its owner as soon as it is
+ *                published, while the unselected range is filtered — the
+ *                transfer overlaps the filter chunk by chunk.
+ * InvalidInput for any other value. */
 covap_status covap_peer_set_fused(covap_peer* peer, int fused);
 covap_status covap_peer_check(covap_peer* peer);
 /* K1 into the parity buffer -> peer allreduce -> K2 (x 1/P) -> ++step. */

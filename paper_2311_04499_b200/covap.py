@@ -803,9 +803,12 @@ class PeerGroup:
     def set_limits(self, max_ctas: int = 0, timeout_s: float = 0.0):
         L.lib().covap_peer_set_limits(self._h, int(max_ctas), float(timeout_s))
 
-    def set_fused(self, fused: bool):
-        """C1 + K2 in one kernel (default) or all-gather then K2."""
-        L.lib().covap_peer_set_fused(self._h, 1 if fused else 0)
+    MODE_GATHER, MODE_FUSED, MODE_STEP = 0, 1, 2
+
+    def set_fused(self, fused):
+        """True / 1: C1 + K2 in one kernel (default); False / 0: all-gather
+        then K2; 2 (MODE_STEP): K1 + C1 + K2 as one kernel, chunk by chunk."""
+        L.lib().covap_peer_set_fused(self._h, int(fused))
 
     def check(self):
         L.lib().covap_peer_check(self._h)

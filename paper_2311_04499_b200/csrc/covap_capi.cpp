@@ -1062,8 +1062,10 @@ struct covap_peer {
   uint64_t cap = 0;                 // send-buffer capacity, elements
   size_t esize = 4;
   void* bufs[2] = {nullptr, nullptr};  // my send buffers (step parity)
-  uint64_t* flags = nullptr;           // my flag block
+  uint64_t* flags = nullptr;           // my flag block (covapb::peer_flag_words(cmax) words)
+  uint64_t cmax = 0;                   // send chunks the flag block covers (whole-step mode)
   unsigned* counter = nullptr;
+  unsigned* queue = nullptr;           // whole-step mode: work queue + finished CTAs
   int* err = nullptr;
   void* peer_bufs[2][covapb::kMaxPeers] = {};
   uint64_t* peer_flags[covapb::kMaxPeers] = {};
@@ -1072,7 +1074,10 @@ struct covap_peer {
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s
   int max_ctas = 0;
   bool attached = false;
-  bool fused = true;  // the collective's last phase writes out (no separate K2)
+  // 0: K1, allreduce kernel (all-gather), K2; 1: K1, allreduce kernel with
+  // the unpack fused (default); 2: the whole step in one kernel (peer_step_kernel)
+  int mode = 1;
+  uint64_t posted = 0;  // last epoch at which every rank published an arrival
 };
 
 extern "C" {
@@ -1094,10 +1099,14 @@ covap_status covap_peer_create(covap_state* s, int nranks, int rank, covap_peer*
       CK(cudaMalloc(&p->bufs[k], p->cap * p->esize));
       CK(cudaMemset(p->bufs[k], 0, p->cap * p->esize));  // alignment gaps stay zero
     }
-    CK(cudaMalloc(reinterpret_cast<void**>(&p->flags), 2 * covapb::kMaxPeers * sizeof(uint64_t)));
-    CK(cudaMemset(p->flags, 0, 2 * covapb::kMaxPeers * sizeof(uint64_t)));
+    p->cmax = (p->cap + covapb::kPeerChunk - 1) / covapb::kPeerChunk;
+    const size_t fbytes = covapb::peer_flag_words(p->cmax) * sizeof(uint64_t);
+    CK(cudaMalloc(reinterpret_cast<void**>(&p->flags), fbytes));
+    CK(cudaMemset(p->flags, 0, fbytes));
     CK(cudaMalloc(reinterpret_cast<void**>(&p->counter), sizeof(unsigned)));
     CK(cudaMemset(p->counter, 0, sizeof(unsigned)));
+    CK(cudaMalloc(reinterpret_cast<void**>(&p->queue), 2 * sizeof(unsigned)));
+    CK(cudaMemset(p->queue, 0, 2 * sizeof(unsigned)));
     CK(cudaMalloc(reinterpret_cast<void**>(&p->err), sizeof(int)));
     CK(cudaMemset(p->err, 0, sizeof(int)));
     for (int k = 0; k < 2; ++k) p->peer_bufs[k][rank] = p->bufs[k];
@@ -1118,6 +1127,7 @@ void covap_peer_destroy(covap_peer* p) {
   cudaFree(p->bufs[0]);
   cudaFree(p->bufs[1]);
   cudaFree(p->flags);
+  cudaFree(p->queue);
   cudaFree(p->counter);
   cudaFree(p->err);
   if (prev >= 0) cudaSetDevice(prev);
@@ -1188,10 +1198,11 @@ covap_status covap_peer_set_limits(covap_peer* p, int max_ctas, double timeout_s
   });
 }
 
-covap_status covap_peer_set_fused(covap_peer* p, int fused) {
+covap_status covap_peer_set_fused(covap_peer* p, int mode) {
   return guarded([&] {
     need(p != nullptr, "NULL peer");
-    p->fused = fused != 0;
+    need(mode >= 0 && mode <= 2, "peer mode must be 0, 1 or 2");
+    p->mode = mode;
   });
 }
 
@@ -1219,8 +1230,39 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
     const auto& ph = phase_of(s->plan, s->num_steps);
     const int par = static_cast<int>(s->num_steps & 1);
     void* buf = p->bufs[par];
+    if (p->mode == 2) {  // K1 + collective + unpack in one kernel
+      covapb::PeerStepArgs a{};
+      for (int q = 0; q < p->P; ++q) {
+        a.bufs[q] = p->peer_bufs[par][q];
+        a.flags[q] = p->peer_flags[q];
+      }
+      a.queue = p->queue;
+      a.err = p->err;
+      a.epoch = ++p->epoch;
+      a.wait_epoch = p->posted;
+      a.len = ph.send_elems;
+      a.cmax = p->cmax;
+      a.timeout_ns = p->timeout_ns;
+      a.P = p->P;
+      a.rank = p->rank;
+      a.g = grad;
+      a.r = s->residual;
+      a.out = out;
+      a.runs = s->d_runs + s->phase_off[s->num_steps % s->plan.interval];
+      a.nruns = static_cast<int>(ph.runs.size());
+      a.n_out = n;
+      a.coeff = coeff_of(s);
+      a.ef = s->ef.enabled;
+      a.inv = 1.0 / static_cast<double>(p->P);
+      need(a.len <= p->cmax * covapb::kPeerChunk, "send length exceeds the peer flag capacity");
+      CK(covapb::launch_peer_step(s->dtype, a, p->max_ctas, st));
+      p->posted = p->epoch;
+      ++s->num_steps;
+      return;
+    }
     k1_range(s, grad, buf, 0, n, st);
     ++p->epoch;
+    if (ph.send_elems > 0) p->posted = p->epoch;
     if (ph.send_elems > 0) {
       covapb::PeerArgs a{};
       for (int q = 0; q < p->P; ++q) {
@@ -1234,7 +1276,7 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
       a.timeout_ns = p->timeout_ns;
       a.P = p->P;
       a.rank = p->rank;
-      a.fused = p->fused ? 1 : 0;
+      a.fused = p->mode == 1 ? 1 : 0;
       a.out = out;
       a.runs = s->d_runs + s->phase_off[s->num_steps % s->plan.interval];
       a.nruns = static_cast<int>(ph.runs.size());
@@ -1243,7 +1285,7 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
       CK(covapb::launch_peer_allreduce(s->dtype, a, p->max_ctas, st));
     }
     // fused: the collective already wrote out (C1 + K2 in one kernel)
-    if (!(p->fused && ph.send_elems > 0))
+    if (!(p->mode == 1 && ph.send_elems > 0))
       k2_range(s, buf, out, 1.0 / static_cast<double>(p->P), 1, 0, n, st);
     ++s->num_steps;
   });

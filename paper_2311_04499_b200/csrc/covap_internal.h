@@ -80,4 +80,43 @@ struct PeerArgs {
 };
 cudaError_t launch_peer_allreduce(int dtype, const PeerArgs& args, int max_ctas, cudaStream_t s);
 
+// The whole multi-rank step as ONE kernel per rank over peer memory
+// (covap_peer.cu, peer_step_kernel): K1 packs the selected shards chunk by
+// chunk and publishes each chunk; the chunk's owner (chunk % P) sums it over
+// the P ranks in rank order as soon as every rank has published it and
+// publishes the sum; every rank unpacks each reduced chunk straight from its
+// owner into out (x 1/P) while the unselected range is filtered (r = c,
+// out = 0).  Work items are taken from one in-order queue (pack, unselected
+// tiles, reduce, unpack), so a CTA only ever waits for items already taken.
+// Flag block (uint64 per rank): [0, 8) / [8, 16) the PeerArgs phases,
+// [16, 24) step arrival, then chunk x published by rank q at
+// 24 + 8 x + q, then the reduced flag of chunk x at 24 + 8 cmax + x.
+constexpr uint64_t kPeerChunk = 16384;  // send elements per chunk
+constexpr uint64_t kPeerTile = 16384;   // layout elements per unselected tile
+constexpr uint64_t kPeerFlagBase = 3 * kMaxPeers;
+inline uint64_t peer_flag_words(uint64_t cmax) { return kPeerFlagBase + cmax * (kMaxPeers + 1); }
+struct PeerStepArgs {
+  void* bufs[kMaxPeers];
+  uint64_t* flags[kMaxPeers];
+  unsigned* queue;        // this rank's [next item, finished CTAs]
+  int* err;
+  uint64_t epoch;         // this step
+  uint64_t wait_epoch;    // every peer must have arrived at this epoch before my buffer is rewritten
+  uint64_t len;           // send elements this step
+  uint64_t cmax;          // chunk capacity of the flag block
+  uint64_t timeout_ns;
+  int P;
+  int rank;
+  const void* g;
+  void* r;
+  void* out;
+  const Run* runs;
+  int nruns;
+  uint64_t n_out;
+  double coeff;
+  int ef;
+  double inv;
+};
+cudaError_t launch_peer_step(int dtype, const PeerStepArgs& args, int max_ctas, cudaStream_t s);
+
 }  // namespace covapb

@@ -219,6 +219,240 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
   }
 }
 
+
+// ------------------------------------------------------------------ whole step
+//
+// peer_step_kernel: K1 -> rank-ordered reduce -> unpack, one launch per rank
+// (see covap_internal.h).  Every item is a 16-byte-vector pass between scalar
+// edges; selected layout elements and their send slots share alignment
+// (dst == begin mod kSendAlign).
+
+constexpr int kStepThreads = 512;
+
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T>
+__device__ __forceinline__ T ldcg(const T* p) {
+  return __ldcg(p);
+}
+
+// Spin (thread 0) until *f >= epoch; false on timeout or a peer's error.
+__device__ __forceinline__ bool wait_flag(const uint64_t* f, uint64_t epoch, uint64_t timeout_ns,
+                                          int* err) {
+  const uint64_t t0 = now_ns();
+  while (ld_acquire_sys(f) < epoch) {
+    if (*reinterpret_cast<volatile int*>(err)) return false;
+    if (now_ns() - t0 > timeout_ns) {
+      atomicExch(err, 1);
+      return false;
+    }
+  }
+  return true;
+}
+
+// Publish (thread 0, after the block's stores): flags[p][idx] = epoch on every rank.
+__device__ __forceinline__ void publish(const PeerStepArgs& A, uint64_t idx) {
+  __threadfence_system();
+  for (int p = 0; p < A.P; ++p) st_release_sys(A.flags[p] + idx, A.epoch);
+}
+
+// First run whose send range [dst, dst + len) ends after send offset o.
+__device__ __forceinline__ int run_by_send(const Run* runs, int n, uint64_t o) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (runs[mid].dst + (runs[mid].end - runs[mid].begin) > o) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// Calls f(layout e, send o, count) for the selected pieces of send [o0, o1):
+// (e, o) pairs with e == o (mod kSendAlign).
+template <typename F>
+__device__ __forceinline__ void for_send_pieces(const PeerStepArgs& A, uint64_t o0, uint64_t o1, F&& f) {
+  for (int j = run_by_send(A.runs, A.nruns, o0); j < A.nruns; ++j) {
+    const uint64_t d0 = A.runs[j].dst, d1 = d0 + (A.runs[j].end - A.runs[j].begin);
+    if (d0 >= o1) break;
+    const uint64_t a = d0 > o0 ? d0 : o0, b = d1 < o1 ? d1 : o1;
+    if (a < b) f(A.runs[j].begin + (a - d0), a, b - a);
+  }
+}
+
+// Block-wide pass over n elements starting at layout e / send o (same
+// alignment mod W): scalar(i) for the unaligned head and tail, vec(i) for
+// 16-byte vectors (i = element offset of the vector).
+template <typename T, typename S, typename Vf>
+__device__ __forceinline__ void block_pass(uint64_t e, uint64_t n, S&& scalar, Vf&& vec) {
+  constexpr uint64_t W = 16 / sizeof(T);
+  const uint64_t head = ((W - e % W) % W) < n ? (W - e % W) % W : n;
+  const uint64_t nv = (n - head) / W;
+  for (uint64_t i = threadIdx.x; i < head; i += kStepThreads) scalar(i);
+  for (uint64_t i = head + nv * W + threadIdx.x; i < n; i += kStepThreads) scalar(i);
+  for (uint64_t v = threadIdx.x; v < nv; v += kStepThreads) vec(head + v * W);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kStepThreads) peer_step_kernel(const PeerStepArgs A) {
+  using V = typename V16<T>::type;
+  constexpr uint64_t W = 16 / sizeof(T);
+  const int P = A.P, rank = A.rank;
+  const T* __restrict__ g = static_cast<const T*>(A.g);
+  T* __restrict__ r = static_cast<T*>(A.r);
+  T* __restrict__ out = static_cast<T*>(A.out);
+  T* mine = static_cast<T*>(A.bufs[rank]);
+  const T coeff = static_cast<T>(A.coeff), inv = static_cast<T>(A.inv);
+  const uint64_t rdy = kPeerFlagBase, red = kPeerFlagBase + A.cmax * kMaxPeers;
+  __shared__ int s_ok;
+  __shared__ unsigned s_item;
+
+  // Arrival: my step has started (so my previous step, and every read of
+  // the peers' buffers it made, is done).  My send buffer of this parity is
+  // rewritten only after every peer arrived at the step after the one that
+  // last read it.
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) publish(A, 2 * kMaxPeers + rank);
+    bool ok = true;
+    for (int q = 0; q < P && ok; ++q) {
+      const uint64_t* f = A.flags[rank];
+      const uint64_t t0 = now_ns();
+      while (umax(ld_acquire_sys(f + 2 * kMaxPeers + q), ld_acquire_sys(f + q)) < A.wait_epoch) {
+        if (*reinterpret_cast<volatile int*>(A.err) || now_ns() - t0 > A.timeout_ns) {
+          atomicExch(A.err, 1);
+          ok = false;
+          break;
+        }
+      }
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+
+  const uint64_t nchunks = (A.len + kPeerChunk - 1) / kPeerChunk;
+  // unselected layout ranges: the gaps between runs, cut into tiles
+  auto gap = [&](int k, uint64_t* b, uint64_t* e) {
+    *b = k == 0 ? 0 : A.runs[k - 1].end;
+    *e = k == A.nruns ? A.n_out : A.runs[k].begin;
+  };
+  uint64_t ntiles = 0;
+  for (int k = 0; k <= A.nruns; ++k) {
+    uint64_t b, e;
+    gap(k, &b, &e);
+    if (e > b) ntiles += (e - b + kPeerTile - 1) / kPeerTile;
+  }
+  const uint64_t nmine = nchunks > static_cast<uint64_t>(rank)
+                             ? (nchunks - rank + P - 1) / P : 0;  // chunks I reduce
+  const uint64_t total = nchunks + ntiles + nmine + nchunks;
+
+  while (s_ok) {
+    if (threadIdx.x == 0) s_item = atomicAdd(A.queue, 1u);
+    __syncthreads();
+    const uint64_t item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    if (item < nchunks) {
+      // ---- pack chunk: c = g + coeff*r -> my send slot, r = 0 (compress.cpp:59-77)
+      const uint64_t o0 = item * kPeerChunk, o1 = umin(A.len, o0 + kPeerChunk);
+      for_send_pieces(A, o0, o1, [&](uint64_t e, uint64_t o, uint64_t n) {
+        block_pass<T>(e, n,
+            [&](uint64_t i) {
+              const T c = A.ef ? add_rn(g[e + i], mul_rn(coeff, r[e + i])) : g[e + i];
+              mine[o + i] = c;
+              r[e + i] = T(0);
+            },
+            [&](uint64_t i) {
+              V x = *reinterpret_cast<const V*>(g + e + i);
+              if (A.ef) {
+                const V y = *reinterpret_cast<const V*>(r + e + i);
+                T* xs = reinterpret_cast<T*>(&x);
+                const T* ys = reinterpret_cast<const T*>(&y);
+#pragma unroll
+                for (int w = 0; w < static_cast<int>(W); ++w) xs[w] = add_rn(xs[w], mul_rn(coeff, ys[w]));
+              }
+              *reinterpret_cast<V*>(mine + o + i) = x;
+              *reinterpret_cast<V*>(r + e + i) = vzero<V>();
+            });
+      });
+      __syncthreads();
+      if (threadIdx.x == 0) publish(A, rdy + item * kMaxPeers + rank);
+    } else if (item < nchunks + ntiles) {
+      // ---- unselected tile: r = c (compress.cpp:79), out = 0 (compress.cpp:91)
+      uint64_t u = item - nchunks, b = 0, e = 0;
+      for (int k = 0; k <= A.nruns; ++k) {
+        gap(k, &b, &e);
+        const uint64_t t = e > b ? (e - b + kPeerTile - 1) / kPeerTile : 0;
+        if (u < t) break;
+        u -= t;
+      }
+      const uint64_t e0 = b + u * kPeerTile, n = umin(e, e0 + kPeerTile) - e0;
+      block_pass<T>(e0, n,
+          [&](uint64_t i) {
+            r[e0 + i] = A.ef ? add_rn(g[e0 + i], mul_rn(coeff, r[e0 + i])) : g[e0 + i];
+            out[e0 + i] = T(0);
+          },
+          [&](uint64_t i) {
+            V x = *reinterpret_cast<const V*>(g + e0 + i);
+            if (A.ef) {
+              const V y = *reinterpret_cast<const V*>(r + e0 + i);
+              T* xs = reinterpret_cast<T*>(&x);
+              const T* ys = reinterpret_cast<const T*>(&y);
+#pragma unroll
+              for (int w = 0; w < static_cast<int>(W); ++w) xs[w] = add_rn(xs[w], mul_rn(coeff, ys[w]));
+            }
+            *reinterpret_cast<V*>(r + e0 + i) = x;
+            *reinterpret_cast<V*>(out + e0 + i) = vzero<V>();
+          });
+    } else if (item < nchunks + ntiles + nmine) {
+      // ---- reduce a chunk I own, in rank order (trainer.cpp:41-43)
+      const uint64_t x = rank + (item - nchunks - ntiles) * P;
+      if (threadIdx.x == 0) {
+        bool ok = true;
+        for (int q = 0; q < P && ok; ++q)
+          ok = wait_flag(A.flags[rank] + rdy + x * kMaxPeers + q, A.epoch, A.timeout_ns, A.err);
+        s_ok = ok;
+      }
+      __syncthreads();
+      if (!s_ok) break;
+      const uint64_t o0 = x * kPeerChunk, o1 = umin(A.len, o0 + kPeerChunk);
+      block_pass<T>(o0, o1 - o0,
+          [&](uint64_t i) {
+            T acc = T(0);
+            for (int q = 0; q < P; ++q) acc = add_rn(acc, ldcg(static_cast<const T*>(A.bufs[q]) + o0 + i));
+            mine[o0 + i] = acc;
+          },
+          [&](uint64_t i) {
+            V acc = vzero<V>();
+            for (int q = 0; q < P; ++q)
+              acc = vadd(acc, ldcg(reinterpret_cast<const V*>(static_cast<const T*>(A.bufs[q]) + o0 + i)));
+            *reinterpret_cast<V*>(mine + o0 + i) = acc;
+          });
+      __syncthreads();
+      if (threadIdx.x == 0) publish(A, red + x);
+    } else {
+      // ---- unpack a reduced chunk from its owner: out = sum * (1/P)
+      const uint64_t x = item - nchunks - ntiles - nmine;
+      const T* src = static_cast<const T*>(A.bufs[x % P]);
+      if (threadIdx.x == 0) s_ok = wait_flag(A.flags[rank] + red + x, A.epoch, A.timeout_ns, A.err);
+      __syncthreads();
+      if (!s_ok) break;
+      const uint64_t o0 = x * kPeerChunk, o1 = umin(A.len, o0 + kPeerChunk);
+      for_send_pieces(A, o0, o1, [&](uint64_t e, uint64_t o, uint64_t n) {
+        block_pass<T>(e, n,
+            [&](uint64_t i) { out[e + i] = mul_rn(ldcg(src + o + i), inv); },
+            [&](uint64_t i) {
+              *reinterpret_cast<V*>(out + e + i) =
+                  vscale(ldcg(reinterpret_cast<const V*>(src + o + i)), inv);
+            });
+      });
+    }
+  }
+  // the last CTA out resets the queue for the next (stream-ordered) launch
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(A.queue + 1, 1u) + 1u == gridDim.x) {
+    A.queue[0] = 0u;
+    A.queue[1] = 0u;
+  }
+}
 }  // namespace
 
 cudaError_t launch_peer_allreduce(int dtype, const PeerArgs& args, int max_ctas, cudaStream_t s) {
@@ -238,6 +472,24 @@ cudaError_t launch_peer_allreduce(int dtype, const PeerArgs& args, int max_ctas,
     peer_allreduce_kernel<float><<<grid, kPeerThreads, 0, s>>>(args);
   else
     peer_allreduce_kernel<double><<<grid, kPeerThreads, 0, s>>>(args);
+  return cudaGetLastError();
+}
+
+
+cudaError_t launch_peer_step(int dtype, const PeerStepArgs& args, int max_ctas, cudaStream_t s) {
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+  // Work items come from an in-order queue, so no CTA waits for an item no
+  // running CTA has taken: any grid is deadlock-free on its own GPU.  Ranks
+  // sharing one GPU (tests) cap the grid so that they are co-resident.
+  int grid = sms * 2;
+  if (max_ctas > 0) grid = std::min(grid, max_ctas);
+  if (dtype == 0)
+    peer_step_kernel<float><<<grid, kStepThreads, 0, s>>>(args);
+  else
+    peer_step_kernel<double><<<grid, kStepThreads, 0, s>>>(args);
   return cudaGetLastError();
 }
 

@@ -453,7 +453,7 @@ def _virtual_ranks(covap, plan, P, dtype, ef, fused=True):
     return states, groups, streams
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["fused", "gather"])
+@pytest.mark.parametrize("fused", [1, 0, 2], ids=["fused", "gather", "step"])
 @pytest.mark.parametrize("case", manifest()["session"], ids=lambda c: c["name"])
 def test_peer_collective_bit_exact_vs_reference(covap, orc, case, fused):
     """The NVLink load/store allreduce sums in rank order, so the whole
@@ -482,9 +482,11 @@ def test_peer_collective_bit_exact_vs_reference(covap, orc, case, fused):
         assert np.array_equal(bits(states[0].residuals.cpu().numpy()), bits(fx[f"residual0_{s}"]))
 
 
-@pytest.mark.parametrize("name,K,P,fused", [("resnet50", 4, 2, True), ("vgg16", 4, 4, True),
-                                            ("resnet50", 1, 8, True), ("vgg16", 3, 3, False),
-                                            ("tablev", 19, 2, True)])
+@pytest.mark.parametrize("name,K,P,fused", [("resnet50", 4, 2, 1), ("vgg16", 4, 4, 1),
+                                            ("resnet50", 1, 8, 1), ("vgg16", 3, 3, 0),
+                                            ("tablev", 19, 2, 1), ("resnet50", 4, 2, 2),
+                                            ("vgg16", 4, 4, 2), ("resnet50", 8, 3, 2),
+                                            ("resnet50", 1, 8, 2), ("tablev", 19, 2, 2)])
 def test_peer_collective_fp32_full_layouts(covap, orc, name, K, P, fused):
     """fp32 at BASELINE sizes, P virtual ranks: every rank's synchronised
     gradient equals the rank-ordered oracle mean, bit for bit."""
@@ -495,7 +497,9 @@ def test_peer_collective_fp32_full_layouts(covap, orc, name, K, P, fused):
     tensors = [(t.bucket, t.begin, t.end) for t in plan.tensors]
     rs = [np.zeros(d, np.float32) for _ in range(P)]
     outs = [torch.empty(d, device=DEV) for _ in range(P)]
-    for s in range(2):
+    # K = 8 walks every phase, the empty ones (ResNet-50 phases 5-7) included,
+    # and reuses each parity buffer several times
+    for s in range(K + 1 if K == 8 else 3):
         keys = [orc.stream_key(9, w, s) for w in range(P)]
         grads = [dev_gen(covap, k, d, 0, torch.float32) for k in keys]
         torch.cuda.synchronize()
