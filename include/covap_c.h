@@ -307,7 +307,7 @@ covap_status covap_peer_set_limits(covap_peer* peer, int max_ctas, double timeou
  *   0            K1, collective with an all-gather into the local send
  *                buffer, then K2;
  *   2            the whole step as ONE kernel per rank: K1 packs the send
- *                buffer chunk by chunk (16 Ki elements) and publishes each
+ *                buffer chunk by chunk (32 Ki elements) and publishes each
  *                chunk; the chunk's owner (chunk mod P) reduces it in rank
  *                order as soon as every rank published it; every rank
  *                unpacks each reduced chunk from its owner as soon as it is

@@ -91,8 +91,8 @@ cudaError_t launch_peer_allreduce(int dtype, const PeerArgs& args, int max_ctas,
 // Flag block (uint64 per rank): [0, 8) / [8, 16) the PeerArgs phases,
 // [16, 24) step arrival, then chunk x published by rank q at
 // 24 + 8 x + q, then the reduced flag of chunk x at 24 + 8 cmax + x.
-constexpr uint64_t kPeerChunk = 16384;  // send elements per chunk
-constexpr uint64_t kPeerTile = 16384;   // layout elements per unselected tile
+constexpr uint64_t kPeerChunk = 32768;  // send elements per chunk
+constexpr uint64_t kPeerTile = 32768;   // layout elements per unselected tile
 constexpr uint64_t kPeerFlagBase = 3 * kMaxPeers;
 inline uint64_t peer_flag_words(uint64_t cmax) { return kPeerFlagBase + cmax * (kMaxPeers + 1); }
 struct PeerStepArgs {

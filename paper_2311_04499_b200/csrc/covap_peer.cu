@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
 // edges; selected layout elements and their send slots share alignment
 // (dst == begin mod kSendAlign).
 
-constexpr int kStepThreads = 512;
+constexpr int kStepThreads = 256;
 
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
@@ -280,20 +280,41 @@ __device__ __forceinline__ void for_send_pieces(const PeerStepArgs& A, uint64_t 
 }
 
 // Block-wide pass over n elements starting at layout e / send o (same
-// alignment mod W): scalar(i) for the unaligned head and tail, vec(i) for
-// 16-byte vectors (i = element offset of the vector).
-template <typename T, typename S, typename Vf>
-__device__ __forceinline__ void block_pass(uint64_t e, uint64_t n, S&& scalar, Vf&& vec) {
+// alignment mod W): scalar(i) for the unaligned head and tail; for the
+// 16-byte vectors, load(i) then store(i, loaded) with kBatch vectors per
+// thread loaded before any is stored, so each thread keeps several loads in
+// flight (the pass is latency-bound otherwise: one CTA walks one chunk).
+constexpr int kBatch = 4;
+template <typename T, typename S, typename Ld, typename St>
+__device__ __forceinline__ void block_pass(uint64_t e, uint64_t n, S&& scalar, Ld&& load, St&& store) {
   constexpr uint64_t W = 16 / sizeof(T);
   const uint64_t head = ((W - e % W) % W) < n ? (W - e % W) % W : n;
   const uint64_t nv = (n - head) / W;
   for (uint64_t i = threadIdx.x; i < head; i += kStepThreads) scalar(i);
   for (uint64_t i = head + nv * W + threadIdx.x; i < n; i += kStepThreads) scalar(i);
-  for (uint64_t v = threadIdx.x; v < nv; v += kStepThreads) vec(head + v * W);
+  using X = decltype(load(uint64_t(0)));
+  for (uint64_t v0 = 0; v0 < nv; v0 += kBatch * kStepThreads) {
+    X x[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint64_t v = v0 + q * kStepThreads + threadIdx.x;
+      if (v < nv) x[q] = load(head + v * W);
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint64_t v = v0 + q * kStepThreads + threadIdx.x;
+      if (v < nv) store(head + v * W, x[q]);
+    }
+  }
 }
 
+template <typename V>
+struct Pair {
+  V a, b;
+};
+
 template <typename T>
-__global__ void __launch_bounds__(kStepThreads) peer_step_kernel(const PeerStepArgs A) {
+__global__ void __launch_bounds__(kStepThreads, 2) peer_step_kernel(const PeerStepArgs A) {
   using V = typename V16<T>::type;
   constexpr uint64_t W = 16 / sizeof(T);
   const int P = A.P, rank = A.rank;
@@ -344,8 +365,14 @@ __global__ void __launch_bounds__(kStepThreads) peer_step_kernel(const PeerStepA
                              ? (nchunks - rank + P - 1) / P : 0;  // chunks I reduce
   const uint64_t total = nchunks + ntiles + nmine + nchunks;
 
+  // thread 0 takes the next item while the block works on the current one
+  unsigned next = 0;
+  if (threadIdx.x == 0) next = atomicAdd(A.queue, 1u);
   while (s_ok) {
-    if (threadIdx.x == 0) s_item = atomicAdd(A.queue, 1u);
+    if (threadIdx.x == 0) {
+      s_item = next;
+      if (next < total) next = atomicAdd(A.queue, 1u);
+    }
     __syncthreads();
     const uint64_t item = s_item;
     __syncthreads();
@@ -361,15 +388,19 @@ __global__ void __launch_bounds__(kStepThreads) peer_step_kernel(const PeerStepA
               r[e + i] = T(0);
             },
             [&](uint64_t i) {
-              V x = *reinterpret_cast<const V*>(g + e + i);
+              Pair<V> x;
+              x.a = *reinterpret_cast<const V*>(g + e + i);
+              x.b = A.ef ? *reinterpret_cast<const V*>(r + e + i) : vzero<V>();
+              return x;
+            },
+            [&](uint64_t i, Pair<V> x) {
+              T* xs = reinterpret_cast<T*>(&x.a);
+              const T* ys = reinterpret_cast<const T*>(&x.b);
               if (A.ef) {
-                const V y = *reinterpret_cast<const V*>(r + e + i);
-                T* xs = reinterpret_cast<T*>(&x);
-                const T* ys = reinterpret_cast<const T*>(&y);
 #pragma unroll
                 for (int w = 0; w < static_cast<int>(W); ++w) xs[w] = add_rn(xs[w], mul_rn(coeff, ys[w]));
               }
-              *reinterpret_cast<V*>(mine + o + i) = x;
+              *reinterpret_cast<V*>(mine + o + i) = x.a;
               *reinterpret_cast<V*>(r + e + i) = vzero<V>();
             });
       });
@@ -391,15 +422,19 @@ __global__ void __launch_bounds__(kStepThreads) peer_step_kernel(const PeerStepA
             out[e0 + i] = T(0);
           },
           [&](uint64_t i) {
-            V x = *reinterpret_cast<const V*>(g + e0 + i);
+            Pair<V> x;
+            x.a = *reinterpret_cast<const V*>(g + e0 + i);
+            x.b = A.ef ? *reinterpret_cast<const V*>(r + e0 + i) : vzero<V>();
+            return x;
+          },
+          [&](uint64_t i, Pair<V> x) {
+            T* xs = reinterpret_cast<T*>(&x.a);
+            const T* ys = reinterpret_cast<const T*>(&x.b);
             if (A.ef) {
-              const V y = *reinterpret_cast<const V*>(r + e0 + i);
-              T* xs = reinterpret_cast<T*>(&x);
-              const T* ys = reinterpret_cast<const T*>(&y);
 #pragma unroll
               for (int w = 0; w < static_cast<int>(W); ++w) xs[w] = add_rn(xs[w], mul_rn(coeff, ys[w]));
             }
-            *reinterpret_cast<V*>(r + e0 + i) = x;
+            *reinterpret_cast<V*>(r + e0 + i) = x.a;
             *reinterpret_cast<V*>(out + e0 + i) = vzero<V>();
           });
     } else if (item < nchunks + ntiles + nmine) {
@@ -424,8 +459,9 @@ __global__ void __launch_bounds__(kStepThreads) peer_step_kernel(const PeerStepA
             V acc = vzero<V>();
             for (int q = 0; q < P; ++q)
               acc = vadd(acc, ldcg(reinterpret_cast<const V*>(static_cast<const T*>(A.bufs[q]) + o0 + i)));
-            *reinterpret_cast<V*>(mine + o0 + i) = acc;
-          });
+            return acc;
+          },
+          [&](uint64_t i, V acc) { *reinterpret_cast<V*>(mine + o0 + i) = acc; });
       __syncthreads();
       if (threadIdx.x == 0) publish(A, red + x);
     } else {
@@ -439,10 +475,8 @@ __global__ void __launch_bounds__(kStepThreads) peer_step_kernel(const PeerStepA
       for_send_pieces(A, o0, o1, [&](uint64_t e, uint64_t o, uint64_t n) {
         block_pass<T>(e, n,
             [&](uint64_t i) { out[e + i] = mul_rn(ldcg(src + o + i), inv); },
-            [&](uint64_t i) {
-              *reinterpret_cast<V*>(out + e + i) =
-                  vscale(ldcg(reinterpret_cast<const V*>(src + o + i)), inv);
-            });
+            [&](uint64_t i) { return ldcg(reinterpret_cast<const V*>(src + o + i)); },
+            [&](uint64_t i, V x) { *reinterpret_cast<V*>(out + e + i) = vscale(x, inv); });
       });
     }
   }
@@ -484,7 +518,7 @@ cudaError_t launch_peer_step(int dtype, const PeerStepArgs& args, int max_ctas, 
   // Work items come from an in-order queue, so no CTA waits for an item no
   // running CTA has taken: any grid is deadlock-free on its own GPU.  Ranks
   // sharing one GPU (tests) cap the grid so that they are co-resident.
-  int grid = sms * 2;
+  int grid = sms * 4;
   if (max_ctas > 0) grid = std::min(grid, max_ctas);
   if (dtype == 0)
     peer_step_kernel<float><<<grid, kStepThreads, 0, s>>>(args);
