@@ -18,11 +18,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "covap_capi_common.hpp"
 #include "covap_feedback.h"
+#include "covap_internal.h"
 #include "covap_plan.hpp"
 
 namespace fb = covapb::fb;
@@ -205,8 +207,15 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       CK(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
       CK(fb::launch_randomk_select(a, f->sms, f->side));
       CK(cudaEventRecord(f->ev_join, f->side));
-      CK(fb::launch_compensate(dt, grad, f->residual, zero, nullptr, f->chunks, f->nchunks,
-                               f->ef.enabled, coeff, f->sms, st));
+      // No histogram is needed, so the compensation pass is the TMA-bulk
+      // filter pass with an empty selection (r = c, zero-filled output):
+      // covap_kernels.cu's K1F / K1 pipeline, 0.9-1.0 of the copy peak.
+      if (zero)
+        CK(covapb::launch_filter_unpack(dt, grad, f->residual, zero, nullptr, 0, 0, f->total, coeff,
+                                        f->ef.enabled, 1.0, st));
+      else
+        CK(covapb::launch_filter_pack(dt, grad, f->residual, nullptr, nullptr, 0, 0, f->total, coeff,
+                                      f->ef.enabled, st));
       CK(cudaStreamWaitEvent(st, f->ev_join, 0));
       CK(fb::launch_randomk_gather(dt, a, f->residual, kept, kept_mean ? 1 : 0, f->list_idx,
                                    f->list_val, f->sms,
@@ -460,6 +469,8 @@ covap_status covap_feedback_reset(covap_feedback* f, void* stream) {
 covap_status covap_feedback_step(covap_feedback* f, const void* grad, void* kept, void* stream) {
   return guarded([&] {
     need(f && grad && kept, "NULL argument");
+    need_aligned(grad, "grad");
+    need_aligned(kept, "kept");
     DeviceGuard dg(f->device);
     ef_step(f, grad, kept, kept, false, as_stream(stream));
   });
@@ -511,6 +522,8 @@ covap_status covap_feedback_pack(covap_feedback* f, const void* grad, void* out,
   return guarded([&] {
     need(f && grad, "NULL argument");
     need(!sparse(f) || out != nullptr, "out must not be NULL for the sparse filters");
+    need_aligned(grad, "grad");
+    if (out) need_aligned(out, "out");
     need(f->filter.kind >= COVAP_FILTER_TOPK, "the identity / covap filters have no sync wire");
     DeviceGuard dg(f->device);
     ef_step(f, grad, nullptr, sparse(f) ? out : nullptr, true, as_stream(stream));
@@ -538,6 +551,8 @@ covap_status covap_feedback_sync_step(covap_feedback* f, covap_comm* comm, const
                                       void* out, void* stream) {
   return guarded([&] {
     need(f && grad && out, "NULL argument");
+    need_aligned(grad, "grad");
+    need_aligned(out, "out");
     need(f->filter.kind >= COVAP_FILTER_TOPK,
          "the identity / covap filters have no sync wire (use covap_sync_step)");
     DeviceGuard dg(f->device);
