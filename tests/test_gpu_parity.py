@@ -307,6 +307,45 @@ def test_full_size_integer_conservation(covap, name, K):
     assert torch.equal(sent + sync.state.residuals, inp)
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["k1f", "k1_k2"])
+def test_beyond_2pow32_elements(covap, fused):
+    """Maximum sizes: a 2-bucket layout of 2^31 + 7 and 2^31 + 5 fp32
+    elements (> 2^32 in total, 17 GB per array) at K = 2, integer gradients,
+    coeff = 1.  Element by element, out + r_new == g + r_old (exact in fp32
+    for integers), out is zero outside the selected bucket and r is zero
+    inside it — so no 32-bit index wraps anywhere in K1F, K1 or K2."""
+    free, _ = torch.cuda.mem_get_info()
+    sizes = [(1 << 31) + 7, (1 << 31) + 5]
+    d = sum(sizes)
+    if free < 7 * 4 * d:
+        pytest.skip("needs ~120 GB of free device memory")
+    plan = covap.BucketPlan(mk_model(covap, sizes, 1), interval=2)
+    assert plan.total_numel() == d and len(plan.tensors) == 2
+    sync = covap.CovapSync(plan, None, torch.float32, 0, covap.EfSchedule(True, 1.0, 1, 0.0),
+                           fuse_single_rank=fused)
+    g = torch.empty(d, device=DEV)
+    out = torch.empty(d, device=DEV)
+    b0 = plan.tensors[1].begin
+    for s in range(3):
+        covap.generate(g, covap.stream_key(5, 0, s), 1)
+        r_old = sync.state.residuals.clone()
+        sync.sync(g, out)
+        r_new = sync.state.residuals
+        sel = (0, b0) if s % 2 == 0 else (b0, d)
+        step = 1 << 28
+        for a in range(0, d, step):  # chunked: bounded temporaries
+            e = min(d, a + step)
+            assert torch.equal(out[a:e] + r_new[a:e], g[a:e] + r_old[a:e]), (s, a)
+            lo, hi = max(a, sel[0]), min(e, sel[1])
+            if lo < hi:
+                assert not torch.any(r_new[lo:hi]), (s, a)
+            for x0, x1 in ((a, min(e, sel[0])), (max(a, sel[1]), e)):
+                if x0 < x1:
+                    assert not torch.any(out[x0:x1]), (s, a)
+        del r_old
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 3), ("tablev", 19), ("resnet50", 1)])
 def test_fused_single_rank_pass_equals_k1_k2(covap, dtype, name, K):
