@@ -148,9 +148,14 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
   const double coeff = coeff_of(f);
   const uint32_t nt = static_cast<uint32_t>(f->numel.size());
   switch (f->filter.kind) {
+    case COVAP_FILTER_FP16:
+      // the TMA-bulk filter pass (covap_kernels.cu, op 5)
+      CK(covapb::launch_filter_fp16(dt, grad, f->residual, kept, kept_mean ? 1 : 0,
+                                    wire ? f->half : nullptr, f->d_sat, f->total, coeff,
+                                    f->ef.enabled, st));
+      break;
     case COVAP_FILTER_IDENTITY:
-    case COVAP_FILTER_COVAP:
-    case COVAP_FILTER_FP16: {
+    case COVAP_FILTER_COVAP: {
       fb::DenseArgs a{};
       a.g = grad;
       a.r = f->residual;

@@ -36,6 +36,14 @@ cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, c
 cudaError_t launch_filter_sgd(int dtype, const void* g, void* r, void* params, const Run* runs,
                               int nruns, uint64_t a, uint64_t b, double coeff, int ef, double inv,
                               double lr, cudaStream_t s);
+// The reference's Fp16Filter under error feedback (compress.cpp:300-309,
+// 323-344) as a TMA-bulk filter pass over [0, n): c = g + coeff*r; h = half
+// bits of c (with the reference's NaN / saturation / underflow rules); kept =
+// widen(h) -> kept (as (0 + kept) when kept_mean), r = c - kept, h -> wire;
+// kept and wire may be NULL; sat counts saturated values.  wire 16-byte aligned.
+cudaError_t launch_filter_fp16(int dtype, const void* g, void* r, void* kept, int kept_mean,
+                              uint16_t* wire, unsigned long long* sat, uint64_t n, double coeff,
+                              int ef, cudaStream_t s);
 // K2 + SGD: selected -> params -= lr * f(recv); unselected untouched.
 cudaError_t launch_unpack_sgd(int dtype, const void* recv, void* params, const Run* runs,
                               int nruns, uint64_t a, uint64_t b, double inv, int mean, double lr,

@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <mutex>
 
+#include "covap_half.cuh"
 #include "covap_internal.h"
 
 namespace covapb {
@@ -70,6 +71,10 @@ constexpr uint32_t kTileK1 = COVAP_K1_TILE;
 constexpr int kStages = COVAP_K1_STAGES;
 constexpr uint32_t kSmemK1 = (2 * kStages + 3) * kTileK1;
 constexpr uint32_t kSmemK1Sgd = (3 * kStages + 3) * kTileK1;
+// K1 fp16 (the reference's Fp16Filter under error feedback): per staging
+// buffer a residual tile, a kept tile and the tile's fp16 wire halves.
+constexpr uint32_t kStageFp16 = 2 * kTileK1 + kTileK1 / 2;
+constexpr uint32_t kSmemK1Fp16 = 2 * kStages * kTileK1 + 2 * kStageFp16;
 // K2: kStagesK2 recv slots + 2 staging tiles + 1 zero tile; K2+SGD adds a
 // params tile per slot.
 constexpr uint32_t kTileK2 = COVAP_K2_TILE;
@@ -238,6 +243,8 @@ struct Args {
   int mean;        // K2: allreduce_mean semantics
   T lr;            // SGD variants: learning rate
   uint64_t te;     // elements per tile of this launch (set by the launcher)
+  uint16_t* wire;  // fp16 (op 5): half bits of the kept values, or NULL
+  unsigned long long* sat;  // fp16: saturation count (compress.cpp:185-190), or NULL
 };
 
 // Operations of the element path / the filter kernel:
@@ -251,8 +258,29 @@ __device__ __forceinline__ T sgd(T p, T lr, T u) {
   return sub_rn(p, mul_rn(lr, u));
 }
 
+// fp16 filter of one compensated value (compress.cpp:300-309, 339-341): wire
+// bits h, kept value (half widened back), residual c - kept.
+template <typename T>
+__device__ __forceinline__ T fp16_keep(T c, uint16_t& h, unsigned& nsat) {
+  bool s = false;
+  h = half_bits(static_cast<float>(c), s);
+  nsat += s ? 1u : 0u;
+  return static_cast<T>(half_to_float(h));
+}
+
 template <typename T, int OP>
 __device__ __forceinline__ void element(const Args<T>& A, int& j, uint64_t e, T gv, T rv) {
+  if (OP == 5) {
+    const T c = A.ef ? add_rn(gv, mul_rn(A.coeff, rv)) : gv;
+    uint16_t h;
+    unsigned ns = 0;
+    const T k = fp16_keep(c, h, ns);
+    A.r[e] = sub_rn(c, k);
+    if (A.out) A.out[e] = A.mean ? add_rn(T(0), k) : k;
+    if (A.wire) A.wire[e] = h;
+    if (ns && A.sat) atomicAdd(A.sat, 1ull);
+    return;
+  }
   const int k = run_at(A.runs, A.nruns, j, e);
   if (OP == 2 || OP == 4) {
     if (k < 0) {
@@ -281,7 +309,7 @@ __device__ __forceinline__ void element(const Args<T>& A, int& j, uint64_t e, T 
 // Elements [a, a16) and [b16, b) that do not fill a 16-byte vector.
 template <typename T, int OP>
 __device__ void edges(const Args<T>& A, uint64_t a16, uint64_t b16) {
-  constexpr bool reads_g = OP == 0 || OP == 1 || OP == 3;
+  constexpr bool reads_g = OP == 0 || OP == 1 || OP == 3 || OP == 5;
   for (uint64_t e = A.a + threadIdx.x; e < a16; e += blockDim.x) {
     int j = first_run_after(A.runs, A.nruns, e);
     element<T, OP>(A, j, e, reads_g ? A.g[e] : T(0), (reads_g && A.ef) ? A.r[e] : T(0));
@@ -306,9 +334,16 @@ constexpr int k1_slot_tiles() {
   return OP == 3 ? 3 : 2;
 }
 
+template <int OP>
+__host__ __device__ constexpr int filter_threads() {
+  return OP == 5 ? 512 : kThreads;  // fp16: conversion-heavy, more warps per SM
+}
+
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
-  static_assert(OP == 0 || OP == 1 || OP == 3, "filter_kernel ops: 0 pack, 1 K1F, 3 K1F+SGD");
+__global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const Args<T> A) {
+  constexpr int NT = filter_threads<OP>();
+  static_assert(OP == 0 || OP == 1 || OP == 3 || OP == 5,
+                "filter_kernel ops: 0 pack, 1 K1F, 3 K1F+SGD, 5 fp16 filter");
   constexpr uint32_t TE = kTileK1 / sizeof(T);  // elements per tile
   using V = typename Vec16<T>::type;
   constexpr uint32_t W = 16 / sizeof(T);
@@ -336,7 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
   const uint64_t te = A.te;  // balanced tile (<= TE): every CTA gets the same tile count
   const uint64_t ntiles = (b16 - a16 + te - 1) / te;
   const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  for (uint32_t i = threadIdx.x; i < TE; i += kThreads) zero[i] = T(0);
+  if (OP != 5)
+    for (uint32_t i = threadIdx.x; i < TE; i += NT) zero[i] = T(0);
+  unsigned nsat = 0;  // fp16: saturated values of this thread
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&bar[i]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -373,6 +410,55 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
     if (threadIdx.x == 0) bulk_wait_read<1>();  // staging tile (k & 1) free again
     mbar_wait(&bar[s], static_cast<uint32_t>((k / kStages) & 1));
     __syncthreads();
+    if (OP == 5) {
+      // fp16 filter: every element is kept as its half (no selection);
+      // residual, kept and wire tiles leave with bulk stores.
+      unsigned char* sb = smem + 2 * kStages * kTileK1 + (k & 1) * kStageFp16;
+      T* sr = reinterpret_cast<T*>(sb);
+      T* sk = reinterpret_cast<T*>(sb + kTileK1);
+      uint16_t* sw = reinterpret_cast<uint16_t*>(sb + 2 * kTileK1);
+      const V* gv = reinterpret_cast<const V*>(gs);
+      const V* rv = reinterpret_cast<const V*>(rs);
+      for (uint32_t v = threadIdx.x; v < n / W; v += NT) {
+        V x = gv[v];
+        if (A.ef) {
+          const V y = rv[v];
+#pragma unroll
+          for (int q = 0; q < static_cast<int>(W); ++q)
+            lane(x, q) = add_rn(lane(x, q), mul_rn(A.coeff, lane(y, q)));
+        }
+        V res, kv;
+        uint16_t h[W];
+#pragma unroll
+        for (int q = 0; q < static_cast<int>(W); ++q) {
+          const T kq = fp16_keep(lane(x, q), h[q], nsat);
+          lane(res, q) = sub_rn(lane(x, q), kq);
+          lane(kv, q) = A.mean ? add_rn(T(0), kq) : kq;
+        }
+        reinterpret_cast<V*>(sr)[v] = res;
+        reinterpret_cast<V*>(sk)[v] = kv;
+        if (W == 4)
+          reinterpret_cast<uint2*>(sw)[v] =
+              make_uint2(h[0] | (uint32_t(h[1 % W]) << 16), h[2 % W] | (uint32_t(h[3 % W]) << 16));
+        else
+          reinterpret_cast<uint32_t*>(sw)[v] = h[0] | (uint32_t(h[1 % W]) << 16);
+      }
+      fence_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = n * sizeof(T);
+        bulk_store(A.r + e0, sr, bytes);
+        if (A.out) bulk_store(A.out + e0, sk, bytes);
+        if (A.wire) {  // 16-byte multiple by bulk store, the rest by thread 0
+          const uint32_t wb = n * 2, wb16 = wb / 16 * 16;
+          if (wb16) bulk_store(A.wire + e0, sw, wb16);
+          for (uint32_t i = wb16 / 2; i < n; ++i) A.wire[e0 + i] = sw[i];
+        }
+        bulk_commit();
+        if (k + kStages < my) issue(k + kStages);
+      }
+      continue;
+    }
     if (sel.cls != kMixed) {
       // 16-byte vectors: a warp touches 512 contiguous bytes, no bank conflicts
       const bool full = sel.cls == kFull;
@@ -380,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
       const V* rv = reinterpret_cast<const V*>(rs);
       const V* pv = reinterpret_cast<const V*>(ps);
       V* sv = reinterpret_cast<V*>(st);
-      for (uint32_t v = threadIdx.x; v < n / W; v += kThreads) {
+      for (uint32_t v = threadIdx.x; v < n / W; v += NT) {
         V x = gv[v];
         if (A.ef) {
           const V y = rv[v];
@@ -429,9 +515,9 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
           }
         };
         const uint64_t body = vec_ok ? nv : 0;
-        for (uint64_t i = threadIdx.x; i < head; i += kThreads) one(i);
-        for (uint64_t i = head + body * W + threadIdx.x; i < len; i += kThreads) one(i);
-        for (uint64_t v = threadIdx.x; v < body; v += kThreads) {
+        for (uint64_t i = threadIdx.x; i < head; i += NT) one(i);
+        for (uint64_t i = head + body * W + threadIdx.x; i < len; i += NT) one(i);
+        for (uint64_t v = threadIdx.x; v < body; v += NT) {
           const uint64_t i = head + v * W, e = pos + i;
           V x = *reinterpret_cast<const V*>(gs + i0 + i);
           if (A.ef) {
@@ -483,6 +569,10 @@ __global__ void __launch_bounds__(kThreads, 1) filter_kernel(const Args<T> A) {
     }
   }
   if (threadIdx.x == 0) bulk_wait_all();
+  if (OP == 5 && A.sat) {
+    for (int o = 16; o > 0; o >>= 1) nsat += __shfl_xor_sync(0xffffffffu, nsat, o);
+    if ((threadIdx.x & 31) == 0 && nsat) atomicAdd(A.sat, static_cast<unsigned long long>(nsat));
+  }
 }
 
 // ------------------------------------------------------------ K2 / K2+SGD
@@ -800,6 +890,8 @@ cudaError_t shape(DeviceShape** out) {
         (e = opt_in(filter_kernel<double, 0>, kSmemK1)) ||
         (e = opt_in(filter_kernel<double, 1>, kSmemK1)) ||
         (e = opt_in(filter_kernel<double, 3>, kSmemK1Sgd)) ||
+        (e = opt_in(filter_kernel<float, 5>, kSmemK1Fp16)) ||
+        (e = opt_in(filter_kernel<double, 5>, kSmemK1Fp16)) ||
         (e = opt_in(unpack_kernel<float, false>, kSmemK2)) ||
         (e = opt_in(unpack_kernel<float, true>, kSmemK2Sgd)) ||
         (e = opt_in(unpack_kernel<double, false>, kSmemK2)) ||
@@ -850,6 +942,8 @@ Args<T> make_args(const void* g, void* r, void* send, void* out, const void* rec
   A.mean = mean;
   A.lr = static_cast<T>(lr);
   A.te = 0;  // set by balance()
+  A.wire = nullptr;
+  A.sat = nullptr;
   return A;
 }
 
@@ -857,10 +951,10 @@ Args<T> make_args(const void* g, void* r, void* send, void* out, const void* rec
 // kernel may start while the previous kernel in the stream drains.
 template <typename T>
 cudaError_t launch(void (*kernel)(const Args<T>), unsigned grid, unsigned smem, cudaStream_t s,
-                   const Args<T>& args) {
+                   const Args<T>& args, unsigned threads = kThreads) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -880,10 +974,12 @@ cudaError_t pass(int op, const Args<T>& A, cudaStream_t s) {
   DeviceShape* sh;
   cudaError_t e = shape(&sh);
   if (e) return e;
-  const bool k1 = op == 0 || op == 1 || op == 3;
+  const bool k1 = op == 0 || op == 1 || op == 3 || op == 5;
   Args<T> B = A;
   const unsigned grid = balance<T>(A.a, A.b, sh->sms, k1 ? kTileK1 : kTileK2, &B.te);
+  if (op == 5) B.te = (B.te + 7) / 8 * 8;  // wire tiles: 16-byte multiples of halves
   switch (op) {
+    case 5: return launch(filter_kernel<T, 5>, grid, kSmemK1Fp16, s, B, filter_threads<5>());
     case 0: return launch(filter_kernel<T, 0>, grid, kSmemK1, s, B);
     case 1: return launch(filter_kernel<T, 1>, grid, kSmemK1, s, B);
     case 3: return launch(filter_kernel<T, 3>, grid, kSmemK1Sgd, s, B);
@@ -930,6 +1026,20 @@ cudaError_t launch_unpack_sgd(int dtype, const void* recv, void* params, const R
                               cudaStream_t s) {
   return pass_dt(dtype, 4, s, nullptr, nullptr, nullptr, params, recv, runs, nruns, a, b, 0.0, 0,
                  inv, mean, lr);
+}
+
+cudaError_t launch_filter_fp16(int dtype, const void* g, void* r, void* kept, int kept_mean,
+                              uint16_t* wire, unsigned long long* sat, uint64_t n, double coeff,
+                              int ef, cudaStream_t s) {
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    Args<T> A = make_args<T>(g, r, nullptr, kept, nullptr, nullptr, 0, 0, n, coeff, ef, 1.0,
+                             kept_mean, 0.0);
+    A.wire = wire;
+    A.sat = sat;
+    return pass<T>(5, A, s);
+  };
+  return dtype == 0 ? go(float(0)) : go(double(0));
 }
 
 cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,
