@@ -61,6 +61,9 @@ namespace {
 #ifndef COVAP_K2_TILE
 #define COVAP_K2_TILE 32768
 #endif
+#ifndef COVAP_FILTER_THREADS  // threads per CTA of the K1 / K1F / K1F+SGD passes
+#define COVAP_FILTER_THREADS 256
+#endif
 #ifndef COVAP_PDL  // programmatic dependent launch between consecutive sync kernels
 #define COVAP_PDL 1
 #endif
@@ -336,7 +339,7 @@ constexpr int k1_slot_tiles() {
 
 template <int OP>
 __host__ __device__ constexpr int filter_threads() {
-  return OP == 5 ? 512 : kThreads;  // fp16: conversion-heavy, more warps per SM
+  return OP == 5 ? 512 : COVAP_FILTER_THREADS;  // fp16: conversion-heavy, more warps per SM
 }
 
 template <typename T, int OP>
@@ -980,9 +983,9 @@ cudaError_t pass(int op, const Args<T>& A, cudaStream_t s) {
   if (op == 5) B.te = (B.te + 7) / 8 * 8;  // wire tiles: 16-byte multiples of halves
   switch (op) {
     case 5: return launch(filter_kernel<T, 5>, grid, kSmemK1Fp16, s, B, filter_threads<5>());
-    case 0: return launch(filter_kernel<T, 0>, grid, kSmemK1, s, B);
-    case 1: return launch(filter_kernel<T, 1>, grid, kSmemK1, s, B);
-    case 3: return launch(filter_kernel<T, 3>, grid, kSmemK1Sgd, s, B);
+    case 0: return launch(filter_kernel<T, 0>, grid, kSmemK1, s, B, filter_threads<0>());
+    case 1: return launch(filter_kernel<T, 1>, grid, kSmemK1, s, B, filter_threads<1>());
+    case 3: return launch(filter_kernel<T, 3>, grid, kSmemK1Sgd, s, B, filter_threads<3>());
     case 2: return launch(unpack_kernel<T, false>, grid, kSmemK2, s, B);
     default: return launch(unpack_kernel<T, true>, grid, kSmemK2Sgd, s, B);
   }
