@@ -158,6 +158,12 @@ covap_status covap_state_set_step(covap_state* state, uint64_t num_steps);
  * (NCCL over the 1-rank communicator when one is given) -> K2 instead, the
  * exact multi-rank code path — used to test that path on one GPU. */
 covap_status covap_state_set_fused(covap_state* state, int fuse_single_rank);
+/* Multi-rank covap_sync_step (P > 1, or one rank with fusion off): run it as
+ * `groups` consecutive bucket groups of about N / groups elements, each
+ * group's allreduce on the state's comm stream overlapping K1 of the later
+ * groups and followed by its own K2.  1 (default) = one K1, one allreduce,
+ * one K2.  Results are identical either way. */
+covap_status covap_state_set_pipeline(covap_state* state, int groups);
 /* covap_sync_step_host's chunk schedule: chunks ramp geometrically from
  * ramp_min_elems (>= 8192) up to the body chunk at both ends (default 1 Mi). */
 covap_status covap_state_set_host_ramp(covap_state* state, uint64_t ramp_min_elems);

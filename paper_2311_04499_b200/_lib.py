@@ -79,6 +79,7 @@ _SIGS = {
     "covap_state_set_step": (None, [vp, u64]),
     "covap_state_set_fused": (None, [vp, i32]),
     "covap_state_set_host_ramp": (None, [vp, u64]),
+    "covap_state_set_pipeline": (None, [vp, i32]),
     "covap_state_reset": (None, [vp, vp]),
     "covap_filter_pack": (None, [vp, vp, vp, sz, sz, vp]),
     "covap_unpack": (None, [vp, vp, vp, f64, i32, sz, sz, vp]),

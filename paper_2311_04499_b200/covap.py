@@ -408,6 +408,11 @@ class CompressorState:
         """One rank: fused K1F pass (default) or the multi-rank K1 -> C1 -> K2 path."""
         L.lib().covap_state_set_fused(self._h, 1 if fuse_single_rank else 0)
 
+    def set_pipeline(self, groups: int):
+        """Multi-rank sync step as `groups` bucket groups whose allreduces
+        overlap the later groups' K1 (1 = serial)."""
+        L.lib().covap_state_set_pipeline(self._h, int(groups))
+
     def set_host_ramp(self, ramp_min_elems: int):
         """Smallest chunk of sync_host's geometric ramp at both ends of the step."""
         L.lib().covap_state_set_host_ramp(self._h, int(ramp_min_elems))
@@ -597,13 +602,15 @@ class CovapSync:
 
     def __init__(self, plan: BucketPlan, comm: Optional[Communicator] = None, dtype=None,
                  device: int = 0, ef: Optional[EfSchedule] = None,
-                 fuse_single_rank: bool = True):
+                 fuse_single_rank: bool = True, pipeline: int = 1):
         self.plan = plan
         self.comm = comm
         self.state = CompressorState(plan, dtype, device, ef)
         self.device = device
         if not fuse_single_rank:
             self.state.set_fused(False)
+        if pipeline != 1:
+            self.state.set_pipeline(pipeline)
 
     @property
     def world(self) -> int:

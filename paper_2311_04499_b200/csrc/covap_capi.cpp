@@ -57,6 +57,7 @@ struct covap_state {
   std::vector<uint8_t> timed;                   // bucket had a collective in the last step
   bool fuse_single_rank = true;                 // P = 1: run K1F instead of K1 -> C1 -> K2
   uint64_t ramp_min = 1u << 20;                 // host pipeline: smallest ramp chunk (elements)
+  int pipeline = 1;                             // P > 1 sync step: bucket groups (1 = serial)
 };
 
 namespace covapb {
@@ -444,6 +445,14 @@ covap_status covap_state_set_fused(covap_state* s, int fuse_single_rank) {
   });
 }
 
+covap_status covap_state_set_pipeline(covap_state* s, int groups) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    need(groups >= 1, "groups must be >= 1");
+    s->pipeline = groups;
+  });
+}
+
 covap_status covap_state_set_host_ramp(covap_state* s, uint64_t ramp_min_elems) {
   return guarded([&] {
     need(s != nullptr, "NULL state");
@@ -596,6 +605,43 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
       // One rank: the allreduce is the identity, so K1 and K2 fuse into one
       // pass (K1F) that writes (0 + c) * 1 straight to the selected slots.
       k1f_range(s, grad, out, 1.0, 0, n, st);
+    } else if (s->pipeline > 1 && s->plan.buckets.size() > 1) {
+      // Pipelined: consecutive bucket groups of about n / G elements; group
+      // g's allreduce (comm stream) overlaps K1 of groups > g (compute
+      // stream), and its K2 follows as soon as its allreduce is done.  Every
+      // rank derives the same groups and envelopes from the plan.
+      const auto& bs = s->plan.buckets;
+      const size_t G = std::min<size_t>(static_cast<size_t>(s->pipeline), bs.size());
+      std::vector<size_t> first{0};
+      for (size_t b = 1; b < bs.size() && first.size() < G; ++b)
+        if (bs[b].dbegin >= n * first.size() / G) first.push_back(b);
+      const size_t ng = first.size();
+      auto lo_of = [&](size_t g) { return g == 0 ? uint64_t(0) : bs[first[g]].dbegin; };
+      auto hi_of = [&](size_t g) { return g + 1 < ng ? bs[first[g + 1]].dbegin : n; };
+      CK(cudaEventRecord(s->done, st));
+      CK(cudaStreamWaitEvent(s->comm_stream, s->done, 0));
+      for (size_t g = 0; g < ng; ++g) {
+        k1_range(s, grad, nullptr, lo_of(g), hi_of(g), st);
+        uint64_t lo = UINT64_MAX, hi = 0;
+        const size_t b1 = g + 1 < ng ? first[g + 1] : bs.size();
+        for (size_t b = first[g]; b < b1; ++b) {
+          const auto& sel = ph.per_bucket[b];
+          if (sel.sel_end <= sel.sel_begin) continue;
+          lo = std::min(lo, sel.send_offset);
+          hi = std::max(hi, sel.send_offset + (sel.sel_end - sel.sel_begin));
+        }
+        CK(cudaEventRecord(s->ready[g], st));
+        CK(cudaStreamWaitEvent(s->comm_stream, s->ready[g], 0));
+        if (comm && hi > lo)
+          NK(ncclAllReduce(static_cast<char*>(s->send) + lo * s->esize,
+                           static_cast<char*>(s->send) + lo * s->esize, hi - lo,
+                           nccl_type(s->dtype), ncclSum, comm->nccl, s->comm_stream));
+        CK(cudaEventRecord(s->end[g], s->comm_stream));
+      }
+      for (size_t g = 0; g < ng; ++g) {
+        CK(cudaStreamWaitEvent(st, s->end[g], 0));
+        k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, lo_of(g), hi_of(g), st);
+      }
     } else {
       k1_range(s, grad, nullptr, 0, n, st);
       if (comm && ph.send_elems > 0)

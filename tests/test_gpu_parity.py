@@ -409,9 +409,10 @@ def test_multi_rank_code_path_on_one_gpu(covap, name, K):
     a = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
     b = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
     c = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
+    e = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False, pipeline=3)
     d = plan.total_numel()
     g = torch.empty(d, device=DEV)
-    o_ref, o_a, o_b = (torch.empty(d, device=DEV) for _ in range(3))
+    o_ref, o_a, o_b, o_e = (torch.empty(d, device=DEV) for _ in range(4))
     hin = torch.empty(d, pin_memory=True)
     hout = torch.empty(d, pin_memory=True)
     for s in range(K + 1):
@@ -423,10 +424,11 @@ def test_multi_rank_code_path_on_one_gpu(covap, name, K):
             b.bucket_ready(bk, g, o_b)
         b.finish()
         c.sync_host(hin, hout, chunk_elems=1 << 20)
+        e.sync(g, o_e)  # pipelined bucket groups
         torch.cuda.synchronize()
-        for o in (o_a, o_b, hout.to(DEV)):
+        for o in (o_a, o_b, hout.to(DEV), o_e):
             assert torch.equal(o, o_ref)
-        for st in (a, b, c):
+        for st in (a, b, c, e):
             assert torch.equal(st.state.residuals, ref.state.residuals)
         durs = b.last_comm_ms()
         for bk in range(len(plan.buckets)):
