@@ -501,14 +501,15 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
         const uint64_t len = end - pos, i0 = pos - e0;
         const uint64_t head = (W - pos % W) % W < len ? (W - pos % W) % W : len;
         const uint64_t nv = (len - head) / W;
-        // send slot of element e (OP 0); vectors need dst == begin (mod W)
-        T* send_at = (OP == 0 && in_run) ? A.send + A.runs[j].dst - A.runs[j].begin : nullptr;
+        // send slot of element pos + i is send_at[i] (OP 0); vectors need
+        // dst == begin (mod W)
+        T* send_at = (OP == 0 && in_run) ? A.send + A.runs[j].dst + (pos - A.runs[j].begin) : nullptr;
         const bool vec_ok = !(OP == 0 && in_run) || (A.runs[j].dst - A.runs[j].begin) % W == 0;
         auto one = [&](uint64_t i) {  // element pos + i
           const uint64_t e = pos + i;
           const T c = A.ef ? add_rn(gs[i0 + i], mul_rn(A.coeff, rs[i0 + i])) : gs[i0 + i];
           if (in_run) {
-            if (OP == 0) send_at[e] = c;
+            if (OP == 0) send_at[i] = c;
             else if (OP == 1) A.out[e] = scale_of(c, A.inv, 1);
             else A.out[e] = sgd(A.out[e], A.lr, scale_of(c, A.inv, 1));
             A.r[e] = T(0);
@@ -534,7 +535,7 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
           for (int q = 0; q < static_cast<int>(W); ++q) lane(z, q) = T(0);
           if (in_run) {
             if (OP == 0) {
-              *reinterpret_cast<V*>(send_at + e) = x;
+              *reinterpret_cast<V*>(send_at + i) = x;
             } else {
               V o = OP == 3 ? *reinterpret_cast<const V*>(A.out + e) : z;
 #pragma unroll
