@@ -228,6 +228,12 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
 // (dst == begin mod kSendAlign).
 
 constexpr int kStepThreads = 256;
+#ifndef COVAP_PEER_BATCH  // 16-byte vectors each thread loads before storing (whole-step kernel)
+#define COVAP_PEER_BATCH 8
+#endif
+#ifndef COVAP_PEER_MINB  // resident CTAs per SM the whole-step kernel is register-capped for
+#define COVAP_PEER_MINB 1
+#endif
 
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
@@ -284,7 +290,7 @@ __device__ __forceinline__ void for_send_pieces(const PeerStepArgs& A, uint64_t 
 // 16-byte vectors, load(i) then store(i, loaded) with kBatch vectors per
 // thread loaded before any is stored, so each thread keeps several loads in
 // flight (the pass is latency-bound otherwise: one CTA walks one chunk).
-constexpr int kBatch = 4;
+constexpr int kBatch = COVAP_PEER_BATCH;
 template <typename T, typename S, typename Ld, typename St>
 __device__ __forceinline__ void block_pass(uint64_t e, uint64_t n, S&& scalar, Ld&& load, St&& store) {
   constexpr uint64_t W = 16 / sizeof(T);
@@ -314,7 +320,7 @@ struct Pair {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kStepThreads, 2) peer_step_kernel(const PeerStepArgs A) {
+__global__ void __launch_bounds__(kStepThreads, COVAP_PEER_MINB) peer_step_kernel(const PeerStepArgs A) {
   using V = typename V16<T>::type;
   constexpr uint64_t W = 16 / sizeof(T);
   const int P = A.P, rank = A.rank;
@@ -518,7 +524,7 @@ cudaError_t launch_peer_step(int dtype, const PeerStepArgs& args, int max_ctas, 
   // Work items come from an in-order queue, so no CTA waits for an item no
   // running CTA has taken: any grid is deadlock-free on its own GPU.  Ranks
   // sharing one GPU (tests) cap the grid so that they are co-resident.
-  int grid = sms * 4;
+  int grid = sms * COVAP_PEER_MINB;  // one wave: the queue hands out the work
   if (max_ctas > 0) grid = std::min(grid, max_ctas);
   if (dtype == 0)
     peer_step_kernel<float><<<grid, kStepThreads, 0, s>>>(args);
