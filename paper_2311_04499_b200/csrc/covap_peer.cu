@@ -131,10 +131,30 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
   const uint64_t per = (nvec + P - 1) / P;
   const uint64_t v_lo = umin(nvec, per * r), v_hi = umin(nvec, per * (r + 1));
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kPeerThreads;
-  for (uint64_t v = v_lo + blockIdx.x * kPeerThreads + threadIdx.x; v < v_hi; v += stride) {
-    V acc = vzero<V>();
-    for (int p = 0; p < P; ++p) acc = vadd(acc, reinterpret_cast<const V*>(bufs[p])[v]);
-    reinterpret_cast<V*>(bufs[r])[v] = acc;
+  // kAllB vectors per thread per round, so each rank's loads of a round are
+  // in flight together (the loop is latency-bound otherwise)
+  constexpr int kAllB = 4;
+  for (uint64_t v0 = v_lo + blockIdx.x * kPeerThreads + threadIdx.x; v0 < v_hi;
+       v0 += kAllB * stride) {
+    V acc[kAllB];
+#pragma unroll
+    for (int b = 0; b < kAllB; ++b) acc[b] = vzero<V>();
+    for (int p = 0; p < P; ++p) {
+      V x[kAllB];
+#pragma unroll
+      for (int b = 0; b < kAllB; ++b) {
+        const uint64_t v = v0 + b * stride;
+        if (v < v_hi) x[b] = reinterpret_cast<const V*>(bufs[p])[v];
+      }
+#pragma unroll
+      for (int b = 0; b < kAllB; ++b)
+        if (v0 + b * stride < v_hi) acc[b] = vadd(acc[b], x[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < kAllB; ++b) {
+      const uint64_t v = v0 + b * stride;
+      if (v < v_hi) reinterpret_cast<V*>(bufs[r])[v] = acc[b];
+    }
   }
   // the scalar tail (L not a multiple of W) belongs to the last rank
   if (r == P - 1 && blockIdx.x == 0)
@@ -198,10 +218,23 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
           const uint64_t o = rd + (e - rb);
           out[e] = mul_rn(bufs[owner(o)][o], inv);
         }
-      for (uint64_t v = a16 / W + blockIdx.x * kPeerThreads + threadIdx.x; v < b16 / W; v += stride) {
-        const uint64_t o = rd + (v * W - rb);
-        V x = *reinterpret_cast<const V*>(bufs[owner(o)] + o);
-        reinterpret_cast<V*>(out)[v] = vscale(x, inv);
+      constexpr int kUnB = 8;  // vectors in flight per thread
+      for (uint64_t v0 = a16 / W + blockIdx.x * kPeerThreads + threadIdx.x; v0 < b16 / W;
+           v0 += kUnB * stride) {
+        V x[kUnB];
+#pragma unroll
+        for (int b = 0; b < kUnB; ++b) {
+          const uint64_t v = v0 + b * stride;
+          if (v < b16 / W) {
+            const uint64_t o = rd + (v * W - rb);
+            x[b] = *reinterpret_cast<const V*>(bufs[owner(o)] + o);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kUnB; ++b) {
+          const uint64_t v = v0 + b * stride;
+          if (v < b16 / W) reinterpret_cast<V*>(out)[v] = vscale(x[b], inv);
+        }
       }
     }
     zero_range(prev, args.n_out);
