@@ -629,3 +629,32 @@ def test_timeline_and_chrome_trace(covap, tmp_path):
         mc = trace.model_check(tl, [0.2] * len(tl), tl[-1]["k2_end"])
         assert mc["predicted_step_ms"] > 0.9
     comm.close()
+
+
+@pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 3)])
+def test_checkpoint_resume_equals_uninterrupted(covap, name, K):
+    """CompressorState is the residual arena plus num_steps (compress.hpp:42-47):
+    saving both mid-run (host copy) and restoring them into a fresh state
+    continues the run bit for bit — the EF coefficient schedule and the
+    round-robin phase resume from num_steps."""
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    ef = covap.EfSchedule(True, 0.3, 2, 0.2)
+    a = covap.CovapSync(plan, None, torch.float32, 0, ef)
+    d = plan.total_numel()
+    g = torch.empty(d, device=DEV)
+    oa, ob = torch.empty(d, device=DEV), torch.empty(d, device=DEV)
+    for s in range(K + 1):
+        covap.generate(g, covap.stream_key(41, 0, s))
+        a.sync(g, oa)
+    torch.cuda.synchronize()
+    saved_r, saved_step = a.state.residuals.cpu(), a.state.num_steps  # the checkpoint
+    b = covap.CovapSync(plan, None, torch.float32, 0, ef)
+    b.state.residuals.copy_(saved_r.to(DEV))
+    b.state.num_steps = saved_step
+    for s in range(K + 1, 2 * K + 3):
+        covap.generate(g, covap.stream_key(41, 0, s))
+        a.sync(g, oa)
+        b.sync(g, ob)
+        torch.cuda.synchronize()
+        assert torch.equal(oa, ob), s
+        assert torch.equal(a.state.residuals, b.state.residuals), s
