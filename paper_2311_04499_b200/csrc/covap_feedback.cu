@@ -670,7 +670,32 @@ __global__ void __launch_bounds__(kThreads) topk_final_kernel(TopkArgs A) {
   const K lowmask = (K(1) << kLow) - 1;
   uint64_t pa = 0;  // fixed prefix of the low key bits
   uint32_t pb = 0;  // fixed prefix of ~index
-  if (need < m) {
+  // Few survivors (the usual case on real gradients): rank each one against
+  // the others by the composite (low key bits, ~index) in one pass instead
+  // of the multi-pass radix select.  Composites are distinct (the index is).
+  __shared__ uint64_t s_a[kThreads];
+  __shared__ uint32_t s_b[kThreads];
+  __shared__ uint8_t s_take[kThreads];
+  const bool fast = need < m && m <= static_cast<uint32_t>(kThreads);
+  if (fast) {
+    const uint32_t e = threadIdx.x;
+    uint64_t a = 0;
+    uint32_t b = 0;
+    if (e < m) {
+      a = static_cast<uint64_t>(ck[e] & lowmask);
+      b = ~cx[e];
+      s_a[e] = a;
+      s_b[e] = b;
+    }
+    __syncthreads();
+    if (e < m) {
+      uint32_t rank = 0;
+      for (uint32_t f = 0; f < m; ++f)
+        rank += (s_a[f] > a || (s_a[f] == a && s_b[f] > b)) ? 1u : 0u;
+      s_take[e] = rank < need ? 1 : 0;
+    }
+    __syncthreads();
+  } else if (need < m) {
     // field 0: the low key bits, field 1: ~index (32 bits)
     for (int field = 0; field < 2; ++field) {
       int left = field == 0 ? kLow : 32;
@@ -717,7 +742,7 @@ __global__ void __launch_bounds__(kThreads) topk_final_kernel(TopkArgs A) {
     if (e < m) {
       const uint64_t a = static_cast<uint64_t>(ck[e] & lowmask);
       const uint32_t b = ~cx[e];
-      take = all || a > pa || (a == pa && b >= pb);
+      take = all || (fast ? s_take[e] != 0 : (a > pa || (a == pa && b >= pb)));
     }
     const uint32_t slot = append_slot(take, &s_count);
     if (take) {
