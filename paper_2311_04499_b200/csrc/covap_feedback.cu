@@ -550,7 +550,10 @@ __global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
 // latency-bound (a dependent key -> r[i] gather per taken candidate), so every
 // lane keeps kF2 candidates in flight and the grid fills the SMs.  Appends are
 // warp-aggregated per tensor (one atomic per tensor present in the warp).
-constexpr int kF2 = 4;
+#ifndef COVAP_F2_INFLIGHT
+#define COVAP_F2_INFLIGHT 4
+#endif
+constexpr int kF2 = COVAP_F2_INFLIGHT;
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) topk_filter2_kernel(TopkArgs A) {
