@@ -174,9 +174,11 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       break;
     }
     case COVAP_FILTER_TOPK: {
+      const bool pdl = f->total < fb::kTopkPdlMaxElems;
       CK(fb::launch_compensate(dt, grad, f->residual, zero, f->hist, f->chunks, f->nchunks,
-                               f->ef.enabled, coeff, f->sms, st));
+                               f->ef.enabled, coeff, f->sms, st, pdl));
       fb::TopkArgs a{};
+      a.pdl = pdl ? 1 : 0;
       a.r = f->residual;
       a.kept = kept;
       a.kept_mean = kept_mean ? 1 : 0;
