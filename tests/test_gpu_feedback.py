@@ -328,21 +328,23 @@ def test_conservation_every_scheme_at_layout_size(covap, orc):
         assert torch.equal(sent + fb.residuals.double(), gin), kind
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("kind", [2, 3, 4])
-def test_sync_one_rank_signed_zero_mean(covap, orc, kind):
+def test_sync_one_rank_signed_zero_mean(covap, orc, kind, dtype):
     """One rank fuses the mean into the filter pass: kept -0.0 must still come
     out as +0.0, the (0.0 + x) of allreduce_mean (trainer.cpp:41)."""
     sizes = [4100, 7]
     n = sum(sizes)
     fb = F().ErrorFeedback(sizes, covap.EfSchedule(False, 0.3, 100, 0.1),
-                           make_filter(kind, 1, 1.0, 5))
-    g = torch.full((n,), -0.0, dtype=torch.float32, device=DEV)
+                           make_filter(kind, 1, 1.0, 5), dtype=dtype)
+    g = torch.full((n,), -0.0, dtype=dtype, device=DEV)
     g[::3] = -2.5
-    out = torch.full((n,), float("nan"), device=DEV)
+    out = torch.full((n,), float("nan"), dtype=dtype, device=DEV)
     fb.sync(g, out, None)
     gh = g.cpu().numpy()
-    k, _, _ = orc.feedback_step(kind, 0, gh, np.zeros(n, np.float32), tensors_of(sizes), 0,
-                                np.float32(0), k_fraction=1.0, seed=5)
+    npt = np.float64 if dtype == torch.float64 else np.float32
+    k, _, _ = orc.feedback_step(kind, 0, gh, np.zeros(n, npt), tensors_of(sizes), 0,
+                                npt(0), k_fraction=1.0, seed=5)
     want = oracle_mean(orc, [k])
     assert np.all(bits(want)[gh == 0] == 0)  # +0.0, not -0.0
     np.testing.assert_array_equal(bits(out.cpu().numpy()), bits(want))
