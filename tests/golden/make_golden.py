@@ -182,6 +182,11 @@ def main():
         ("p2_k3", [37, 5, 129, 64, 1, 300, 77, 2, 515], 600, 3, 0, (1, 0.3, 100, 0.1), 0, 2, 9),
         ("p4_sharded_k4", [4000, 12, 9000, 33, 700, 1500], 8000, 4, 0, (1, 0.4, 3, 0.2), 0, 4, 8),
         ("p3_int_k2", [1000, 999, 1001, 17, 4096], 4400, 2, 1, (1, 1.0, 1, 0.0), 1, 3, 6),
+        # eight workers (one B200 box), kPlusStep, five tensors
+        ("p8_plus_k5", [513, 2048, 77, 1500, 4096, 9, 640, 3000, 1200], 9000, 5, 1,
+         (1, 0.3, 2, 0.15), 0, 8, 11),
+        # more phases than tensors: empty selections on some steps, five workers
+        ("p5_k8_empty", [700, 5000, 300, 2500], 5200, 8, 0, (1, 0.5, 4, 0.1), 0, 5, 10),
     ]
     smanifest = []
     for name, sizes, cap, K, rule, efp, kind, P, steps in sessions:
