@@ -855,7 +855,11 @@ __global__ void randomk_link_kernel(RandomkArgs A) {
        e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t t = tensor_of_entry(A, e);
     const uint32_t i = static_cast<uint32_t>(e - A.list_off[t]);
-    A.nxt[e] = atomicExch(&A.head[A.t_begin[t] + A.j[e]], i);
+    // epoch-tagged list heads: an entry of another epoch reads as empty, so
+    // the heads never need clearing (one random write per draw less)
+    const unsigned long long old = atomicExch(&A.head[A.t_begin[t] + A.j[e]],
+                                              (static_cast<unsigned long long>(A.tag) << 32) | i);
+    A.nxt[e] = (old >> 32) == A.tag ? static_cast<uint32_t>(old) : kNone;
   }
 }
 
@@ -864,7 +868,9 @@ __device__ __forceinline__ uint32_t last_before(const RandomkArgs& A, uint32_t t
                                                 uint32_t before) {
   const uint64_t lo = A.list_off[t];
   uint32_t best = kNone;
-  for (uint32_t m = A.head[A.t_begin[t] + p]; m != kNone; m = A.nxt[lo + m])
+  const unsigned long long h = A.head[A.t_begin[t] + p];
+  for (uint32_t m = (h >> 32) == A.tag ? static_cast<uint32_t>(h) : kNone; m != kNone;
+       m = A.nxt[lo + m])
     if (m < before && (best == kNone || m > best)) best = m;
   return best;
 }
@@ -909,17 +915,9 @@ __global__ void randomk_gather_kernel(RandomkArgs A, T* __restrict__ r, T* __res
     list_val[e] = c;
     if (kept) kept[flat] = kept_value(c, kept_mean);
     r[flat] = sub_rn(c, c);
-    A.head[A.t_begin[t] + j] = kNone;  // the chain kernel is done with the lists
   }
 }
 
-__global__ void randomk_clear_kernel(RandomkArgs A) {
-  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
-       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t t = tensor_of_entry(A, e);
-    A.head[A.t_begin[t] + A.j[e]] = kNone;
-  }
-}
 
 // ------------------------------------------------------------ exchange
 

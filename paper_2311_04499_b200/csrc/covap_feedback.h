@@ -115,11 +115,12 @@ struct RandomkArgs {
   uint32_t* nxt;
   uint32_t* prv;
   uint32_t* src;
-  uint32_t* head;             // per flat position, kNone when idle
+  unsigned long long* head;   // per flat position: (tag << 32) | last draw targeting it
+  uint32_t tag;               // this selection's epoch (> 0): entries of other epochs are empty
   int* reject;                // per tensor
 };
 cudaError_t launch_randomk_select(const RandomkArgs& a, int sms, cudaStream_t s);
-// list[e] = (flat index S_e, c); kept[S] = c; r[S] = c - c; head cleared.
+// list[e] = (flat index S_e, c); kept[S] = c; r[S] = c - c.
 cudaError_t launch_randomk_gather(int dtype, const RandomkArgs& a, void* r, void* kept,
                                   int kept_mean, uint32_t* list_idx, void* list_val, int sms,
                                   cudaStream_t s);

@@ -64,7 +64,9 @@ struct covap_feedback {
   void* acc = nullptr;  // rank-ordered scatter accumulator, zero between steps
   // random-k
   uint32_t* tensor_of = nullptr;
-  uint32_t *j = nullptr, *nxt = nullptr, *prv = nullptr, *src = nullptr, *head = nullptr;
+  uint32_t *j = nullptr, *nxt = nullptr, *prv = nullptr, *src = nullptr;
+  unsigned long long* head = nullptr;  // epoch-tagged list heads, one per flat position
+  uint32_t rk_epoch = 0;               // random-k selections made (the head tag)
   int* reject = nullptr;
   cudaStream_t side = nullptr;  // index sampling, concurrent with the compensation pass
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -134,6 +136,13 @@ fb::RandomkArgs randomk_args(covap_feedback* f) {
   a.prv = f->prv;
   a.src = f->src;
   a.head = f->head;
+  a.tag = ++f->rk_epoch;
+  if (a.tag == 0) {  // 2^32 selections: clear the heads and start over
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemset(f->head, 0, std::max<uint64_t>(f->total, 1) * 8));
+    CK(cudaDeviceSynchronize());
+    a.tag = f->rk_epoch = 1;
+  }
   a.reject = f->reject;
   return a;
 }
@@ -415,8 +424,8 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
       f->nxt = dalloc<uint32_t>(f, f->k_total * 4);
       f->prv = dalloc<uint32_t>(f, f->k_total * 4);
       f->src = dalloc<uint32_t>(f, f->k_total * 4);
-      f->head = dalloc<uint32_t>(f, f->total * 4);
-      CK(cudaMemset(f->head, 0xff, std::max<uint64_t>(f->total, 4) * 4));
+      f->head = dalloc<unsigned long long>(f, f->total * 8);
+      CK(cudaMemset(f->head, 0, std::max<uint64_t>(f->total, 1) * 8));  // tag 0: never current
       f->reject = dalloc<int>(f, n_tensors * 4);
       CK(cudaMemset(f->reject, 0, n_tensors * 4));
       CK(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
