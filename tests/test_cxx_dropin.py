@@ -95,3 +95,33 @@ def test_reference_device_cases_pass_on_b200():
     rc, out = run(["--skip=" + "|".join(OUT_OF_SCOPE)])
     assert rc == 0, out
     assert out.count("[PASS]") == len(HOST_ONLY) + len(DEVICE), out
+
+
+# ------------------------------------------------ the device-resident C++ API
+API_BIN = os.path.join(ROOT, "tests", "cxx", "_build", "b200_api_tests")
+API_HOST = ["device-resident API raises the reference's exception classes"]
+
+
+def api_run(args):
+    if not os.path.exists(API_BIN):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cxx"),
+                        "_build/b200_api_tests"], check=True)
+    p = subprocess.run([API_BIN] + args, capture_output=True, text=True, timeout=600)
+    return p.returncode, p.stdout + p.stderr
+
+
+def test_b200_api_host_cases():
+    rc, out = api_run(["--only=" + "|".join(API_HOST)])
+    assert rc == 0, out
+    assert out.count("[PASS]") == len(API_HOST)
+
+
+@pytest.mark.gpu
+def test_b200_api_device_cases_on_b200():
+    """covap::b200::Plan / Sync (include/covap/b200_api.hpp), the API
+    INTEGRATION.md recommends to C++ training loops: the device-resident step
+    equals covap_compress + covap_decompress bit for bit (fp64), and the
+    per-bucket overlapped schedule equals the standalone step (fp32)."""
+    rc, out = api_run([])
+    assert rc == 0, out
+    assert "2 failed" not in out and out.count("[PASS]") == 3, out
