@@ -64,6 +64,9 @@ namespace {
 #ifndef COVAP_FILTER_THREADS  // threads per CTA of the K1 / K1F / K1F+SGD passes
 #define COVAP_FILTER_THREADS 256
 #endif
+#ifndef COVAP_FP16_THREADS  // threads per CTA of the fp16 filter pass (op 5)
+#define COVAP_FP16_THREADS 1024
+#endif
 #ifndef COVAP_PDL  // programmatic dependent launch between consecutive sync kernels
 #define COVAP_PDL 1
 #endif
@@ -339,7 +342,7 @@ constexpr int k1_slot_tiles() {
 
 template <int OP>
 __host__ __device__ constexpr int filter_threads() {
-  return OP == 5 ? 512 : COVAP_FILTER_THREADS;  // fp16: conversion-heavy, more warps per SM
+  return OP == 5 ? COVAP_FP16_THREADS : COVAP_FILTER_THREADS;  // fp16: conversion-heavy, more warps
 }
 
 template <typename T, int OP>
