@@ -341,6 +341,15 @@ covap_status covap_embed(int device, int dtype, const void* payload, void* out, 
                          const uint64_t* sel_begin, const uint64_t* sel_end,
                          const uint64_t* payload_off, size_t nsel, double scale, int mean,
                          void* stream);
+/* allreduce_mean (trainer.cpp:35-47) of one device buffer per rank, one
+ * process per GPU: NCCL sum of `buf` in place over the communicator (skipped
+ * when comm is NULL or has one rank), then out = (0 + sum) * (1/P) — the
+ * reference's "start from +0.0, sum, scale by 1.0/P" order (trainer.cpp:41-45).
+ * out may alias buf.  Stream-ordered, no allocation, no state.  With P <= 2
+ * the result is bit-identical to the reference; for P > 2 NCCL's summation
+ * order differs (|d| <= 1e-6 * sum_w |x_w|). */
+covap_status covap_comm_allreduce_mean(covap_comm* comm, int dtype, void* buf, void* out,
+                                       uint64_t count, void* stream);
 /* allreduce_mean of P in-process workers (trainer.cpp:35-47): rows is P x n
  * (worker-major), out = (0 + x_0 + ... + x_{P-1}) * (1/P) in worker order. */
 covap_status covap_mean_rows(int device, int dtype, const void* rows, void* out, uint64_t P,
@@ -457,6 +466,11 @@ covap_status covap_generate(void* out, uint64_t n, int dtype, uint64_t key, int 
                             uint64_t begin, void* stream);
 /* K3: backward emulator, spins `blocks` CTAs for `us` microseconds. */
 covap_status covap_spin(double us, int blocks, void* stream);
+/* K3, full-GPU form: emulated backward of `us` microseconds as a sequence of
+ * kernels of `slice_us` each, every one a 1024-thread CTA per SM holding
+ * 160 KB of shared memory — the SMs are owned the way real backward kernels
+ * own them, so side-stream K1 / K2 run only in the gaps (harness only). */
+covap_status covap_busy(double us, double slice_us, void* stream);
 
 #ifdef __cplusplus
 }

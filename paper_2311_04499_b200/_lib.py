@@ -106,6 +106,7 @@ _SIGS = {
     "covap_comm_destroy": ("void", [vp]),
     "covap_comm_size": (None, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
     "covap_allreduce": (None, [vp, vp, u64, i32, vp]),
+    "covap_comm_allreduce_mean": (None, [vp, i32, vp, vp, u64, vp]),
     "covap_comm_profile_exchange": (None, [vp, f64p, sz, f64, f64p, f64p]),
     "covap_peer_create": (None, [vp, i32, i32, ctypes.POINTER(vp)]),
     "covap_peer_destroy": ("void", [vp]),
@@ -146,6 +147,7 @@ _SIGS = {
     "covap_stream_key": (u64, [u64, u64, u64]),
     "covap_generate": (None, [vp, u64, i32, u64, i32, u64, vp]),
     "covap_spin": (None, [f64, i32, vp]),
+    "covap_busy": (None, [ctypes.c_double, ctypes.c_double, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

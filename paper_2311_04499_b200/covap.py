@@ -567,22 +567,21 @@ class Communicator:
             self._h = None
 
 
-def allreduce_mean(buf, comm: Optional[Communicator], out=None, stream=None):
-    """allreduce_mean (trainer.cpp:35-47) of one device buffer: NCCL sum in
-    place, then (0 + sum) * 1/P via the K2 kernel with a single full run."""
+def allreduce_mean(buf, comm: Optional[Communicator] = None, out=None, stream=None):
+    """allreduce_mean (trainer.cpp:35-47) of one device buffer per rank: NCCL
+    sum in place (P > 1), then out = (0 + sum) * (1/P) — one stream-ordered
+    native call (covap_comm_allreduce_mean), no state, no allocation beyond
+    ``out``.  fp32 or fp64; ``out`` may be ``buf``."""
     torch = _torch()
-    P = comm.nranks if comm is not None else 1
-    if comm is not None:
-        comm.allreduce(buf, stream)
+    code = _dtype_code(buf.dtype)
+    if not buf.is_cuda or not buf.is_contiguous():
+        raise InvalidInput("allreduce_mean needs a contiguous CUDA tensor")
     if out is None:
         out = torch.empty_like(buf)
-    plan = BucketPlan(ModelSpec([LayerSpec("x", buf.numel(), 8 if buf.dtype == torch.float64 else 4)],
-                                bucket_cap_bytes=1 << 62))
-    st = CompressorState(plan, buf.dtype, buf.device.index or 0, EfSchedule(enabled=False))
-    # Phase 0 of a K=1 plan selects everything: one run [0, n) -> send[0, n);
-    # recv is the caller's buffer, so K2 computes (0 + buf) * 1/P.
-    st.unpack(out, 1.0 / P, True, recv=buf, stream=stream)
-    (stream or torch.cuda.current_stream(buf.device)).synchronize()  # st is freed on return
+    elif out.dtype != buf.dtype or out.numel() != buf.numel() or not out.is_contiguous():
+        raise InvalidInput("allreduce vectors differ in length")  # trainer.cpp:38-39
+    L.lib().covap_comm_allreduce_mean(None if comm is None else comm.handle, code, _ptr(buf),
+                                      _ptr(out), buf.numel(), _stream_ptr(stream, buf.device))
     return out
 
 
@@ -700,6 +699,12 @@ def generate(out, key: int, kind: int = 0, begin: int = 0, stream=None):
 def spin(us: float, blocks: int = 1, stream=None, device=None):
     """K3: occupy `blocks` CTAs for `us` microseconds (backward emulator)."""
     L.lib().covap_spin(float(us), int(blocks), _stream_ptr(stream, device))
+
+
+def busy(us: float, slice_us: float = 50.0, stream=None, device=None):
+    """K3, full-GPU form: `us` microseconds of kernels that each own every SM
+    (1024 threads + 160 KB shared memory per SM), `slice_us` per kernel."""
+    L.lib().covap_busy(float(us), float(slice_us), _stream_ptr(stream, device))
 
 
 # ------------------------------------------------------------ CCR controller

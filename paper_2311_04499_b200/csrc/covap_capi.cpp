@@ -963,6 +963,29 @@ covap_status covap_allreduce(covap_comm* c, void* buf, uint64_t count, int dtype
   });
 }
 
+covap_status covap_comm_allreduce_mean(covap_comm* c, int dtype, void* buf, void* out,
+                                       uint64_t count, void* stream) {
+  return guarded([&] {
+    need(buf && out, "NULL argument");
+    need(dtype == COVAP_F32 || dtype == COVAP_F64, "bad dtype");
+    if (count == 0) return;  // allreduce_mean of empty vectors is empty (trainer.cpp:40)
+    need_aligned(buf, "buf");
+    need_aligned(out, "out");
+    const int P = world(c);
+    int dev = 0;
+    if (c) {
+      dev = c->device;
+    } else {
+      CK(cudaGetDevice(&dev));
+    }
+    DeviceGuard dg(dev);
+    cudaStream_t st = as_stream(stream);
+    if (c && P > 1) NK(ncclAllReduce(buf, buf, count, nccl_type(dtype), ncclSum, c->nccl, st));
+    // (0 + sum) * (1/P), trainer.cpp:41-45: one row, scale 1/P
+    CK(covapb::launch_mean_rows(dtype, buf, out, 1, count, st, 1.0 / static_cast<double>(P)));
+  });
+}
+
 covap_status covap_comm_profile_exchange(covap_comm* c, const double* dur, size_t n_coll,
                                          double comp_ms, double* aligned_ms, double* comp_out) {
   return guarded([&] {
@@ -1093,6 +1116,10 @@ covap_status covap_spin(double us, int blocks, void* stream) {
   return guarded([&] { CK(covapb::launch_spin(us, blocks, as_stream(stream))); });
 }
 
+covap_status covap_busy(double us, double slice_us, void* stream) {
+  return guarded([&] { CK(covapb::launch_busy(us, slice_us, as_stream(stream))); });
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------- peer collective
@@ -1124,6 +1151,14 @@ struct covap_peer {
   // the unpack fused (default); 2: the whole step in one kernel (peer_step_kernel)
   int mode = 1;
   uint64_t posted = 0;  // last epoch at which every rank published an arrival
+  // Collective launches so far.  The send buffer is picked by its parity, not
+  // by the step's: a step with an empty selection launches no collective (no
+  // barrier), so two step-parity-equal steps around empty phases could have
+  // no barrier between them, and K1 of the later one could rewrite a buffer
+  // a slower peer is still reading.  Consecutive LAUNCHES alternate buffers,
+  // and launch j + 2 is packed only after this rank passed launch j + 1's
+  // arrival barrier, which every peer reaches only after finishing launch j.
+  uint64_t launches = 0;
 };
 
 extern "C" {
@@ -1274,7 +1309,7 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
     cudaStream_t st = as_stream(stream);
     const uint64_t n = s->plan.dtotal;
     const auto& ph = phase_of(s->plan, s->num_steps);
-    const int par = static_cast<int>(s->num_steps & 1);
+    const int par = static_cast<int>(p->launches & 1);
     void* buf = p->bufs[par];
     if (p->mode == 2) {  // K1 + collective + unpack in one kernel
       covapb::PeerStepArgs a{};
@@ -1302,6 +1337,7 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
       a.inv = 1.0 / static_cast<double>(p->P);
       need(a.len <= p->cmax * covapb::kPeerChunk, "send length exceeds the peer flag capacity");
       CK(covapb::launch_peer_step(s->dtype, a, p->max_ctas, st));
+      ++p->launches;
       p->posted = p->epoch;
       ++s->num_steps;
       return;
@@ -1329,6 +1365,7 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
       a.n_out = n;
       a.inv = 1.0 / static_cast<double>(p->P);
       CK(covapb::launch_peer_allreduce(s->dtype, a, p->max_ctas, st));
+      ++p->launches;
     }
     // fused: the collective already wrote out (C1 + K2 in one kernel)
     if (!(p->mode == 1 && ph.send_elems > 0))

@@ -54,12 +54,13 @@ cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* run
                           uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s);
 // allreduce_mean over P rows (P x n, worker-major) in worker order.
 cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,
-                             cudaStream_t s);
+                             cudaStream_t s, double inv = 0.0);
 // K0: synthetic gradients.
 cudaError_t launch_generate(int dtype, void* out, uint64_t n, uint64_t key, int kind,
                             uint64_t begin, cudaStream_t s);
 // K3: spin emulator.
 cudaError_t launch_spin(double us, int blocks, cudaStream_t s);
+cudaError_t launch_busy(double us, double slice_us, cudaStream_t s);
 
 uint64_t stream_key(uint64_t seed, uint64_t rank, uint64_t step);
 

@@ -1050,14 +1050,16 @@ cudaError_t launch_filter_fp16(int dtype, const void* g, void* r, void* kept, in
 }
 
 cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,
-                             cudaStream_t s) {
+                             cudaStream_t s, double inv_override) {
   if (n == 0) return cudaSuccess;
   DeviceShape* sh;
   cudaError_t e = shape(&sh);
   if (e) return e;
   const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(
       1, std::min<uint64_t>(static_cast<uint64_t>(sh->sms) * 8, (n + kThreads - 1) / kThreads)));
-  const double inv = 1.0 / static_cast<double>(P);
+  // inv_override: the scale of an already-summed single row (an NCCL sum of
+  // P ranks is one row here, but still scales by 1/P)
+  const double inv = inv_override > 0.0 ? inv_override : 1.0 / static_cast<double>(P);
   if (dtype == 0)
     mean_rows_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<const float*>(rows),
                                                       static_cast<float*>(out), P, n,
@@ -1087,6 +1089,45 @@ cudaError_t launch_spin(double us, int blocks, cudaStream_t s) {
   if (us <= 0) return cudaSuccess;
   spin_kernel<<<std::max(blocks, 1), 32, 0, s>>>(static_cast<uint64_t>(us * 1000.0));
   return cudaGetLastError();
+}
+
+// K3 (full-GPU form): a backward pass's kernels own the SMs while they run —
+// one 1024-thread CTA per SM holding kBusySmem of shared memory, so no CTA of
+// the filter / unpack kernels (172 / 229 KB) fits beside it; only small-
+// footprint kernels (NCCL's) can co-reside.  The emulated backward of `us`
+// is a sequence of such kernels of `slice_us` each, and side-stream work
+// runs in the gaps between them, as it does between real backward kernels.
+constexpr int kBusySmem = 160 * 1024;
+__global__ void __launch_bounds__(1024) busy_kernel(uint64_t ns) {
+  extern __shared__ unsigned char busy_smem[];
+  if (threadIdx.x == 0) busy_smem[0] = 0;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+cudaError_t launch_busy(double us, double slice_us, cudaStream_t s) {
+  if (us <= 0) return cudaSuccess;
+  DeviceShape* sh;
+  cudaError_t e = shape(&sh);
+  if (e) return e;
+  static bool attr = false;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(busy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kBusySmem)))
+      return e;
+    attr = true;
+  }
+  if (slice_us <= 0) slice_us = us;
+  const int n = std::max(1, static_cast<int>(us / slice_us + 0.5));
+  const uint64_t ns = static_cast<uint64_t>(us * 1000.0 / n);
+  for (int i = 0; i < n; ++i) {
+    busy_kernel<<<sh->sms, 1024, kBusySmem, s>>>(ns);
+    if ((e = cudaGetLastError())) return e;
+  }
+  return cudaSuccess;
 }
 
 // Per-worker stream key: mix_seed(seed, 0x100 + rank) (trainer.cpp:126), then

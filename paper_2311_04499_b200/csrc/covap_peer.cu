@@ -15,10 +15,11 @@
 //            locally.
 //
 // Remote traffic per rank is 2(P-1)/P x 4S bytes, the ring/NCCL bus volume.
-// Send buffers are double-buffered by step parity: a rank packs step s+2 into
-// the buffer peers read at step s only after the step s+1 arrival, which
-// every peer reaches only after finishing step s — so no end-of-step barrier
-// is needed.  Every spin-wait is bounded (%globaltimer): on timeout the
+// Send buffers are double-buffered by collective-launch parity (steps with an
+// empty selection launch nothing and do not count): a rank packs launch j+2
+// into the buffer peers read at launch j only after the launch j+1 arrival,
+// which every peer reaches only after finishing launch j — so no end-of-step
+// barrier is needed.  Every spin-wait is bounded (%globaltimer): on timeout the
 // kernel raises an error flag the host turns into COVAP_ERR_GENERIC instead of
 // hanging the GPU.
 #include <cuda_runtime.h>

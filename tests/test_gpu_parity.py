@@ -658,3 +658,166 @@ def test_checkpoint_resume_equals_uninterrupted(covap, name, K):
         torch.cuda.synchronize()
         assert torch.equal(oa, ob), s
         assert torch.equal(a.state.residuals, b.state.residuals), s
+
+
+# ------------------------------------------------------------------ allreduce_mean (a11)
+
+def _signed_zero_input(n, dtype, seed):
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(n, generator=g, dtype=torch.float64).to(dtype)
+    x[::7] = -0.0
+    x[1::7] = 0.0
+    x[2::11] = torch.tensor(-1e-30, dtype=torch.float64).to(dtype)
+    return x
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_allreduce_mean_python_boundary(covap, orc, dtype):
+    """covap.allreduce_mean (trainer.cpp:35-47) through covap_comm_allreduce_mean:
+    (0 + sum) * (1/P) — with no communicator and with a 1-rank NCCL
+    communicator, into a new tensor and in place; -0.0 comes out as +0.0 as
+    in the reference (the sum starts from +0.0, trainer.cpp:41)."""
+    npd = np.float32 if dtype == torch.float32 else np.float64
+    comm = covap.Communicator(covap.Communicator.unique_id(), 1, 0, 0)
+    for n in (1, 3, 17, 1000, 1 << 20, 5_000_001):
+        x = _signed_zero_input(n, dtype, n)
+        want = orc.allreduce_mean(x.numpy()[None, :].astype(npd))
+        for c in (None, comm):
+            buf = x.to(DEV)
+            out = covap.allreduce_mean(buf, c)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(out.cpu().numpy()), bits(want)), (n, c)
+            assert not np.signbit(out.cpu().numpy()[::7]).any()
+            inplace = x.to(DEV)
+            covap.allreduce_mean(inplace, c, out=inplace)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(inplace.cpu().numpy()), bits(want))
+    empty = torch.empty(0, dtype=dtype, device=DEV)
+    assert covap.allreduce_mean(empty).numel() == 0
+    with pytest.raises(covap.InvalidInput):
+        covap.allreduce_mean(torch.zeros(4, dtype=dtype, device=DEV), None,
+                             out=torch.zeros(3, dtype=dtype, device=DEV))
+    comm.close()
+
+
+def test_allreduce_mean_rows_bit_exact_vs_reference(covap, ref):
+    """The kernel behind the C++ drop-in covap::allreduce_mean
+    (covap_cxx.cpp -> covap_mean_rows): P = 1..8 in-process worker vectors,
+    fp64, against the reference's own allreduce_mean, bit for bit; plus the
+    reference's known answers (test_trainer.cpp:45-49)."""
+    import ctypes
+    from paper_2311_04499_b200 import _lib as L
+
+    def mean_rows(rows):
+        rows = np.ascontiguousarray(rows, np.float64)
+        P, n = rows.shape
+        d_rows = torch.from_numpy(rows.reshape(-1).copy()).to(DEV)
+        d_out = torch.empty(n, dtype=torch.float64, device=DEV)
+        L.lib().covap_mean_rows(0, L.F64, ctypes.c_void_p(d_rows.data_ptr()),
+                                ctypes.c_void_p(d_out.data_ptr()), P, n, None)
+        torch.cuda.synchronize()
+        return d_out.cpu().numpy()
+
+    assert mean_rows([[1, 2], [3, 4]]).tolist() == [2, 3]
+    assert mean_rows([[5, 6, 7]]).tolist() == [5, 6, 7]
+    for P in range(1, 9):
+        for n in (1, 5, 4099, 300_007):
+            rows = np.stack([_signed_zero_input(n, torch.float64, 100 * P + w).numpy()
+                             * (10.0 ** (w - 3)) for w in range(P)])
+            rows[:, 3::13] = -0.0  # all-negative-zero columns: the reference gives +0.0
+            got, want = mean_rows(rows), ref.allreduce_mean(rows)
+            assert np.array_equal(bits(got), bits(want)), (P, n)
+
+
+# ------------------------------------------------------------------ fp32 vs the fp64 reference
+
+@pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 4), ("bert_large", 4)])
+def test_fp32_path_normwise_vs_fp64_reference(covap, orc, name, K):
+    """the fp32 sync path against the REFERENCE's fp64
+    covap_compress / allreduce_mean / covap_decompress (compress.cpp:50-103,
+    trainer.cpp:35-47; oracle/_ref, else its pinned fp64 restatement) on the
+    same gradients widened to fp64, default EF schedule (0.3, 100, 0.1), full
+    BASELINE layouts: ||a - b||_2 / ||b||_2 <= 1e-6 for the synchronised
+    gradient and the residual arena at every step of a K + 1 step run.
+    (Per-element relative error is unbounded — cancellation in g + c*r —
+    so the north star's 1e-6 is normwise; SURVEY §7 hard part 1.)"""
+    from oracle.oracle import REF_SO, Ref, RefSession
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    sync = covap.CovapSync(plan, None, torch.float32, 0)  # default EfSchedule
+    numels = [t.numel() for t in plan.tensors]
+    tensors = [(t.bucket, t.begin, t.end) for t in plan.tensors]
+    d = plan.total_numel()
+    sess = RefSession(Ref(), numels, 1, K) if os.path.exists(REF_SO) else None
+    r64 = np.zeros(d)
+    g, out = torch.empty(d, device=DEV), torch.empty(d, device=DEV)
+
+    def rel(a, b):
+        nb = np.linalg.norm(b)
+        return np.linalg.norm(a.astype(np.float64) - b) / (nb if nb > 0 else 1.0)
+
+    worst = 0.0
+    for s in range(K + 1):
+        covap.generate(g, covap.stream_key(61, 0, s))
+        sync.sync(g, out)
+        g64 = g.cpu().numpy().astype(np.float64)
+        if sess is not None:
+            upd, res, _ = sess.step(g64[None, :], want_residual=True)
+        else:
+            keep = orc.select(s, K, len(tensors))
+            p = orc.compress(g64, r64, tensors, keep, 1, orc.ef_coefficient(s))
+            upd = orc.decompress(orc.allreduce_mean(p[None, :]) if len(p) else p, tensors, keep,
+                                 d, np.float64)
+            res = r64
+        torch.cuda.synchronize()
+        e_out = rel(out.cpu().numpy(), upd)
+        e_res = rel(sync.state.residuals.cpu().numpy(), res)
+        worst = max(worst, e_out, e_res)
+        assert e_out <= 1e-6 and e_res <= 1e-6, (s, e_out, e_res)
+    if sess is not None:
+        sess.close()
+    assert worst > 0.0  # fp32 really differs from fp64 (the comparison is not vacuous)
+
+
+# ------------------------------------------------------------------ ADVICE r1: buffer parity
+
+@pytest.mark.parametrize("fused", [0, 1], ids=["gather", "fused"])
+def test_peer_back_to_back_across_empty_phases(covap, orc, fused):
+    """ResNet-50 at K = 8 has empty phases 5-7 (no collective, no barrier):
+    steps 4 and 12 and 8 and 16 must still not share a send buffer a slower
+    peer may be reading.  Two virtual ranks run 17 steps back to back with
+    no host synchronisation; every step's output (copied aside on each rank's
+    stream) and the final residuals equal the rank-ordered oracle."""
+    K, P, S = 8, 2, 17
+    plan = covap.plan_for(covap.load_layout("resnet50"), covap.CovapConfig(interval=K))
+    ef = covap.EfSchedule(True, 0.3, 1, 0.2)
+    states, groups, streams = _virtual_ranks(covap, plan, P, torch.float32, ef, fused)
+    d = plan.total_numel()
+    tensors = [(t.bucket, t.begin, t.end) for t in plan.tensors]
+    grads = [[dev_gen(covap, orc.stream_key(17, w, s), d, 0, torch.float32) for s in range(S)]
+             for w in range(P)]
+    outs = [[torch.empty(d, device=DEV) for _ in range(S)] for _ in range(P)]
+    tmp = [torch.empty(d, device=DEV) for _ in range(P)]
+    torch.cuda.synchronize()
+    for s in range(S):
+        for w in range(P):
+            groups[w].sync(grads[w][s], tmp[w], streams[w])
+            with torch.cuda.stream(streams[w]):
+                outs[w][s].copy_(tmp[w])
+        if s % 3 == 0:  # rank 1 falls behind: give rank 0 a head start
+            streams[1].wait_stream(streams[1])
+            covap.spin(300.0, 1, streams[1])
+    torch.cuda.synchronize()
+    for g in groups:
+        g.check()
+    rs = [np.zeros(d, np.float32) for _ in range(P)]
+    for s in range(S):
+        keep = orc.select(s, K, len(tensors))
+        coeff = np.float32(orc.ef_coefficient(s, 0.3, 1, 0.2))
+        pays = [orc.compress(grads[w][s].cpu().numpy(), rs[w], tensors, keep, 1, coeff)
+                for w in range(P)]
+        mean = orc.allreduce_mean(np.stack(pays)) if len(pays[0]) else pays[0]
+        want = orc.decompress(mean, tensors, keep, d, np.float32)
+        for w in range(P):
+            assert np.array_equal(bits(outs[w][s].cpu().numpy()), bits(want)), (s, w)
+    for w in range(P):
+        assert np.array_equal(bits(states[w].residuals.cpu().numpy()), bits(rs[w]))
