@@ -255,6 +255,26 @@ std::vector<double> allreduce_mean(const std::vector<std::vector<double>>& per_w
 double ccr(double comm_ms, double comp_ms);
 std::uint32_t choose_interval(double ccr_value);
 
+// overlap_schedule (perf.hpp:37-58, perf.cpp:63-103): the exact overlapped
+// iteration of per-tensor compute / compression / communication times.
+struct ScheduleBubble {
+  std::int64_t after_tensor = 0;
+  double duration_ms = 0.0;
+};
+struct OverlapSchedule {
+  double total_ms = 0.0;
+  double stream_end_ms = 0.0;
+  double unoverlapped_comm_ms = 0.0;
+  std::vector<double> comm_start_ms;  // communicated tensors only
+  std::vector<double> comm_end_ms;
+  std::vector<std::int64_t> comm_tensor;
+  std::vector<ScheduleBubble> bubbles;
+};
+OverlapSchedule overlap_schedule(double before_ms, std::span<const double> comp_ms,
+                                 std::span<const double> compress_ms,
+                                 std::span<const double> comm_ms,
+                                 const std::vector<bool>& communicated = {});
+
 enum class EventKind { kComputeStart, kComputeEnd, kCompressStart, kCompressEnd, kCommStart, kCommEnd };
 struct Event {
   EventKind kind;
@@ -262,9 +282,13 @@ struct Event {
   std::uint32_t worker;
   double time_ms;
 };
+// One worker's (or every worker's) trace of an iteration (sim.hpp:45-52).
 struct IterationTimeline {
   std::vector<Event> events;
   double t_total_ms = 0.0;
+  std::vector<ScheduleBubble> bubbles;
+  double unoverlapped_comm_ms = 0.0;
+  std::uint64_t transmitted_bytes = 0;
 };
 struct ProfileResult {
   double ccr = 0.0;
@@ -275,6 +299,21 @@ struct ProfileResult {
 };
 ProfileResult profile_ccr(std::span<const IterationTimeline> per_worker,
                           std::uint32_t expected_workers);
+
+// ------------------------------------------------------------------ settings (a17)
+// The "covap" section of an experiment document (config.cpp:133-157),
+// parsed natively (covap_settings_from_json): ConfigError with the field
+// path on a bad value; the document's other sections are not read.
+struct CovapSettings {
+  std::uint32_t interval = 1;
+  bool auto_interval = false;  // "auto": K = choose_interval(measured CCR)
+  SelectionRule rule = SelectionRule::kMatchStep;
+  EfSchedule ef;
+  CovapConfig config(std::uint32_t k) const { return CovapConfig{k, rule, ef}; }
+};
+CovapSettings covap_settings_from_json(const std::string& document);
+// resolve_interval (config.cpp:238-241)
+std::uint32_t resolve_interval(const CovapSettings& settings, double ccr_value);
 
 // ------------------------------------------------------------------ device-resident API
 namespace b200 {
@@ -327,11 +366,33 @@ class Sync {
   Sync(const Plan& plan, const Comm* comm, int dtype, int device, const EfSchedule& ef);
   void step(const void* grad, void* out, void* stream);                   // covap_sync_step
   void bucket_ready(std::size_t bucket, const void* grad, void* out, void* stream);
+  void dense_bucket_ready(std::size_t bucket, void* grad, void* out, void* stream);
   void finish(void* stream);
+  // Per bucket: this rank's arrival -> completion time of its last
+  // collective, ms (-1: none ran).  Blocks on the side stream.
+  std::vector<double> last_comm_ms();
   State& state() { return state_; }
 
  private:
   State state_;
+  covap_comm* comm_;
+  std::size_t n_buckets_;
+};
+
+// The CCR-driven choice of K on a live job (PAPER §IV-B, sim.cpp:164-216,
+// perf.cpp:40-53): profile one dense iteration through Sync with the
+// dense_bucket_ready schedule, then decide() with this rank's per-bucket
+// durations and backward time — rank-min exchange over the communicator,
+// rank 0's compute time; every rank gets the same result.
+class CcrController {
+ public:
+  explicit CcrController(const Comm* comm) : comm_(comm ? comm->get() : nullptr) {}
+  ProfileResult decide(const std::vector<double>& own_comm_ms, double own_comp_ms) const;
+  // "auto" -> the decided K, else the configured one (config.cpp:238-241).
+  std::uint32_t interval(const CovapSettings& settings, const std::vector<double>& own_comm_ms,
+                         double own_comp_ms) const;
+
+ private:
   covap_comm* comm_;
 };
 

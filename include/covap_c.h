@@ -185,6 +185,17 @@ covap_status covap_filter_pack(covap_state* state, const void* grad, void* send,
  * out may alias the gradient passed to K1. */
 covap_status covap_unpack(covap_state* state, const void* recv, void* out, double scale, int mean,
                           size_t b0, size_t b1, void* stream);
+/* The split the multi-rank sync step uses (covap_sync_step, covap_bucket_ready,
+ * the peer modes): the zero fill of the unselected output moves into K1,
+ * ahead of the allreduce, and the unpack after it touches only the selected
+ * slots — so the part of the step that waits for the collective is 8S bytes,
+ * not 4N + 4S, and a bucket with no selected shard needs no unpack at all.
+ *   covap_filter_pack_zero: covap_filter_pack + out[unsel] = 0 (out may alias grad);
+ *   covap_unpack_selected:  out[sel] = (0 + recv) * scale, unselected slots untouched. */
+covap_status covap_filter_pack_zero(covap_state* state, const void* grad, void* send, void* out,
+                                    size_t b0, size_t b1, void* stream);
+covap_status covap_unpack_selected(covap_state* state, const void* recv, void* out, double scale,
+                                   size_t b0, size_t b1, void* stream);
 /* K1F: K1 and K2 fused for a single rank over buckets [b0, b1): selected ->
  * out = (0 + c) * scale and r = 0, unselected -> r = c and out = 0.  Equal to
  * covap_filter_pack + covap_unpack(mean = 1) when the allreduce is the
@@ -288,6 +299,47 @@ covap_status covap_allreduce(covap_comm* comm, void* buf, uint64_t count, int dt
  * (sim.cpp:208-211).  Blocking.  comm NULL -> single rank. */
 covap_status covap_comm_profile_exchange(covap_comm* comm, const double* dur, size_t n_coll,
                                          double comp_ms, double* aligned_ms, double* comp_out);
+
+/* ------------------------------------ settings and the CCR controller --
+ * SURVEY.md §8 rows a14-a17.  covap_settings mirrors the "covap" section of
+ * the reference's experiment document (config.cpp:133-157): interval (an
+ * integer >= 1, or "auto"), selection ("narrative" = kMatchStep, "formula" =
+ * kPlusStep) and ef {enabled, init_value, ascend_steps, ascend_range}. */
+typedef struct covap_settings {
+  uint32_t interval;     /* fixed K; meaningful when auto_interval == 0 */
+  int32_t auto_interval; /* 1: "auto", K = choose_interval(measured CCR) */
+  int32_t rule;          /* 0 kMatchStep ("narrative"), 1 kPlusStep ("formula") */
+  covap_ef ef;
+} covap_settings;
+
+/* The defaults: interval 1, narrative, EF (on, 0.3, 100, 0.1) (compress.hpp:27-40). */
+covap_status covap_settings_default(covap_settings* out);
+/* Parse a JSON document and read its "covap" object (absent -> defaults).
+ * Errors: COVAP_ERR_CONFIG with the reference's field path in the message,
+ * "config field 'covap.interval': must be >= 1" (config.cpp:17-19, 27-38,
+ * 133-157).  Other sections of the document are not read. */
+covap_status covap_settings_from_json(const char* document, covap_settings* out);
+/* resolve_interval (config.cpp:238-241): "auto" -> choose_interval(ccr),
+ * else the configured K. */
+covap_status covap_resolve_interval(const covap_settings* settings, double ccr, uint32_t* out);
+
+typedef struct covap_ccr_result { /* ProfileResult (sim.hpp:84-92), rank-independent part */
+  double ccr;
+  double comp_ms;
+  double comm_aligned_ms;
+  uint32_t recommended_interval;
+} covap_ccr_result;
+/* The live CCR controller (PAPER §IV-B; sim.cpp:164-216 on real events):
+ * own_comm_ms[c] = this rank's arrival -> completion time of collective c
+ * of one profiled dense iteration (covap_state_last_comm_ms; < 0 = did not
+ * run, counts 0), own_comp_ms = this rank's backward time.  The aligned time
+ * of c is the rank-MIN of the durations (completion is common, so the
+ * minimum is end - last arrival, sim.cpp:202-203), compute time is rank 0's
+ * (sim.cpp:208-211); CCR = comm / comp, K = max(1, ceil(CCR)) (perf.cpp:40-53).
+ * Every rank gets the same result.  Blocking (one NCCL min-reduce +
+ * broadcast).  comm NULL -> one rank. */
+covap_status covap_ccr_decide(covap_comm* comm, const double* own_comm_ms, size_t n_coll,
+                              double own_comp_ms, covap_ccr_result* out);
 
 /* ------------------------------------------- peer (NVLink) collective -- */
 /* C1 as one load/store kernel over peer memory instead of NCCL: two send

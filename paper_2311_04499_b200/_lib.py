@@ -46,6 +46,16 @@ class BucketRangeC(ctypes.Structure):
                 ("sel_end", u64), ("send_offset", u64), ("device_begin", u64)]
 
 
+class SettingsC(ctypes.Structure):
+    _fields_ = [("interval", u32), ("auto_interval", ctypes.c_int32), ("rule", ctypes.c_int32),
+                ("ef", EfC)]
+
+
+class CcrResultC(ctypes.Structure):
+    _fields_ = [("ccr", f64), ("comp_ms", f64), ("comm_aligned_ms", f64),
+                ("recommended_interval", u32)]
+
+
 class FilterC(ctypes.Structure):
     _fields_ = [("kind", i32), ("interval", u32), ("rule", i32), ("k_fraction", f64),
                 ("seed", u64)]
@@ -82,6 +92,8 @@ _SIGS = {
     "covap_state_set_pipeline": (None, [vp, i32]),
     "covap_state_reset": (None, [vp, vp]),
     "covap_filter_pack": (None, [vp, vp, vp, sz, sz, vp]),
+    "covap_filter_pack_zero": (None, [vp, vp, vp, vp, sz, sz, vp]),
+    "covap_unpack_selected": (None, [vp, vp, vp, f64, sz, sz, vp]),
     "covap_unpack": (None, [vp, vp, vp, f64, i32, sz, sz, vp]),
     "covap_filter_unpack": (None, [vp, vp, vp, f64, sz, sz, vp]),
     "covap_filter_sgd": (None, [vp, vp, vp, f64, f64, sz, sz, vp]),
@@ -108,6 +120,10 @@ _SIGS = {
     "covap_allreduce": (None, [vp, vp, u64, i32, vp]),
     "covap_comm_allreduce_mean": (None, [vp, i32, vp, vp, u64, vp]),
     "covap_comm_profile_exchange": (None, [vp, f64p, sz, f64, f64p, f64p]),
+    "covap_settings_default": (None, [ctypes.POINTER(SettingsC)]),
+    "covap_settings_from_json": (None, [ctypes.c_char_p, ctypes.POINTER(SettingsC)]),
+    "covap_resolve_interval": (None, [ctypes.POINTER(SettingsC), f64, ctypes.POINTER(u32)]),
+    "covap_ccr_decide": (None, [vp, f64p, sz, f64, ctypes.POINTER(CcrResultC)]),
     "covap_peer_create": (None, [vp, i32, i32, ctypes.POINTER(vp)]),
     "covap_peer_destroy": ("void", [vp]),
     "covap_peer_export": (None, [vp, ctypes.c_char_p, sz, ctypes.POINTER(sz)]),

@@ -421,23 +421,38 @@ class CompressorState:
         L.lib().covap_state_reset(self._h, _stream_ptr(stream, self.device))
 
     # -- kernels ---------------------------------------------------------
-    def filter_pack(self, grad, b0: int = 0, b1: Optional[int] = None, send=None, stream=None):
-        """K1 over buckets [b0, b1) at the current step."""
+    def filter_pack(self, grad, b0: int = 0, b1: Optional[int] = None, send=None, stream=None,
+                    out=None):
+        """K1 over buckets [b0, b1) at the current step.  With ``out``, K1 also
+        zero-fills the unselected output (the multi-rank step's split; pair
+        it with ``unpack(..., selected_only=True)``)."""
         self._check(grad)
         b1 = len(self.plan.buckets) if b1 is None else b1
-        L.lib().covap_filter_pack(self._h, _ptr(grad), None if send is None else _ptr(send),
-                                  int(b0), int(b1), _stream_ptr(stream, self.device))
+        snd = None if send is None else _ptr(send)
+        if out is None:
+            L.lib().covap_filter_pack(self._h, _ptr(grad), snd, int(b0), int(b1),
+                                      _stream_ptr(stream, self.device))
+        else:
+            self._check(out)
+            L.lib().covap_filter_pack_zero(self._h, _ptr(grad), snd, _ptr(out), int(b0), int(b1),
+                                           _stream_ptr(stream, self.device))
 
     def unpack(self, out, scale: float = 1.0, mean: bool = True, b0: int = 0,
-               b1: Optional[int] = None, recv=None, stream=None):
+               b1: Optional[int] = None, recv=None, stream=None, selected_only: bool = False):
         """K2 over buckets [b0, b1) at the current step: selected slots get
         (0 + recv) * scale (mean=True, allreduce_mean's order) or recv * scale
-        (mean=False, covap_decompress); the rest is zero-filled."""
+        (mean=False, covap_decompress); the rest is zero-filled — unless
+        ``selected_only`` (after a zero-filling K1: only the selected slots
+        are written, mean semantics)."""
         self._check(out)
         b1 = len(self.plan.buckets) if b1 is None else b1
-        L.lib().covap_unpack(self._h, None if recv is None else _ptr(recv), _ptr(out),
-                             float(scale), 1 if mean else 0, int(b0), int(b1),
-                             _stream_ptr(stream, self.device))
+        rcv = None if recv is None else _ptr(recv)
+        if selected_only:
+            L.lib().covap_unpack_selected(self._h, rcv, _ptr(out), float(scale), int(b0), int(b1),
+                                          _stream_ptr(stream, self.device))
+        else:
+            L.lib().covap_unpack(self._h, rcv, _ptr(out), float(scale), 1 if mean else 0,
+                                 int(b0), int(b1), _stream_ptr(stream, self.device))
 
     def filter_unpack(self, grad, out, scale: float = 1.0, b0: int = 0,
                       b1: Optional[int] = None, stream=None):
@@ -739,6 +754,68 @@ class TorchDistExchange:
         return d.cpu().tolist(), float(c.item())
 
 
+@dataclass
+class CovapSettings:
+    """The "covap" section of an experiment document (config.cpp:133-157):
+    ``interval`` (K >= 1) or ``auto_interval`` ("auto": K from the measured
+    CCR), the selection rule ("narrative" = kMatchStep, "formula" =
+    kPlusStep) and the EF schedule.  Parsed and validated natively
+    (covap_settings_from_json): ConfigError carries the field path."""
+    interval: int = 1
+    auto_interval: bool = False
+    rule: int = SelectionRule.kMatchStep
+    ef: EfSchedule = field(default_factory=EfSchedule)
+
+    @staticmethod
+    def from_json(doc) -> "CovapSettings":
+        text = doc if isinstance(doc, str) else json.dumps(doc)
+        c = L.SettingsC()
+        L.lib().covap_settings_from_json(text.encode(), ctypes.byref(c))
+        return CovapSettings._from_c(c)
+
+    @staticmethod
+    def _from_c(c) -> "CovapSettings":
+        return CovapSettings(int(c.interval), bool(c.auto_interval), int(c.rule),
+                             EfSchedule(bool(c.ef.enabled), c.ef.init_value, int(c.ef.ascend_steps),
+                                        c.ef.ascend_range))
+
+    def c(self):
+        return L.SettingsC(int(self.interval), 1 if self.auto_interval else 0, int(self.rule),
+                           self.ef.c())
+
+    def resolve_interval(self, ccr_value: float) -> int:
+        """resolve_interval (config.cpp:238-241)."""
+        c, k = self.c(), ctypes.c_uint32()
+        L.lib().covap_resolve_interval(ctypes.byref(c), float(ccr_value), ctypes.byref(k))
+        return k.value
+
+    def config(self, interval: Optional[int] = None) -> CovapConfig:
+        """The CovapConfig of a run once K is known."""
+        return CovapConfig(self.interval if interval is None else int(interval), self.rule, self.ef)
+
+
+def settings_from_json(doc) -> CovapSettings:
+    return CovapSettings.from_json(doc)
+
+
+def resolve_interval(settings: CovapSettings, ccr_value: float) -> int:
+    return settings.resolve_interval(ccr_value)
+
+
+def ccr_decide(comm: Optional["Communicator"], own_comm_ms: Sequence[float],
+               own_comp_ms: float) -> ProfileResult:
+    """The live CCR controller in the library (covap_ccr_decide): rank-min of
+    the per-collective arrival->completion durations over the communicator,
+    rank 0's compute time, CCR and K — the same result on every rank."""
+    n = len(own_comm_ms)
+    d = (ctypes.c_double * max(n, 1))(*[float(x) for x in own_comm_ms])
+    r = L.CcrResultC()
+    L.lib().covap_ccr_decide(None if comm is None else comm.handle, d, n, float(own_comp_ms),
+                             ctypes.byref(r))
+    return ProfileResult(r.ccr, r.comp_ms, r.comm_aligned_ms,
+                         [max(0.0, float(x)) for x in own_comm_ms], r.recommended_interval)
+
+
 class CcrController:
     """CCR-driven choice of K (PAPER §IV-B; perf.cpp:40-53, sim.cpp:164-216).
 
@@ -754,6 +831,8 @@ class CcrController:
         self.exchange = exchange
 
     def decide(self, own_comm_ms: Sequence[float], own_comp_ms: float) -> ProfileResult:
+        if isinstance(self.exchange, NcclExchange):  # all of it in the library
+            return ccr_decide(self.exchange.comm, own_comm_ms, own_comp_ms)
         durs = [max(0.0, float(x)) for x in own_comm_ms]
         aligned, comp0 = self.exchange(durs, own_comp_ms)
         comm = float(sum(aligned))

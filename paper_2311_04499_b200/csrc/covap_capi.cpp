@@ -80,13 +80,26 @@ double coeff_of(const covap_state* s) {
 }
 
 
+// K1 over [a, b).  out != NULL: K1 also writes the zero fill of the
+// unselected slots (compress.cpp:91) so that the unpack after the allreduce
+// (k2sel_range) touches only the selected ones.
 void k1_range(covap_state* s, const void* grad, void* send, uint64_t a, uint64_t b,
-              cudaStream_t st) {
+              cudaStream_t st, void* out = nullptr) {
   const size_t ph = s->num_steps % s->plan.interval;
   const int nr = static_cast<int>(s->plan.phases[ph].runs.size());
   CK(covapb::launch_filter_pack(s->dtype, grad, s->residual, send ? send : s->send,
                                 s->d_runs + s->phase_off[ph], nr, a, b, coeff_of(s),
-                                s->ef.enabled, st));
+                                s->ef.enabled, st, out));
+}
+
+// K2 over the selected slots of [a, b) only (after k1_range with out): no
+// launch at all when nothing in [a, b) is selected.
+void k2sel_range(covap_state* s, const void* recv, void* out, double inv, uint64_t a, uint64_t b,
+                 cudaStream_t st) {
+  const size_t ph = s->num_steps % s->plan.interval;
+  const auto& runs = s->plan.phases[ph].runs;
+  CK(covapb::launch_unpack(s->dtype, recv ? recv : s->send, out, s->d_runs + s->phase_off[ph],
+                           static_cast<int>(runs.size()), a, b, inv, 1, st, 0, runs.data()));
 }
 
 void k1f_range(covap_state* s, const void* grad, void* out, double inv, uint64_t a, uint64_t b,
@@ -501,6 +514,37 @@ covap_status covap_unpack(covap_state* s, const void* recv, void* out, double sc
   });
 }
 
+covap_status covap_filter_pack_zero(covap_state* s, const void* grad, void* send, void* out,
+                                    size_t b0, size_t b1, void* stream) {
+  return guarded([&] {
+    need(s && grad && out, "NULL argument");
+    need(b0 <= b1 && b1 <= s->plan.buckets.size(), "bucket range out of bounds");
+    need_aligned(grad, "grad");
+    need_aligned(out, "out");
+    if (send) need_aligned(send, "send");
+    if (b0 == b1) return;
+    DeviceGuard dg(s->device);
+    const uint64_t a = s->plan.buckets[b0].dbegin;
+    const uint64_t b = s->plan.buckets[b1 - 1].dbegin + s->plan.buckets[b1 - 1].numel;
+    k1_range(s, grad, send, a, b, as_stream(stream), out);
+  });
+}
+
+covap_status covap_unpack_selected(covap_state* s, const void* recv, void* out, double scale,
+                                   size_t b0, size_t b1, void* stream) {
+  return guarded([&] {
+    need(s != nullptr && out != nullptr, "NULL argument");
+    need(b0 <= b1 && b1 <= s->plan.buckets.size(), "bucket range out of bounds");
+    need_aligned(out, "out");
+    if (recv) need_aligned(recv, "recv");
+    if (b0 == b1) return;
+    DeviceGuard dg(s->device);
+    const uint64_t a = s->plan.buckets[b0].dbegin;
+    const uint64_t b = s->plan.buckets[b1 - 1].dbegin + s->plan.buckets[b1 - 1].numel;
+    k2sel_range(s, recv, out, scale, a, b, as_stream(stream));
+  });
+}
+
 covap_status covap_filter_unpack(covap_state* s, const void* grad, void* out, double scale,
                                  size_t b0, size_t b1, void* stream) {
   return guarded([&] {
@@ -621,7 +665,7 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
       CK(cudaEventRecord(s->done, st));
       CK(cudaStreamWaitEvent(s->comm_stream, s->done, 0));
       for (size_t g = 0; g < ng; ++g) {
-        k1_range(s, grad, nullptr, lo_of(g), hi_of(g), st);
+        k1_range(s, grad, nullptr, lo_of(g), hi_of(g), st, out);
         uint64_t lo = UINT64_MAX, hi = 0;
         const size_t b1 = g + 1 < ng ? first[g + 1] : bs.size();
         for (size_t b = first[g]; b < b1; ++b) {
@@ -640,14 +684,14 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
       }
       for (size_t g = 0; g < ng; ++g) {
         CK(cudaStreamWaitEvent(st, s->end[g], 0));
-        k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, lo_of(g), hi_of(g), st);
+        k2sel_range(s, nullptr, out, 1.0 / static_cast<double>(P), lo_of(g), hi_of(g), st);
       }
     } else {
-      k1_range(s, grad, nullptr, 0, n, st);
+      k1_range(s, grad, nullptr, 0, n, st, out);
       if (comm && ph.send_elems > 0)
         NK(ncclAllReduce(s->send, s->send, ph.send_elems, nccl_type(s->dtype), ncclSum,
                          comm->nccl, st));
-      k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, 0, n, st);
+      k2sel_range(s, nullptr, out, 1.0 / static_cast<double>(P), 0, n, st);
     }
     ++s->num_steps;
   });
@@ -714,7 +758,7 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
       if (P == 1 && s->fuse_single_rank) {
         k1f_range(s, dev_grad, dev_out, 1.0, a, b, st);
       } else {
-        k1_range(s, dev_grad, nullptr, a, b, st);
+        k1_range(s, dev_grad, nullptr, a, b, st, dev_out);
         // The chunk's selected elements occupy one contiguous envelope of the
         // send buffer (runs map monotonically); every rank derives the same
         // envelopes from the plan, so the collectives match.
@@ -729,7 +773,7 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
           NK(ncclAllReduce(static_cast<char*>(s->send) + lo * es,
                            static_cast<char*>(s->send) + lo * es, hi - lo, nccl_type(s->dtype),
                            ncclSum, comm->nccl, st));
-        k2_range(s, nullptr, dev_out, inv, 1, a, b, st);
+        k2sel_range(s, nullptr, dev_out, inv, a, b, st);
       }
       CK(cudaEventRecord(ek, st));
       CK(cudaStreamWaitEvent(s->d2h_stream, ek, 0));
@@ -764,7 +808,10 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
       s->tl_mode[bucket] = 0;
       return;
     }
-    k1_range(s, grad, nullptr, a, b, st);
+    // K1 also zero-fills the bucket's unselected output, so the side stream
+    // only carries the allreduce of the selected range and its unpack — and
+    // nothing at all for a bucket with no selected shard this step.
+    k1_range(s, grad, nullptr, a, b, st, out);
     CK(cudaEventRecord(s->ready[bucket], st));
     CK(cudaStreamWaitEvent(s->comm_stream, s->ready[bucket], 0));
     const uint64_t len = sel.sel_end - sel.sel_begin;
@@ -776,7 +823,7 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
                        static_cast<char*>(s->send) + sel.send_offset * s->esize, len,
                        nccl_type(s->dtype), ncclSum, comm->nccl, s->comm_stream));
     CK(cudaEventRecord(s->end[bucket], s->comm_stream));
-    k2_range(s, nullptr, out, 1.0 / static_cast<double>(P), 1, a, b, s->comm_stream);
+    k2sel_range(s, nullptr, out, 1.0 / static_cast<double>(P), a, b, s->comm_stream);
     if (s->timeline) CK(cudaEventRecord(s->k2e[bucket], s->comm_stream));
   });
 }
@@ -1342,7 +1389,7 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
       ++s->num_steps;
       return;
     }
-    k1_range(s, grad, buf, 0, n, st);
+    k1_range(s, grad, buf, 0, n, st, out);  // + zero fill of the unselected output
     ++p->epoch;
     if (ph.send_elems > 0) p->posted = p->epoch;
     if (ph.send_elems > 0) {
@@ -1364,12 +1411,12 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
       a.nruns = static_cast<int>(ph.runs.size());
       a.n_out = n;
       a.inv = 1.0 / static_cast<double>(p->P);
+      a.zfill = 0;  // K1 zeroed the unselected output
       CK(covapb::launch_peer_allreduce(s->dtype, a, p->max_ctas, st));
       ++p->launches;
     }
-    // fused: the collective already wrote out (C1 + K2 in one kernel)
-    if (!(p->mode == 1 && ph.send_elems > 0))
-      k2_range(s, buf, out, 1.0 / static_cast<double>(p->P), 1, 0, n, st);
+    // fused: the collective already wrote the selected output (C1 + K2 in one kernel)
+    if (p->mode != 1) k2sel_range(s, buf, out, 1.0 / static_cast<double>(p->P), 0, n, st);
     ++s->num_steps;
   });
 }

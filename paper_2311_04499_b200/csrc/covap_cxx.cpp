@@ -147,7 +147,8 @@ Comm::Comm(const std::vector<std::uint8_t>& id, int nranks, int rank, int device
 }
 
 Sync::Sync(const Plan& plan, const Comm* comm, int dtype, int device, const EfSchedule& ef)
-    : state_(plan, dtype, device, ef), comm_(comm ? comm->get() : nullptr) {}
+    : state_(plan, dtype, device, ef), comm_(comm ? comm->get() : nullptr),
+      n_buckets_(plan.info().n_buckets) {}
 
 void Sync::step(const void* grad, void* out, void* stream) {
   check(covap_sync_step(state_.get(), comm_, grad, out, stream));
@@ -157,7 +158,37 @@ void Sync::bucket_ready(std::size_t bucket, const void* grad, void* out, void* s
   check(covap_bucket_ready(state_.get(), comm_, bucket, grad, out, stream));
 }
 
+void Sync::dense_bucket_ready(std::size_t bucket, void* grad, void* out, void* stream) {
+  check(covap_dense_bucket_ready(state_.get(), comm_, bucket, grad, out, stream));
+}
+
 void Sync::finish(void* stream) { check(covap_step_finish(state_.get(), stream)); }
+
+std::vector<double> Sync::last_comm_ms() {
+  std::vector<double> d(n_buckets_);
+  if (!d.empty()) check(covap_state_last_comm_ms(state_.get(), d.data(), d.size()));
+  return d;
+}
+
+ProfileResult CcrController::decide(const std::vector<double>& own_comm_ms,
+                                    double own_comp_ms) const {
+  covap_ccr_result r{};
+  check(covap_ccr_decide(comm_, own_comm_ms.data(), own_comm_ms.size(), own_comp_ms, &r));
+  ProfileResult out;
+  out.ccr = r.ccr;
+  out.comp_ms = r.comp_ms;
+  out.comm_aligned_ms = r.comm_aligned_ms;
+  out.recommended_interval = r.recommended_interval;
+  for (double x : own_comm_ms) out.naive_comm_ms.push_back(x > 0.0 ? x : 0.0);
+  return out;
+}
+
+std::uint32_t CcrController::interval(const CovapSettings& settings,
+                                      const std::vector<double>& own_comm_ms,
+                                      double own_comp_ms) const {
+  if (!settings.auto_interval) return resolve_interval(settings, 0.0);
+  return resolve_interval(settings, decide(own_comm_ms, own_comp_ms).ccr);
+}
 
 }  // namespace b200
 
@@ -701,6 +732,58 @@ GradientSet ErrorFeedback::step(const GradientSet& gradients, const GradientFilt
   residuals_ = unflatten(rnew, numels_);
   ++num_steps_;
   return unflatten(kept, numels_);
+}
+
+OverlapSchedule overlap_schedule(double before_ms, std::span<const double> comp_ms,
+                                 std::span<const double> compress_ms,
+                                 std::span<const double> comm_ms,
+                                 const std::vector<bool>& communicated) {
+  const size_t n = comp_ms.size();
+  if (comm_ms.size() != n || (!compress_ms.empty() && compress_ms.size() != n) ||
+      (!communicated.empty() && communicated.size() != n))
+    throw InvalidInput("per-tensor lists have inconsistent lengths");
+  std::vector<std::uint8_t> sent(communicated.begin(), communicated.end());
+  OverlapSchedule o;
+  o.comm_start_ms.resize(n);
+  o.comm_end_ms.resize(n);
+  o.comm_tensor.resize(n);
+  std::vector<std::int64_t> after(n);
+  std::vector<double> bubble(n);
+  size_t nc = 0, nb = 0;
+  check(covap_overlap_schedule(before_ms, comp_ms.data(),
+                               compress_ms.empty() ? nullptr : compress_ms.data(), comm_ms.data(),
+                               sent.empty() ? nullptr : sent.data(), n, &o.total_ms,
+                               &o.stream_end_ms, &o.unoverlapped_comm_ms, o.comm_start_ms.data(),
+                               o.comm_end_ms.data(), o.comm_tensor.data(), &nc, after.data(),
+                               bubble.data(), &nb));
+  o.comm_start_ms.resize(nc);
+  o.comm_end_ms.resize(nc);
+  o.comm_tensor.resize(nc);
+  for (size_t i = 0; i < nb; ++i) o.bubbles.push_back(ScheduleBubble{after[i], bubble[i]});
+  return o;
+}
+
+CovapSettings covap_settings_from_json(const std::string& document) {
+  covap_settings c{};
+  check(::covap_settings_from_json(document.c_str(), &c));
+  CovapSettings s;
+  s.interval = c.interval;
+  s.auto_interval = c.auto_interval != 0;
+  s.rule = c.rule == 1 ? SelectionRule::kPlusStep : SelectionRule::kMatchStep;
+  s.ef = EfSchedule{c.ef.enabled != 0, c.ef.init_value, c.ef.ascend_steps, c.ef.ascend_range};
+  return s;
+}
+
+std::uint32_t resolve_interval(const CovapSettings& settings, double ccr_value) {
+  covap_settings c{};
+  c.interval = settings.interval;
+  c.auto_interval = settings.auto_interval ? 1 : 0;
+  c.rule = settings.rule == SelectionRule::kPlusStep ? 1 : 0;
+  c.ef = covap_ef{settings.ef.enabled ? 1 : 0, settings.ef.init_value, settings.ef.ascend_steps,
+                  settings.ef.ascend_range};
+  std::uint32_t k = 0;
+  check(covap_resolve_interval(&c, ccr_value, &k));
+  return k;
 }
 
 double ccr(double comm_ms, double comp_ms) {

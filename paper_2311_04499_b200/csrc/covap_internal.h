@@ -21,10 +21,13 @@ struct Run {
 
 constexpr uint64_t kSendAlign = 32;  // elements (128 B fp32, 256 B fp64)
 
-// K1: c = g + coeff*r for flat [a, b); selected -> send, r = 0; else r = c.
+// K1: c = g + coeff*r for flat [a, b); selected -> send, r = 0; else r = c
+// and, when out != NULL, out = 0 (the zero fill of covap_decompress,
+// compress.cpp:91, moved ahead of the allreduce so the unpack after it only
+// touches the selected slots).  out may alias g.
 cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, const Run* runs,
                                int nruns, uint64_t a, uint64_t b, double coeff, int ef,
-                               cudaStream_t s);
+                               cudaStream_t s, void* out = nullptr);
 // K1F (one rank, fused K1 + K2): selected -> out = (0 + c) * inv, r = 0;
 // unselected -> r = c, out = 0.  No send buffer: the allreduce over one rank
 // is the identity.
@@ -50,8 +53,12 @@ cudaError_t launch_unpack_sgd(int dtype, const void* recv, void* params, const R
                               cudaStream_t s);
 // K2: out = in-run ? f(recv[dst + e - begin]) : 0 for flat [a, b), with
 // f(x) = (0 + x) * inv when mean (allreduce_mean), x * inv otherwise.
+// zfill = 0: unselected slots are not written (K1 already zeroed them), and
+// the launch covers only the envelope of the selected runs in [a, b) —
+// nothing at all when none is selected.
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
-                          uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s);
+                          uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s,
+                          int zfill = 1, const Run* host_runs = nullptr);
 // allreduce_mean over P rows (P x n, worker-major) in worker order.
 cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,
                              cudaStream_t s, double inv = 0.0);
@@ -86,6 +93,7 @@ struct PeerArgs {
   int nruns;
   uint64_t n_out;   // device elements of out
   double inv;
+  int zfill;        // fused: zero the unselected slots too (0: K1 already did)
 };
 cudaError_t launch_peer_allreduce(int dtype, const PeerArgs& args, int max_ctas, cudaStream_t s);
 

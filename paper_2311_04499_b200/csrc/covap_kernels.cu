@@ -249,6 +249,7 @@ struct Args {
   int mean;        // K2: allreduce_mean semantics
   T lr;            // SGD variants: learning rate
   uint64_t te;     // elements per tile of this launch (set by the launcher)
+  int zfill;       // K2: zero-fill unselected slots (0: K1 did it); K1 (op 0): out != NULL zero-fills
   uint16_t* wire;  // fp16 (op 5): half bits of the kept values, or NULL
   unsigned long long* sat;  // fp16: saturation count (compress.cpp:185-190), or NULL
 };
@@ -290,7 +291,7 @@ __device__ __forceinline__ void element(const Args<T>& A, int& j, uint64_t e, T 
   const int k = run_at(A.runs, A.nruns, j, e);
   if (OP == 2 || OP == 4) {
     if (k < 0) {
-      if (OP == 2) A.out[e] = T(0);
+      if (OP == 2 && A.zfill) A.out[e] = T(0);
       return;
     }
     const T u = scale_of(A.recv[A.runs[k].dst + (e - A.runs[k].begin)], A.inv, A.mean);
@@ -308,7 +309,7 @@ __device__ __forceinline__ void element(const Args<T>& A, int& j, uint64_t e, T 
     A.r[e] = T(0);
   } else {
     A.r[e] = c;
-    if (OP == 1) A.out[e] = T(0);
+    if (OP == 1 || (OP == 0 && A.out)) A.out[e] = T(0);
   }
 }
 
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
             A.r[e] = T(0);
           } else {
             A.r[e] = c;
-            if (OP == 1) A.out[e] = T(0);
+            if (OP == 1 || (OP == 0 && A.out)) A.out[e] = T(0);
           }
         };
         const uint64_t body = vec_ok ? nv : 0;
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
             *reinterpret_cast<V*>(A.r + e) = z;
           } else {
             *reinterpret_cast<V*>(A.r + e) = x;
-            if (OP == 1) *reinterpret_cast<V*>(A.out + e) = z;
+            if (OP == 1 || (OP == 0 && A.out)) *reinterpret_cast<V*>(A.out + e) = z;
           }
         }
         if (in_run) ++j;
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
         bulk_store(A.r + e0, zero, bytes);    // residual reset (compress.cpp:77)
       } else if (sel.cls == kNone) {
         bulk_store(A.r + e0, st, bytes);      // r = compensated (compress.cpp:79)
-        if (OP == 1) bulk_store(A.out + e0, zero, bytes);
+        if (OP == 1 || (OP == 0 && A.out)) bulk_store(A.out + e0, zero, bytes);  // compress.cpp:91
       }
       bulk_commit();  // one group per tile (possibly empty)
       if (k + kStages < my) issue(k + kStages);  // input slot s is consumed
@@ -660,8 +661,8 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
     const uint64_t e0 = tile_lo(k), e1 = min(e0 + te, b16);
     const uint32_t n = static_cast<uint32_t>(e1 - e0);
     const TileSel sel = classify<T>(A.runs, A.nruns, e0, e1);
-    if (sel.cls == kNone) {  // zero fill (compress.cpp:91); SGD: nothing to do
-      if (!SGD && threadIdx.x == 0) bulk_store(A.out + e0, zero, n * sizeof(T));
+    if (sel.cls == kNone) {  // zero fill (compress.cpp:91); SGD or K1-filled: nothing to do
+      if (!SGD && A.zfill && threadIdx.x == 0) bulk_store(A.out + e0, zero, n * sizeof(T));
 #ifdef COVAP_K2_TRACE
       ++tr_none;
 #endif
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
             }
           }
           ++j;
-        } else if (!SGD) {  // zero fill; tiles are 16-byte aligned, segments need not be
+        } else if (!SGD && A.zfill) {  // zero fill; tiles are 16-byte aligned, segments need not be
           T* dst = A.out + pos;
           const uint64_t len = end - pos;
           const uint64_t mis = (reinterpret_cast<uintptr_t>(dst) / sizeof(T)) % W;
@@ -949,6 +950,7 @@ Args<T> make_args(const void* g, void* r, void* send, void* out, const void* rec
   A.mean = mean;
   A.lr = static_cast<T>(lr);
   A.te = 0;  // set by balance()
+  A.zfill = 1;
   A.wire = nullptr;
   A.sat = nullptr;
   return A;
@@ -1005,8 +1007,8 @@ cudaError_t pass_dt(int dtype, int op, cudaStream_t s, X... x) {
 
 cudaError_t launch_filter_pack(int dtype, const void* g, void* r, void* send, const Run* runs,
                                int nruns, uint64_t a, uint64_t b, double coeff, int ef,
-                               cudaStream_t s) {
-  return pass_dt(dtype, 0, s, g, r, send, nullptr, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1, 0.0);
+                               cudaStream_t s, void* out) {
+  return pass_dt(dtype, 0, s, g, r, send, out, nullptr, runs, nruns, a, b, coeff, ef, 1.0, 1, 0.0);
 }
 
 cudaError_t launch_filter_unpack(int dtype, const void* g, void* r, void* out, const Run* runs,
@@ -1023,9 +1025,31 @@ cudaError_t launch_filter_sgd(int dtype, const void* g, void* r, void* params, c
 }
 
 cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* runs, int nruns,
-                          uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s) {
-  return pass_dt(dtype, 2, s, nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
-                 mean, 0.0);
+                          uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s, int zfill,
+                          const Run* host_runs) {
+  if (!zfill) {
+    // Only the selected slots: shrink [a, b) to the envelope of the runs
+    // that meet it (host copy of the run table), launch nothing if none does.
+    if (host_runs == nullptr) return cudaErrorInvalidValue;
+    uint64_t lo = UINT64_MAX, hi = 0;
+    for (int j = 0; j < nruns; ++j) {
+      const uint64_t x0 = std::max(a, host_runs[j].begin), x1 = std::min(b, host_runs[j].end);
+      if (x0 >= x1) continue;
+      lo = std::min(lo, x0);
+      hi = std::max(hi, x1);
+    }
+    if (hi <= lo) return cudaSuccess;
+    a = lo;
+    b = hi;
+  }
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    Args<T> A = make_args<T>(nullptr, nullptr, nullptr, out, recv, runs, nruns, a, b, 0.0, 0, inv,
+                             mean, 0.0);
+    A.zfill = zfill;
+    return pass<T>(2, A, s);
+  };
+  return dtype == 0 ? go(float(0)) : go(double(0));
 }
 
 cudaError_t launch_unpack_sgd(int dtype, const void* recv, void* params, const Run* runs,

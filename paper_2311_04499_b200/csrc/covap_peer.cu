@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
       return v >= nvec ? P - 1 : static_cast<int>(v / per);
     };
     auto zero_range = [&](uint64_t a, uint64_t b) {
-      if (a >= b) return;
+      if (a >= b || !args.zfill) return;
       const uint64_t a16 = umin(b, (a + W - 1) / W * W), b16 = umax(a16, b / W * W);
       if (blockIdx.x == 0)
         for (uint64_t e = a + threadIdx.x; e < a16; e += kPeerThreads) out[e] = T(0);

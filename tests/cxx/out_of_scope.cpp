@@ -1,7 +1,16 @@
-// Stubs for tests/cxx/out_of_scope.hpp — TEST INFRASTRUCTURE ONLY.
+// Definitions for tests/cxx/out_of_scope.hpp — TEST INFRASTRUCTURE ONLY.
+//
+// Most entries throw: the cases that reach them are skipped by name.  Three
+// are restated because hot-path cases use them as fixture generators or
+// reference values (see the header): the rendezvous event loop + worker
+// views (traces for profile_ccr), t_ovlp_totals (the closed form the
+// overlap_schedule case compares with), and the "covap" section of
+// config_from_json + resolve_interval, which go through the library.
 #include "out_of_scope.hpp"
 
+#include <algorithm>
 #include <nlohmann/json.hpp>
+#include <tuple>
 
 namespace covap {
 namespace {
@@ -9,8 +18,167 @@ namespace {
   throw Error(std::string("out of scope for the B200 hot path: ") + what);
 }
 }  // namespace
+
 std::vector<double> split_compute_times(const ModelSpec&, const BucketPlan&, double) { oos("split_compute_times"); }
 ModelSpec model_from_json(const nlohmann::json&) { oos("model_from_json"); }
 nlohmann::json model_to_json(const ModelSpec&) { oos("model_to_json"); }
 nlohmann::json plan_to_json(const BucketPlan&) { oos("plan_to_json"); }
+
+// ---- perf model
+void PhaseTimes::validate() const { oos("PhaseTimes::validate"); }
+double t_dp(const PhaseTimes&) { oos("t_dp"); }
+double t_dp_ls(const PhaseTimes&) { oos("t_dp_ls"); }
+// The communication-bound overlap of Eq (2): the stream, plus whatever part
+// of the transfer outlasts the backward pass (perf.cpp:59-61).
+double t_ovlp_totals(double before_ms, double comp_ms, double comm_ms) {
+  const double tail = comm_ms > comp_ms ? comm_ms - comp_ms : 0.0;
+  return before_ms + comp_ms + tail;
+}
+double t_ovlp(const PhaseTimes&) { oos("t_ovlp"); }
+double t_gc(double, double, double, double) { oos("t_gc"); }
+double t_gc_ovlp(double, double, double, double) { oos("t_gc_ovlp"); }
+double speedup_fraction(double, double, double, double) { oos("speedup_fraction"); }
+SpeedupReport make_speedup_report(const PhaseTimes&, double) { oos("make_speedup_report"); }
+void add_expected_check(SpeedupReport&, const std::string&, double, double) { oos("add_expected_check"); }
+std::span<const BaselineCost> baseline_cost_table() { oos("baseline_cost_table"); }
+std::optional<BaselineCost> baseline_cost(const std::string&) { oos("baseline_cost"); }
+std::optional<BaselineCost> scaled_baseline_cost(const std::string&, std::uint64_t) { oos("scaled_baseline_cost"); }
+
+// ---- event simulator (fixture generator for the profiler cases)
+void ClusterConfig::validate() const {
+  if (workers < 1) throw InvalidInput("cluster needs at least one worker");
+  if (!skew_ms.empty() && skew_ms.size() != workers)
+    throw InvalidInput("skew vector length must equal the worker count");
+}
+double ClusterConfig::max_skew() const {
+  return skew_ms.empty() ? 0.0 : *std::max_element(skew_ms.begin(), skew_ms.end());
+}
+double comm_time_ms(std::uint64_t, const ClusterConfig&) { oos("comm_time_ms"); }
+const char* event_kind_name(EventKind) { oos("event_kind_name"); }
+
+// One iteration of P workers sharing one collective channel: each worker's
+// compute stream starts at its skew + before_ms; tensor i leaves the stream
+// at the start of its block (compression either extends the stream or runs
+// in a side lane that delays only that tensor); a collective starts at the
+// LAST worker's arrival (arrival = max(data ready, previous transfer end))
+// and ends at start + comm_ms for everyone.  Events sorted by (time, worker,
+// tensor, kind).  Restates sim.cpp:60-143 as a fixture generator.
+IterationTimeline simulate_iteration(double before_ms, std::span<const TensorWork> work,
+                                     const ClusterConfig& cluster, bool compress_on_stream) {
+  cluster.validate();
+  const std::uint32_t P = cluster.workers;
+  IterationTimeline tl;
+  std::vector<double> clock(P), last_busy(P);
+  for (std::uint32_t w = 0; w < P; ++w) clock[w] = last_busy[w] = cluster.skew(w) + before_ms;
+  double chan_end = 0.0;
+  bool chan_busy = false;
+  std::int64_t last_sent = -1;
+  auto emit = [&](EventKind k, std::int64_t t, std::uint32_t w, double at) {
+    tl.events.push_back(Event{k, t, w, at});
+  };
+  for (std::size_t i = 0; i < work.size(); ++i) {
+    const TensorWork& tw = work[i];
+    const auto t = static_cast<std::int64_t>(i);
+    std::vector<double> ready(P);
+    for (std::uint32_t w = 0; w < P; ++w) {
+      const double leave = clock[w];
+      ready[w] = leave;
+      emit(EventKind::kComputeStart, t, w, clock[w]);
+      clock[w] += tw.comp_ms;
+      emit(EventKind::kComputeEnd, t, w, clock[w]);
+      if (tw.compress_ms > 0.0 && compress_on_stream) {
+        emit(EventKind::kCompressStart, t, w, clock[w]);
+        clock[w] += tw.compress_ms;
+        emit(EventKind::kCompressEnd, t, w, clock[w]);
+      } else if (tw.compress_ms > 0.0) {
+        emit(EventKind::kCompressStart, t, w, leave);
+        emit(EventKind::kCompressEnd, t, w, leave + tw.compress_ms);
+        ready[w] = leave + tw.compress_ms;
+        last_busy[w] = std::max(last_busy[w], ready[w]);
+      }
+      last_busy[w] = std::max(last_busy[w], clock[w]);
+    }
+    if (!tw.communicate) continue;
+    std::vector<double> arrive(P);
+    double start = 0.0;
+    for (std::uint32_t w = 0; w < P; ++w) {
+      arrive[w] = chan_busy ? std::max(chan_end, ready[w]) : ready[w];
+      start = w == 0 ? arrive[w] : std::max(start, arrive[w]);
+    }
+    if (chan_busy && start > chan_end) tl.bubbles.push_back(ScheduleBubble{last_sent, start - chan_end});
+    const double end = start + tw.comm_ms;
+    for (std::uint32_t w = 0; w < P; ++w) {
+      emit(EventKind::kCommStart, t, w, arrive[w]);
+      emit(EventKind::kCommEnd, t, w, end);
+    }
+    chan_end = end;
+    chan_busy = true;
+    last_sent = t;
+    tl.transmitted_bytes += tw.wire_bytes;
+  }
+  double stream_end = last_busy.empty() ? before_ms : last_busy[0];
+  for (double b : last_busy) stream_end = std::max(stream_end, b);
+  tl.t_total_ms = chan_busy ? std::max(stream_end, chan_end) : stream_end;
+  tl.unoverlapped_comm_ms = std::max(0.0, tl.t_total_ms - stream_end);
+  std::sort(tl.events.begin(), tl.events.end(), [](const Event& a, const Event& b) {
+    return std::make_tuple(a.time_ms, a.worker, a.tensor, static_cast<int>(a.kind)) <
+           std::make_tuple(b.time_ms, b.worker, b.tensor, static_cast<int>(b.kind));
+  });
+  return tl;
+}
+
+IterationTimeline worker_view(const IterationTimeline& all, std::uint32_t worker) {
+  IterationTimeline v = all;
+  v.events.clear();
+  std::copy_if(all.events.begin(), all.events.end(), std::back_inserter(v.events),
+               [&](const Event& e) { return e.worker == worker; });
+  return v;
+}
+std::vector<IterationTimeline> worker_views(const IterationTimeline& all, std::uint32_t workers) {
+  std::vector<IterationTimeline> out;
+  for (std::uint32_t w = 0; w < workers; ++w) out.push_back(worker_view(all, w));
+  return out;
+}
+
+Scheme scheme_from_name(const std::string&) { oos("scheme_from_name"); }
+const char* scheme_name(Scheme) { oos("scheme_name"); }
+IterationInputs build_iteration_inputs(const ModelSpec&, const BucketPlan&, const ClusterConfig&,
+                                       const PhaseTimes&, const CompressorSpec&, std::uint64_t) {
+  oos("build_iteration_inputs");
+}
+
+// ---- toy trainer
+Objective objective_from_name(const std::string&) { oos("objective_from_name"); }
+const char* objective_name(Objective) { oos("objective_name"); }
+std::uint64_t ToyModelSpec::dimension() const { oos("ToyModelSpec::dimension"); }
+TrainRun train(const TrainConfig&) { oos("train"); }
+ContractionAudit contraction_audit(const TrainRun&, std::uint32_t) { oos("contraction_audit"); }
+
+// ---- config: only the "covap" section, through the library
+void ExperimentConfig::validate() const { oos("ExperimentConfig::validate"); }
+ExperimentConfig config_from_json(const nlohmann::json& j, const std::string&) {
+  if (!j.is_object()) throw ConfigError("config root must be a JSON object");
+  const CovapSettings s = covap_settings_from_json(j.dump());
+  ExperimentConfig c;
+  c.compressor.covap = s.config(s.interval);
+  c.covap_auto_interval = s.auto_interval;
+  return c;
+}
+ExperimentConfig load_config_file(const std::string&) { oos("load_config_file"); }
+std::string hash_json(const nlohmann::json&) { oos("hash_json"); }
+std::uint32_t resolve_interval(const ExperimentConfig& c, double ccr_value) {
+  CovapSettings s;
+  s.interval = c.compressor.covap.interval;
+  s.auto_interval = c.covap_auto_interval;
+  return resolve_interval(s, ccr_value);
+}
+
+// ---- experiment runner, reports
+ExperimentResult run_experiment(const ExperimentConfig&, unsigned) { oos("run_experiment"); }
+PhaseTimes resolve_phases(const ExperimentConfig&) { oos("resolve_phases"); }
+std::string format_table(const std::vector<std::string>&, const std::vector<std::vector<std::string>>&) {
+  oos("format_table");
+}
+std::string format_ms(double) { oos("format_ms"); }
+
 }  // namespace covap

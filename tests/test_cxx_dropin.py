@@ -1,12 +1,21 @@
-"""The reference's OWN unit tests (proj/tests/test_compress.cpp and
-test_model.cpp, compiled unchanged by tests/cxx/Makefile) against the B200
+"""The reference's OWN unit tests (proj/tests/test_compress.cpp,
+test_model.cpp, test_trainer.cpp, test_perf.cpp, test_sim.cpp and
+test_config.cpp, compiled unchanged by tests/cxx/Makefile) against the B200
 library's drop-in C++ headers (include/covap/) and libcovap_cxx.so.
 
 Skipped by name: the cases that exercise components outside the hot path
-(compute-time split, JSON I/O).  Every other case of the two files must pass:
-the planner/selection/EF ones on CPU; covap_compress / covap_decompress and
-the baseline compressors under the error-feedback wrapper (Top-k, Random-k,
-fp16, §8(f4)) on the GPU (fp64 kernels).
+(compute-time split, JSON I/O, the toy trainer, the
+closed-form perf model, the collective cost model, the experiment runner and
+the config system beyond its "covap" section).  Every other case must pass:
+the planner / selection / EF / ccr / choose_interval / profile_ccr /
+overlap_schedule / "auto" interval ones on CPU; covap_compress /
+covap_decompress / allreduce_mean and the baseline compressors under the
+error-feedback wrapper (Top-k, Random-k, fp16, §8(f4)) on the GPU.
+
+The profiler cases (test_sim.cpp:254-326) get their per-worker traces from
+the reference's rendezvous event loop, restated as a test fixture in
+tests/cxx/out_of_scope.cpp; SIM_FIXTURE lists the reference's own cases for
+that event loop, which pin the restatement.
 """
 import os
 import subprocess
@@ -21,6 +30,48 @@ OUT_OF_SCOPE = [
     "compute time split is proportional to elements",
     "declared layer times win over proportional split",
     "model JSON round trip",
+    # toy trainer (trainer.cpp:49-236, 257-443)
+    "threaded and sequential runs are bit-identical",
+    "interval one reproduces the dense run bit for bit",
+    "compensated run tracks dense; uncompensated run is worse",
+    "transmitted volume per window covers the dimension exactly once",
+    "quadratic objective converges to the dense minimizer",
+    "longer transmission intervals never help the quadratic benchmark",
+    "a runaway step size raises the divergence flag",
+    "zero steps yield an empty loss list",
+    "sharding path is exercised by an oversized layer",
+    "logistic regression learns",
+    "two-layer network learns under compression",
+    "windowed contraction ratios on a frozen snapshot",
+    "interval one never drops gradient mass",
+    "drop ratios from a real run stay within the contraction bound",
+    # closed-form perf model, cost table (perf.cpp:55-155, costs.cpp)
+    "serial iteration time",
+    "overlapped iteration time from totals",
+    "compressed iteration time",
+    "compressed and overlapped iteration time",
+    "speedup fraction",
+    "speedup fraction decreases in the ratio",
+    "published breakdown rows reproduce within tolerance",
+    "speedup ordering and time bounds hold on random inputs",
+    "overlap time is monotone in each input",
+    "per-tensor lists must sum to the totals",
+    # collective cost model, experiment runner (sim.cpp:28-35, 240-324; experiment.cpp)
+    "collective cost model",
+    "fitted efficiency reproduces the measured per-tensor shares",
+    "iteration inputs honor the compressor choice",
+    "ratio sweep flattens at the recommended interval",
+    "a ratio-four workload flattens at four",
+    "experiments are deterministic",
+    "worker sweep scales the declared communication volume",
+    # config system beyond the covap section, reports (config.cpp, report.cpp)
+    "a full document parses",
+    "bad fields carry their path in the error",
+    "sweep ranges expand",
+    "model can live in a separate file",
+    "the document hash is stable and content sensitive",
+    "train section populates the trainer configuration",
+    "table formatting pads columns",
 ]
 HOST_ONLY = [
     "selection walks tensors with the step",
@@ -44,6 +95,32 @@ HOST_ONLY = [
     "partition and slicing invariants on random models",
     "uncapped shards stay below twice the median",
     "identical inputs give identical plans",
+    # perf.hpp (test_perf.cpp:27-102): ccr, choose_interval, overlap_schedule
+    "communication-to-computation ratio",
+    "interval selection rounds the ratio up",
+    "per-tensor schedule with zero communication ends with the stream",
+    "per-tensor schedule tracks the busiest resource",
+    "uniform per-tensor schedule agrees with the totals form",
+    # sim.hpp: overlap_schedule vs the event loop, and the profiler (test_sim.cpp:171-197, 254-326)
+    "event loop equals the closed-form schedule on arbitrary inputs",
+    "profile equals the raw measurement without skew",
+    "rendezvous waiting inflates only the naive estimate",
+    "aligned profile is invariant to any skew vector",
+    "a communication-free iteration profiles as ratio zero",
+    "missing worker traces are rejected",
+    # config.cpp:238-241 through the library's covap-section parser (test_config.cpp:57-66)
+    "interval auto resolves through the measured ratio",
+]
+# the reference's own checks of its event loop, run against the restated fixture generator
+SIM_FIXTURE = [
+    "dense uniform iteration matches the totals approximation exactly",
+    "aligned transmission interval hides all communication",
+    "a tensor count not divisible by the interval leaves a small tail",
+    "side-lane compression delays only its own tensor",
+    "compute-bound iteration ends with the stream and shows bubbles",
+    "uniform configs match the totals approximation to nanoseconds",
+    "per-worker collectives never overlap",
+    "identical configs produce identical event lists",
 ]
 DEVICE = [
     "two-step compression trace with full compensation",
@@ -60,6 +137,8 @@ DEVICE = [
     "half precision conversion is idempotent",
     "shared feedback wrapper conserves mass for every scheme",
     "feedback wrapper with the tensor filter matches the fused compressor",
+    # allreduce_mean on the GPU (covap_mean_rows), test_trainer.cpp:45-49
+    "fixed-order mean reduction",
 ]
 
 
@@ -81,20 +160,20 @@ def test_case_inventory_is_complete():
     rc, out = run(["--only=__none__"])
     rc, out = run([])  # lists every case with PASS/FAIL (device ones may fail without a GPU)
     names = [l.split("] ", 1)[1] for l in out.splitlines() if l.startswith("[")]
-    assert sorted(names) == sorted(OUT_OF_SCOPE + HOST_ONLY + DEVICE)
+    assert sorted(names) == sorted(OUT_OF_SCOPE + HOST_ONLY + SIM_FIXTURE + DEVICE)
 
 
 def test_reference_host_cases_pass():
-    rc, out = run(["--only=" + "|".join(HOST_ONLY)])
+    rc, out = run(["--only=" + "|".join(HOST_ONLY + SIM_FIXTURE)])
     assert rc == 0, out
-    assert out.count("[PASS]") == len(HOST_ONLY)
+    assert out.count("[PASS]") == len(HOST_ONLY) + len(SIM_FIXTURE)
 
 
 @pytest.mark.gpu
 def test_reference_device_cases_pass_on_b200():
     rc, out = run(["--skip=" + "|".join(OUT_OF_SCOPE)])
     assert rc == 0, out
-    assert out.count("[PASS]") == len(HOST_ONLY) + len(DEVICE), out
+    assert out.count("[PASS]") == len(HOST_ONLY) + len(SIM_FIXTURE) + len(DEVICE), out
 
 
 # ------------------------------------------------ the device-resident C++ API

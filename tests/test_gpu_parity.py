@@ -687,7 +687,8 @@ def test_allreduce_mean_python_boundary(covap, orc, dtype):
             out = covap.allreduce_mean(buf, c)
             torch.cuda.synchronize()
             assert np.array_equal(bits(out.cpu().numpy()), bits(want)), (n, c)
-            assert not np.signbit(out.cpu().numpy()[::7]).any()
+            zeros = x.numpy() == 0
+            assert not np.signbit(out.cpu().numpy()[zeros]).any()  # -0.0 -> +0.0
             inplace = x.to(DEV)
             covap.allreduce_mean(inplace, c, out=inplace)
             torch.cuda.synchronize()
@@ -821,3 +822,43 @@ def test_peer_back_to_back_across_empty_phases(covap, orc, fused):
             assert np.array_equal(bits(outs[w][s].cpu().numpy()), bits(want)), (s, w)
     for w in range(P):
         assert np.array_equal(bits(states[w].residuals.cpu().numpy()), bits(rs[w]))
+
+
+# ------------------------------------------------------------------ K1 zero fill + selected-only K2
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 4), ("tablev", 19),
+                                    ("resnet50", 8), ("bert_large", 2)])
+def test_zero_filling_k1_and_selected_k2_equal_full_k2(covap, dtype, name, K):
+    """The multi-rank step's split — K1 also writes out = 0 for unselected
+    slots (compress.cpp:91 moved ahead of the allreduce), K2 then writes only
+    the selected slots — equals K1 -> full K2 bit for bit at every phase
+    (empty phases included), into a NaN-poisoned output and in place (out
+    aliasing the gradient, the DDP-bucket case)."""
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    ef = covap.EfSchedule(True, 0.3, 1, 0.2)
+    a = covap.CompressorState(plan, dtype, 0, ef)
+    b = covap.CompressorState(plan, dtype, 0, ef)
+    c = covap.CompressorState(plan, dtype, 0, ef)
+    d = plan.total_numel()
+    g = torch.empty(d, dtype=dtype, device=DEV)
+    oa = torch.empty(d, dtype=dtype, device=DEV)
+    ob = torch.empty(d, dtype=dtype, device=DEV)
+    for s in range(K + 1):
+        covap.generate(g, covap.stream_key(71, 0, s))
+        ob.fill_(float("nan"))
+        gc = g.clone()
+        a.filter_pack(g)
+        a.unpack(oa, 0.5, True)
+        b.filter_pack(g, out=ob)
+        b.unpack(ob, 0.5, True, selected_only=True)
+        c.filter_pack(gc, out=gc)  # in place
+        c.unpack(gc, 0.5, True, selected_only=True)
+        for st in (a, b, c):
+            st.step_end()
+        torch.cuda.synchronize()
+        assert torch.equal(oa, ob), s
+        assert torch.equal(oa, gc), s
+        assert torch.equal(a.residuals, b.residuals) and torch.equal(a.residuals, c.residuals)
+        se, _ = plan.send_elems(s)
+        assert torch.equal(a.send[:se], b.send[:se])
