@@ -125,3 +125,37 @@ TEST_CASE("device-resident API raises the reference's exception classes") {
   }
   CHECK(threw);
 }
+
+TEST_CASE("covap settings, resolve_interval and the CCR controller (host)") {
+  // the "covap" section of the reference's test document (test_config.cpp:18-39)
+  const std::string doc =
+      R"({"name": "unit", "covap": {"interval": "auto", "selection": "formula",
+          "ef": {"enabled": true, "init_value": 0.3, "ascend_steps": 10, "ascend_range": 0.1}}})";
+  const CovapSettings s = covap_settings_from_json(doc);
+  CHECK(s.auto_interval);
+  CHECK(s.rule == SelectionRule::kPlusStep);
+  CHECK(s.ef.ascend_steps == 10);
+  CHECK(resolve_interval(s, 2.5) == 3);  // test_config.cpp:59-60
+  CHECK(resolve_interval(s, 0.2) == 1);
+  const CovapSettings fixed = covap_settings_from_json(R"({"covap": {"interval": 7}})");
+  CHECK(resolve_interval(fixed, 2.5) == 7);
+  bool threw = false;
+  try {
+    covap_settings_from_json(R"({"covap": {"interval": 0}})");
+  } catch (const ConfigError& e) {
+    threw = std::string(e.what()).find("covap.interval") != std::string::npos;
+  }
+  CHECK(threw);
+  // one rank: the controller is ccr / choose_interval of the summed durations
+  const b200::CcrController ctl(nullptr);
+  const ProfileResult r = ctl.decide({100.0, -1.0, 180.0}, 135.0);
+  CHECK(r.comm_aligned_ms == 280.0);
+  CHECK(r.recommended_interval == 3);  // test_perf.cpp:36
+  CHECK(ctl.interval(s, {100.0, 180.0}, 135.0) == 3);
+  CHECK(ctl.interval(fixed, {100.0, 180.0}, 135.0) == 7);
+  // overlap_schedule over the C-ABI (perf.cpp:63-103; test_perf.cpp:67-81)
+  const std::vector<double> comp = {10, 10, 10}, comm = {4, 4, 4};
+  const OverlapSchedule o = overlap_schedule(7, comp, {}, comm, {});
+  CHECK(o.total_ms == 37);
+  CHECK(o.bubbles.size() == 2);
+}
