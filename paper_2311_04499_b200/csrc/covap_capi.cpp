@@ -1013,9 +1013,9 @@ covap_status covap_allreduce(covap_comm* c, void* buf, uint64_t count, int dtype
 covap_status covap_comm_allreduce_mean(covap_comm* c, int dtype, void* buf, void* out,
                                        uint64_t count, void* stream) {
   return guarded([&] {
-    need(buf && out, "NULL argument");
     need(dtype == COVAP_F32 || dtype == COVAP_F64, "bad dtype");
     if (count == 0) return;  // allreduce_mean of empty vectors is empty (trainer.cpp:40)
+    need(buf && out, "NULL argument");
     need_aligned(buf, "buf");
     need_aligned(out, "out");
     const int P = world(c);

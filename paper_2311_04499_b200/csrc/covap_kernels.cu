@@ -61,6 +61,12 @@ namespace {
 #ifndef COVAP_K2_TILE
 #define COVAP_K2_TILE 32768
 #endif
+#ifndef COVAP_K1_MIN_WAVES  // small ranges: shrink tiles until every SM gets this many
+#define COVAP_K1_MIN_WAVES 0
+#endif
+#ifndef COVAP_K2_MIN_WAVES
+#define COVAP_K2_MIN_WAVES 0
+#endif
 #ifndef COVAP_FILTER_THREADS  // threads per CTA of the K1 / K1F / K1F+SGD passes
 #define COVAP_FILTER_THREADS 256
 #endif
@@ -86,6 +92,7 @@ constexpr uint32_t kSmemK1Fp16 = 2 * kStages * kTileK1 + 2 * kStageFp16;
 constexpr uint32_t kTileK2 = COVAP_K2_TILE;
 constexpr int kStagesK2 = COVAP_K2_STAGES;
 constexpr uint32_t kSmemK2 = (kStagesK2 + 3) * kTileK2;
+constexpr uint32_t kSmemK2Sel = (kStagesK2 + 2) * kTileK2;  // ring + 2 staging tiles
 constexpr int kStagesK2Sgd = 2;
 constexpr uint32_t kSmemK2Sgd = (2 * kStagesK2Sgd + 3) * kTileK2;
 
@@ -803,6 +810,133 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_kernel(const Args<T> A) {
   }
 }
 
+// ------------------------------------------------------------ K2, selected slots only
+//
+// After a zero-filling K1 the unpack is a scaled gather of the allreduced
+// send buffer back into the layout: out[begin_j + i] = (0 + recv[dst_j + i])
+// * inv over the phase's runs.  It is tiled over the SEND space [o_lo, o_hi)
+// — the packed selected shards, contiguous up to the < 32-element alignment
+// gaps between runs — so every CTA streams the same number of bytes however
+// the selected shards are scattered over the layout (tiling the layout
+// instead left CTAs idle on unselected tiles: 0.45 of peak at BERT-large
+// K=4).  A tile is bulk-loaded into a kStagesK2-slot ring, scaled into a
+// staging tile and bulk-stored piece by piece (one piece per run it meets:
+// dst == begin (mod kSendAlign), so a piece is 16-byte aligned in both
+// spaces); scalar heads/tails only where a run or the [a, b) clip is not.
+
+template <typename T>
+struct SelArgs {
+  const T* recv;
+  T* out;
+  const Run* runs;
+  int nruns;
+  uint64_t o_lo, o_hi;  // send-space range of the launch (o_lo 16-byte aligned)
+  uint64_t a, b;        // layout clip (one bucket, or the whole arena)
+  uint64_t te;          // elements per tile (balanced)
+  T inv;
+  int mean;
+};
+
+// Run holding send offset o, or the first run after it (runs ascend in dst).
+__device__ __forceinline__ int run_by_dst(const Run* __restrict__ runs, int n, uint64_t o) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (runs[mid].dst + (runs[mid].end - runs[mid].begin) > o)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) unpack_sel_kernel(const SelArgs<T> A) {
+  constexpr uint32_t TE = kTileK2 / sizeof(T);
+  constexpr uint64_t W = 16 / sizeof(T);
+  using V = typename Vec16<T>::type;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* in = reinterpret_cast<T*>(smem);  // kStagesK2 tiles
+  T* stage = in + kStagesK2 * TE;      // 2 staging tiles
+  __shared__ __align__(8) uint64_t bar[kStagesK2];
+
+  pdl_launch_dependents();
+  const uint64_t te = A.te;
+  const uint64_t ntiles = (A.o_hi - A.o_lo + te - 1) / te;
+  const uint64_t my = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStagesK2; ++i) mbar_init(&bar[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_async_smem();
+  __syncthreads();
+  pdl_wait();  // the allreduce (or K1) wrote recv
+
+  auto tile_lo = [&](uint64_t k) { return A.o_lo + (blockIdx.x + k * gridDim.x) * te; };
+  auto issue = [&](uint64_t k) {  // thread 0
+    const int s = static_cast<int>(k % kStagesK2);
+    const uint64_t o0 = tile_lo(k), o1 = min(o0 + te, A.o_hi);
+    // whole 16-byte vectors only (a last tile ending mid-vector reads its
+    // few tail elements from global memory below)
+    const uint32_t bytes = static_cast<uint32_t>((o1 - o0) / W * W * sizeof(T));
+    mbar_arrive_tx(&bar[s], bytes);
+    if (bytes) bulk_load(in + s * TE, A.recv + o0, bytes, &bar[s]);
+  };
+  if (threadIdx.x == 0)
+    for (uint64_t k = 0; k < my && k < kStagesK2; ++k) issue(k);
+
+  for (uint64_t k = 0; k < my; ++k) {
+    const int s = static_cast<int>(k % kStagesK2);
+    const uint64_t o0 = tile_lo(k), o1 = min(o0 + te, A.o_hi);
+    const uint32_t nv = static_cast<uint32_t>((o1 - o0) / W);
+    T* st = stage + (k & 1) * TE;
+    if (threadIdx.x == 0) bulk_wait_read<1>();  // staging tile (k & 1) free again
+    mbar_wait(&bar[s], static_cast<uint32_t>((k / kStagesK2) & 1));
+    __syncthreads();
+    const V* xv = reinterpret_cast<const V*>(in + s * TE);
+    V* sv = reinterpret_cast<V*>(st);
+    for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
+      V x = xv[v];
+#pragma unroll
+      for (int q = 0; q < static_cast<int>(W); ++q) lane(x, q) = scale_of(lane(x, q), A.inv, A.mean);
+      sv[v] = x;
+    }
+    for (uint64_t i = nv * W + threadIdx.x; i < o1 - o0; i += kThreads)
+      st[i] = scale_of(A.recv[o0 + i], A.inv, A.mean);
+    fence_async_smem();
+    __syncthreads();
+    // the pieces of this tile: one per run it meets, clipped to [a, b)
+    const int j0 = run_by_dst(A.runs, A.nruns, o0);
+    for (int j = j0; j < A.nruns; ++j) {
+      const Run R = A.runs[j];
+      const uint64_t d1 = R.dst + (R.end - R.begin);
+      if (R.dst >= o1) break;
+      uint64_t ps = R.dst > o0 ? R.dst : o0, pe = d1 < o1 ? d1 : o1;  // send space
+      // clip to the layout range [a, b)
+      const uint64_t e_s = R.begin + (ps - R.dst);
+      if (e_s < A.a) ps += A.a - e_s;
+      if (R.begin + (pe - R.dst) > A.b) pe -= R.begin + (pe - R.dst) - A.b;
+      if (ps >= pe) continue;
+      const uint64_t e = R.begin + (ps - R.dst), n = pe - ps;
+      // e == ps (mod W) for the planner's runs: head up to the next vector
+      // boundary, bulk body, tail (a caller-built misaligned run: all scalar)
+      const bool aligned = (R.dst - R.begin) % W == 0;
+      const uint64_t head = !aligned ? n : (((W - e % W) % W) < n ? (W - e % W) % W : n);
+      const uint64_t body = (n - head) / W * W;
+      for (uint64_t i = threadIdx.x; i < head; i += kThreads) A.out[e + i] = st[ps - o0 + i];
+      for (uint64_t i = head + body + threadIdx.x; i < n; i += kThreads)
+        A.out[e + i] = st[ps - o0 + i];
+      if (threadIdx.x == 0 && body)
+        bulk_store(A.out + e + head, st + (ps - o0 + head), static_cast<uint32_t>(body * sizeof(T)));
+    }
+    if (threadIdx.x == 0) {
+      bulk_commit();
+      if (k + kStagesK2 < my) issue(k + kStagesK2);  // input slot s is consumed
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
 // ---------------------------------------------------------------- mean of rows
 // allreduce_mean for P in-process workers (trainer.cpp:41-45): out[i] =
 // ((0 + x_0[i]) + x_1[i] + ... + x_{P-1}[i]) * inv, in worker order.
@@ -903,7 +1037,9 @@ cudaError_t shape(DeviceShape** out) {
         (e = opt_in(unpack_kernel<float, false>, kSmemK2)) ||
         (e = opt_in(unpack_kernel<float, true>, kSmemK2Sgd)) ||
         (e = opt_in(unpack_kernel<double, false>, kSmemK2)) ||
-        (e = opt_in(unpack_kernel<double, true>, kSmemK2Sgd)))
+        (e = opt_in(unpack_kernel<double, true>, kSmemK2Sgd)) ||
+        (e = opt_in(unpack_sel_kernel<float>, kSmemK2Sel)) ||
+        (e = opt_in(unpack_sel_kernel<double>, kSmemK2Sel)))
       return e;
     s.ready = true;
   }
@@ -916,13 +1052,20 @@ cudaError_t shape(DeviceShape** out) {
 // 16-byte vectors, never above the smem tile) so that the vector range splits
 // into grid x m tiles: every CTA streams the same number of equal tiles and
 // no CTA is left with one extra tile at the end (a ~3% tail at ResNet-50 size).
+// Small ranges: at least min_tiles tiles (down to kMinTileBytes each), so a
+// few-MB pass still spreads over every SM instead of giving a handful of
+// CTAs one full-size tile each.
+constexpr uint64_t kMinTileBytes = 4096;
 template <typename T>
-unsigned balance(uint64_t a, uint64_t b, int sms, uint32_t tile_bytes, uint64_t* te) {
+unsigned balance(uint64_t a, uint64_t b, int sms, uint32_t tile_bytes, uint64_t* te,
+                 uint64_t min_tiles = 0) {
   constexpr uint64_t W = 16 / sizeof(T);
   const uint64_t a16 = (a + W - 1) / W * W, b16 = b / W * W;
   const uint64_t nvec = b16 > a16 ? (b16 - a16) / W : 0;
   const uint64_t max_vec = tile_bytes / 16;
-  const uint64_t tiles = std::max<uint64_t>(1, (nvec + max_vec - 1) / max_vec);
+  uint64_t tiles = std::max<uint64_t>(1, (nvec + max_vec - 1) / max_vec);
+  if (tiles < min_tiles)
+    tiles = std::max(tiles, std::min(min_tiles, nvec / (kMinTileBytes / 16)));
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(sms, tiles));
   const uint64_t m = (tiles + grid - 1) / grid;  // tiles per CTA
   const uint64_t vec = std::max<uint64_t>(1, (nvec + grid * m - 1) / (grid * m));
@@ -985,7 +1128,8 @@ cudaError_t pass(int op, const Args<T>& A, cudaStream_t s) {
   if (e) return e;
   const bool k1 = op == 0 || op == 1 || op == 3 || op == 5;
   Args<T> B = A;
-  const unsigned grid = balance<T>(A.a, A.b, sh->sms, k1 ? kTileK1 : kTileK2, &B.te);
+  const uint64_t min_tiles = static_cast<uint64_t>(sh->sms) * (k1 ? COVAP_K1_MIN_WAVES : COVAP_K2_MIN_WAVES);
+  const unsigned grid = balance<T>(A.a, A.b, sh->sms, k1 ? kTileK1 : kTileK2, &B.te, min_tiles);
   if (op == 5) B.te = (B.te + 7) / 8 * 8;  // wire tiles: 16-byte multiples of halves
   switch (op) {
     case 5: return launch(filter_kernel<T, 5>, grid, kSmemK1Fp16, s, B, filter_threads<5>());
@@ -1028,19 +1172,52 @@ cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* run
                           uint64_t a, uint64_t b, double inv, int mean, cudaStream_t s, int zfill,
                           const Run* host_runs) {
   if (!zfill) {
-    // Only the selected slots: shrink [a, b) to the envelope of the runs
-    // that meet it (host copy of the run table), launch nothing if none does.
+    // Only the selected slots: the send-space range of the runs that meet
+    // [a, b) (host copy of the run table); nothing to launch if none does.
+    if (nruns == 0 || b <= a) return cudaSuccess;  // nothing selected (an empty phase)
     if (host_runs == nullptr) return cudaErrorInvalidValue;
     uint64_t lo = UINT64_MAX, hi = 0;
     for (int j = 0; j < nruns; ++j) {
-      const uint64_t x0 = std::max(a, host_runs[j].begin), x1 = std::min(b, host_runs[j].end);
+      const Run& R = host_runs[j];
+      const uint64_t x0 = std::max(a, R.begin), x1 = std::min(b, R.end);
       if (x0 >= x1) continue;
-      lo = std::min(lo, x0);
-      hi = std::max(hi, x1);
+      lo = std::min(lo, R.dst + (x0 - R.begin));
+      hi = std::max(hi, R.dst + (x1 - R.begin));
     }
     if (hi <= lo) return cudaSuccess;
-    a = lo;
-    b = hi;
+    DeviceShape* sh;
+    cudaError_t e = shape(&sh);
+    if (e) return e;
+    auto go = [&](auto tag) {
+      using T = decltype(tag);
+      constexpr uint64_t W = 16 / sizeof(T);
+      SelArgs<T> A;
+      A.recv = static_cast<const T*>(recv);
+      A.out = static_cast<T*>(out);
+      A.runs = runs;
+      A.nruns = nruns;
+      A.o_lo = lo / W * W;  // the send buffer's runs start 16-byte aligned; keep tiles so
+      A.o_hi = hi;
+      A.a = a;
+      A.b = b;
+      A.inv = static_cast<T>(inv);
+      A.mean = mean;
+      const unsigned grid = balance<T>(A.o_lo, (A.o_hi + W - 1) / W * W, sh->sms, kTileK2, &A.te,
+                                       static_cast<uint64_t>(sh->sms) * COVAP_K2_MIN_WAVES);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = kSmemK2Sel;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = COVAP_PDL ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      const cudaError_t err = cudaLaunchKernelEx(&cfg, unpack_sel_kernel<T>, A);
+      return err != cudaSuccess ? err : cudaGetLastError();
+    };
+    return dtype == 0 ? go(float(0)) : go(double(0));
   }
   auto go = [&](auto tag) {
     using T = decltype(tag);

@@ -4,7 +4,7 @@
 DDP hands the hook one ``GradBucket`` at a time, in bucket index order, as
 backward produces them.  The hook runs the B200 path on the bucket's own
 buffer: K1 (filter_pack) on the producing stream, the allreduce of the
-bucket's selected shard and K2 (unpack, x1/P, zero fill) on the side stream
+bucket's selected shard and K2 (unpack, x1/P) on the side stream
 (``covap_bucket_ready_local``); the last bucket closes the step
 (``covap_step_finish``).  DDP's buckets are the reference's buckets: the plan
 is built with one "layer" per DDP bucket and a 1-byte cap, so
@@ -36,12 +36,15 @@ class CovapDDPHook:
     """State object for ``DistributedDataParallel.register_comm_hook``."""
 
     def __init__(self, config: CovapConfig, comm: Optional[Communicator] = None,
-                 device: Optional[int] = None, warmup: int = 2):
+                 device: Optional[int] = None, warmup: int = 2, fuse_single_rank: bool = True):
         torch = _torch()
         self.config = config
         self.comm = comm
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.warmup = int(warmup)
+        # one rank: the fused K1F pass on the producing stream (default), or the
+        # multi-rank schedule (K1 here, allreduce + unpack on the side stream)
+        self.fuse_single_rank = bool(fuse_single_rank)
         self.sync: Optional[CovapSync] = None
         self.plan: Optional[BucketPlan] = None
         self.iterations = 0
@@ -70,7 +73,8 @@ class CovapDDPHook:
         self.plan = BucketPlan(model, None, interval=self.config.interval, rule=self.config.rule,
                                shard=-1, pad=True)
         assert [b.numel for b in self.plan.buckets] == self._sizes
-        self.sync = CovapSync(self.plan, self.comm, _torch().float32, self.device, self.config.ef)
+        self.sync = CovapSync(self.plan, self.comm, _torch().float32, self.device, self.config.ef,
+                              fuse_single_rank=self.fuse_single_rank)
 
     # -- the hook ---------------------------------------------------------
     @staticmethod

@@ -57,6 +57,11 @@ def main():
     ap.add_argument("--intervals", default="1,4")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=6)
+    ap.add_argument("--schedules", default="fused,side",
+                    help="COVAP hook schedules at one rank: 'fused' (K1F on the producing stream) "
+                         "and/or 'side' (the multi-rank schedule through a 1-rank NCCL "
+                         "communicator: K1 on the producing stream, allreduce + K2 on the side "
+                         "stream)")
     args = ap.parse_args()
 
     import torch
@@ -75,7 +80,9 @@ def main():
     sk.close()
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     torch.backends.cudnn.benchmark = True
-    modes = ["dense"] + [int(k) for k in args.intervals.split(",")]
+    scheds = args.schedules.split(",")
+    modes = ["dense"] + [(int(k), sc) for k in args.intervals.split(",") for sc in scheds]
+    comm1 = covap.Communicator(covap.Communicator.unique_id(), 1, 0, 0) if "side" in scheds else None
     for name in args.models.split(","):
         res, info = {}, {}
         for mode in modes:
@@ -84,7 +91,9 @@ def main():
             model = DDP(net, device_ids=[0], bucket_cap_mb=25, gradient_as_bucket_view=True)
             hook = None
             if mode != "dense":
-                hook = CovapDDPHook(covap.CovapConfig(interval=mode), None, 0, warmup=2)
+                k, sc = mode
+                hook = CovapDDPHook(covap.CovapConfig(interval=k), comm1 if sc == "side" else None,
+                                    0, warmup=2, fuse_single_rank=sc == "fused")
                 model.register_comm_hook(hook, CovapDDPHook.hook)
             opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9)
 
@@ -115,10 +124,11 @@ def main():
         dense = res["dense"]
         line = {"model": name, "desc": desc + ", bf16 autocast, fp32 grads, SGD, DDP 25 MB buckets, 1 GPU",
                 "step_ms_dense": round(dense, 3)}
-        for k in modes[1:]:
-            line[f"step_ms_covap_K{k}"] = round(res[str(k)], 3)
-            line[f"overhead_K{k}"] = round((res[str(k)] - dense) / dense, 5)
-            line[f"hook_K{k}"] = info[str(k)]
+        for k, sc in modes[1:]:
+            key = str((k, sc))
+            line[f"step_ms_covap_K{k}_{sc}"] = round(res[key], 3)
+            line[f"overhead_K{k}_{sc}"] = round((res[key] - dense) / dense, 5)
+            line[f"hook_K{k}_{sc}"] = info[key]
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 

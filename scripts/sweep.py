@@ -51,9 +51,9 @@ while mb <= a.max_mb:
             if mode == "k1f":
                 st.filter_unpack(g, out)
             elif mode == "k1":
-                st.filter_pack(g)
+                st.filter_pack(g, out=out)  # + zero fill of the unselected output
             else:
-                st.unpack(out, 1.0, True)
+                st.unpack(out, 1.0, True, selected_only=True)
             st.step_end()
 
         # Kernel-only time: one K-cycle (every phase once) captured in a CUDA
@@ -83,7 +83,8 @@ while mb <= a.max_mb:
         for mode in ("k1f", "k1", "k2"):
             for _ in range(K):  # warm-up cycle
                 st.filter_unpack(grads[0], out) if mode == "k1f" else (
-                    st.filter_pack(grads[0]) if mode == "k1" else st.unpack(out, 1.0, True))
+                    st.filter_pack(grads[0], out=out) if mode == "k1" else
+                    st.unpack(out, 1.0, True, selected_only=True))
                 st.step_end()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -97,11 +98,11 @@ while mb <= a.max_mb:
                         st.filter_unpack(g, out)
                         byts += 16 * n
                     elif mode == "k1":
-                        st.filter_pack(g)
-                        byts += 12 * n + 4 * S
+                        st.filter_pack(g, out=out)
+                        byts += 16 * n
                     else:
-                        st.unpack(out, 1.0, True)
-                        byts += 4 * n + 4 * S
+                        st.unpack(out, 1.0, True, selected_only=True)
+                        byts += 8 * S
                     st.step_end()
             e1.record()
             torch.cuda.synchronize()
@@ -118,19 +119,23 @@ while mb <= a.max_mb:
 lines = ["# Synthetic bucket sweep (BASELINE config 5), one B200\n",
          "16 equal buckets of B MB (N = 16 B / 4 fp32 elements), S = N/K.  Fraction of the "
          f"measured {peak} GB/s copy peak.  K1F = fused single-rank sync (16N bytes); "
-         "K1 = filter_pack (12N + 4S); K2 = unpack (4N + 4S).  *graph*: one K-cycle "
+         "K1 = filter_pack with the output zero fill (16N); K2 = selected-only unpack (8S); "
+         "K1+K2 = the multi-rank kernels together (16N + 8S).  *graph*: one K-cycle "
          "captured in a CUDA graph and replayed (kernel time); *eager*: the same launches "
          "issued one by one from Python through the C-ABI (includes the host launch path, "
          "which dominates below ~8 MB buckets).\n",
          "| bucket | K | N (M elems) | K1F µs graph | K1F frac graph | K1F frac eager | K1 µs graph | "
-         "K1 frac graph | K1 frac eager | K2 µs graph | K2 frac graph | K2 frac eager |",
-         "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+         "K1 frac graph | K1 frac eager | K2 µs graph | K2 frac graph | K2 frac eager | "
+         "K1+K2 frac graph |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
 for mb, K, n, res in rows:
     c = []
     for m in ("k1f", "k1", "k2"):
         ms, gbs, gms, ggbs = res[m]
         c += [f"{gms * 1e3:.1f}", f"{ggbs / peak:.3f}", f"{gbs / peak:.3f}"]
-    lines.append(f"| {mb} MB | {K} | {n / 1e6:.1f} | " + " | ".join(c) + " |")
+    (m1, _, g1, gb1), (m2, _, g2, gb2) = res["k1"], res["k2"]
+    both = (gb1 * g1 + gb2 * g2) / (g1 + g2)  # bytes over the summed kernel time
+    lines.append(f"| {mb} MB | {K} | {n / 1e6:.1f} | " + " | ".join(c) + f" | {both / peak:.3f} |")
 os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
 with open(a.out, "w") as f:
     f.write("\n".join(lines) + "\n")

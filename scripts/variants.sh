@@ -12,12 +12,25 @@ declare -A V=(
   [base]=""
   [nopdl]="-DCOVAP_PDL=0"
   [k1t16]="-DCOVAP_K1_TILE=16384"
+  [k2w1]="-DCOVAP_K2_MIN_WAVES=1"
+  [k2w2]="-DCOVAP_K2_MIN_WAVES=2"
+  [k2w4]="-DCOVAP_K2_MIN_WAVES=4"
+  [k12w2]="-DCOVAP_K1_MIN_WAVES=2 -DCOVAP_K2_MIN_WAVES=2"
+  [k2t16]="-DCOVAP_K2_TILE=16384 -DCOVAP_K2_STAGES=6"
 )
 if [ "$1" = "build" ]; then
   for name in "${!V[@]}"; do
     out=$ROOT/paper_2311_04499_b200/_variants/$name
     mkdir -p $out
     make -s -C $ROOT/paper_2311_04499_b200/csrc OUT=$out/libcovap_b200.so OBJ=$out/obj KDEFS="${V[$name]}"
+  done
+  exit 0
+fi
+if [ "$1" = "k12" ]; then  # graph-timed K1 / K2 of the multi-rank step per variant
+  for name in ${NAMES:-base k2w1 k2w2 k2w4 k12w2 k2t16}; do
+    lib=$ROOT/paper_2311_04499_b200/_variants/$name/libcovap_b200.so
+    COVAP_LIB_PATH=$lib timeout 600 python $ROOT/scripts/k12_graph.py --label $name \
+      --layouts resnet50:4,resnet50:1,vgg16:4,bert_large:4 2>/dev/null
   done
   exit 0
 fi

@@ -27,17 +27,27 @@ def bits(a):
     return np.ascontiguousarray(a).view(np.uint32)
 
 
-@pytest.mark.parametrize("K", [1, 3])
-def test_ddp_hook_matches_oracle(pg, covap, orc, K):
+@pytest.mark.parametrize("K,schedule,view", [(1, "fused", True), (3, "fused", True),
+                                             (3, "side", True), (3, "side", False),
+                                             (1, "side", False), (3, "fused", False)])
+def test_ddp_hook_matches_oracle(pg, covap, orc, K, schedule, view):
+    """schedule 'fused': one rank's K1F on the producing stream; 'side': the
+    multi-rank schedule through a 1-rank NCCL communicator (K1 with the zero
+    fill on the producing stream, allreduce + selected-only unpack on the
+    side stream, finish() joins the streams).  view False: DDP copies the
+    bucket back into .grad after the hook's future — the copy must see the
+    side-stream unpack."""
     from torch.nn.parallel import DistributedDataParallel as DDP
     from paper_2311_04499_b200.ddp import CovapDDPHook
     torch.manual_seed(0)
     net = torch.nn.Sequential(
         torch.nn.Linear(256, 1024), torch.nn.ReLU(), torch.nn.Linear(1024, 4096), torch.nn.ReLU(),
         torch.nn.Linear(4096, 1024), torch.nn.ReLU(), torch.nn.Linear(1024, 64)).cuda()
-    model = DDP(net, bucket_cap_mb=4, gradient_as_bucket_view=True)
+    model = DDP(net, bucket_cap_mb=4, gradient_as_bucket_view=view)
     ef = covap.EfSchedule(True, 0.5, 1, 0.25)
-    hook = CovapDDPHook(covap.CovapConfig(interval=K, ef=ef), None, 0, warmup=2)
+    comm = covap.Communicator(covap.Communicator.unique_id(), 1, 0, 0) if schedule == "side" else None
+    hook = CovapDDPHook(covap.CovapConfig(interval=K, ef=ef), comm, 0, warmup=2,
+                        fuse_single_rank=schedule == "fused")
     raw = {}
 
     def spy(state, bucket):  # the bucket's local gradient before COVAP touches it
@@ -75,3 +85,5 @@ def test_ddp_hook_matches_oracle(pg, covap, orc, K):
                               for b in range(len(plan.buckets))])
         assert np.array_equal(bits(dev), bits(r)), s
         model.zero_grad(set_to_none=False)
+    if comm is not None:
+        comm.close()

@@ -862,3 +862,40 @@ def test_zero_filling_k1_and_selected_k2_equal_full_k2(covap, dtype, name, K):
         assert torch.equal(a.residuals, b.residuals) and torch.equal(a.residuals, c.residuals)
         se, _ = plan.send_elems(s)
         assert torch.equal(a.send[:se], b.send[:se])
+
+
+@pytest.mark.parametrize("sizes,cap,K", [
+    ([1001, 77, 65539, 3, 300007, 12345, 5, 777777], 1 << 20, 1),   # one run across odd buckets
+    ([1001, 77, 65539, 3, 300007, 12345, 5, 777777], 1 << 20, 3),
+    ([4099] * 7 + [1_000_003, 33, 250_001], 1 << 16, 2),             # sharded, tiny buckets
+    ([2_000_001, 5, 9, 1_500_007], 4 << 20, 4),
+])
+def test_selected_unpack_per_bucket_ragged(covap, sizes, cap, K):
+    """The send-space-tiled selected-only unpack clipped to one bucket at a
+    time (covap_bucket_ready's K2) on layouts whose buckets start at odd
+    offsets and whose runs span several buckets: every bucket-local K2 plus
+    the zero-filling K1 equals the full K1 -> K2, bit for bit, fp32 and fp64."""
+    for dtype in (torch.float32, torch.float64):
+        plan = covap.BucketPlan(mk_model(covap, sizes, cap), interval=K)
+        ef = covap.EfSchedule(True, 0.3, 1, 0.2)
+        a = covap.CompressorState(plan, dtype, 0, ef)
+        b = covap.CompressorState(plan, dtype, 0, ef)
+        d = plan.total_numel()
+        g = torch.empty(d, dtype=dtype, device=DEV)
+        oa = torch.empty(d, dtype=dtype, device=DEV)
+        ob = torch.empty(d, dtype=dtype, device=DEV)
+        nb = len(plan.buckets)
+        for s in range(K + 1):
+            covap.generate(g, covap.stream_key(72, 0, s))
+            ob.fill_(float("nan"))
+            a.filter_pack(g)
+            a.unpack(oa, 0.25, True)
+            for bk in range(nb):
+                b.filter_pack(g, bk, bk + 1, out=ob)
+            for bk in reversed(range(nb)):
+                b.unpack(ob, 0.25, True, bk, bk + 1, selected_only=True)
+            a.step_end()
+            b.step_end()
+            torch.cuda.synchronize()
+            assert torch.equal(oa, ob), (s, dtype)
+            assert torch.equal(a.residuals, b.residuals)
