@@ -1,7 +1,8 @@
 """Run only the sync kernels of one layout, for ncu (not product code).
 
     python scripts/profile_step.py --layout resnet50 --interval 1 --mode fused --iters 6
-modes: fused (K1F), unfused (K1 then K2).  L2 is flushed before every step.
+modes: fused (K1F), unfused (the multi-rank kernels: K1 with the output zero
+fill, then the selected-only K2).  L2 is flushed before every step.
 """
 import argparse
 import os
@@ -31,8 +32,8 @@ for s in range(a.iters):
     if a.mode == "fused":
         st.filter_unpack(g, out)
     else:
-        st.filter_pack(g)
-        st.unpack(out, 1.0, True)
+        st.filter_pack(g, out=out)
+        st.unpack(out, 1.0, True, selected_only=True)
     st.step_end()
 torch.cuda.synchronize()
 print("done", a)

@@ -54,7 +54,7 @@ def raw(rep):
 lines = [f"# {tag}: ncu --set full captures (B200, --clock-control none)\n",
          "Captured with `scripts/gpu_check.sh` (`scripts/profile_step.py`, L2 flushed before each "
          "step; ncu's own cache control also flushes).  Per launch: duration, DRAM bytes, and "
-         "the algorithmic bytes the bench uses (K1F 16N, K1 12N+4S, K2 4N+4S).  DRAM writes "
+         "the algorithmic bytes the bench uses (K1F 16N; multi-rank split: K1 16N with the output zero fill, K2 8S selected-only).  DRAM writes "
          "below the algorithmic figure are lines still dirty in the 126 MB L2 at kernel end.\n"]
 traffic = {}
 tpath = os.path.join(P, "dram_traffic.json")
