@@ -57,6 +57,9 @@ def main():
     ap.add_argument("--intervals", default="1,4")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=6)
+    ap.add_argument("--trace", default="",
+                    help="directory: for each COVAP mode also record one step's per-bucket "
+                         "timeline (CUDA events, paper_2311_04499_b200.trace) -> Chrome trace")
     ap.add_argument("--schedules", default="fused,side",
                     help="COVAP hook schedules at one rank: 'fused' (K1F on the producing stream) "
                          "and/or 'side' (the multi-rank schedule through a 1-rank NCCL "
@@ -114,8 +117,25 @@ def main():
             e1.record()
             torch.cuda.synchronize(dev)
             res[str(mode)] = e0.elapsed_time(e1) / args.steps
+            tl_info = None
+            if hook is not None and args.trace and hook.sync is not None:
+                from paper_2311_04499_b200 import trace
+                tl = trace.record_step(hook.sync, step)
+                k, sc = mode
+                os.makedirs(args.trace, exist_ok=True)
+                trace.chrome_trace(os.path.join(args.trace, f"trace_{name}_K{k}_{sc}.json"), tl)
+                last = len(tl) - 1
+                # what runs after the last bucket's gradient is ready: its K1 and
+                # whatever is still on the side stream (collectives, unpacks)
+                tail = max(r["k2_end"] for r in tl) - tl[last]["k1_start"]
+                tl_info = {"buckets": len(tl),
+                           "k1_ms": [round(r["k1_end"] - r["k1_start"], 4) for r in tl],
+                           "side_ms": [round(r["k2_end"] - r["comm_start"], 4)
+                                       if r["comm_start"] >= 0 else None for r in tl],
+                           "sync_after_last_gradient_ms": round(tail, 4),
+                           "sync_after_last_gradient_frac_of_step": round(tail / res[str(mode)], 5)}
             if hook is not None:
-                info[str(mode)] = {"hook_active": hook.sync is not None,
+                info[str(mode)] = {"timeline": tl_info, "hook_active": hook.sync is not None,
                                    "buckets": len(hook.plan.buckets) if hook.plan else None,
                                    "tensors": len(hook.plan.tensors) if hook.plan else None,
                                    "params": sum(b.numel for b in hook.plan.buckets) if hook.plan else None}

@@ -102,9 +102,10 @@ if os.path.exists(lc):
         agg[r[ki].split("(")[0]][0] += 1
         agg[r[ki].split("(")[0]][1] += float(r[mi].replace(",", ""))
     tot = sum(v[1] for v in agg.values())
-    prod = {k: v for k, v in agg.items() if "spin_kernel" not in k and "generate_kernel" not in k}
+    prod = {k: v for k, v in agg.items() if "spin_kernel" not in k and "busy_kernel" not in k
+            and "generate_kernel" not in k and "at::" not in k}
     ptot = sum(v[1] for v in prod.values())
-    out2 = ["", "Product kernels only (K3 spin = the emulated backward of the CCR profile step, "
+    out2 = ["", "Product kernels only (K3 spin / busy = the emulated backward of the CCR profile step, "
             "K0 generate = synthetic inputs):", "", "| kernel | launches | total µs | share |",
             "|---|---|---|---|"]
     for k, v in sorted(prod.items(), key=lambda x: -x[1][1]):
