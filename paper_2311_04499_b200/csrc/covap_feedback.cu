@@ -226,21 +226,11 @@ __global__ void __launch_bounds__(kThreads) dense_kernel(DenseArgs A) {
 
 // ---------------------------------------------------------- compensate
 
-// Top-k (HIST) also records, per 32-element segment of every body chunk, the
-// largest level-1 bin in it (segmax[chunk * kSegsPerChunk + segment]): the
-// collect pass then reads only the segments that can hold an element at or
-// above the tensor's threshold bin — a segment whose largest bin is below it
-// has no candidate and no taken element, so skipping it changes nothing.
-// A warp's 32 lanes cover exactly one segment per unrolled step (body chunks
-// start 32-element aligned relative to their chunk), so the segment maximum
-// is one warp max-reduction.
-constexpr uint32_t kSegsPerChunk = static_cast<uint32_t>(kChunk / 32);
-
 template <typename T, bool HIST>
 __global__ void __launch_bounds__(kThreads)
     compensate_kernel(const T* __restrict__ g, T* __restrict__ r, T* __restrict__ zero,
                       uint32_t* __restrict__ ghist, const Chunk* __restrict__ chunks,
-                      uint32_t nchunks, int ef, T coeff, uint16_t* __restrict__ segmax) {
+                      uint32_t nchunks, int ef, T coeff) {
   pdl_begin();
   __shared__ uint32_t hist[HIST ? kBins : 1];
   uint32_t cur = kNone;
@@ -279,23 +269,11 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int q = 0; q < kUnroll; ++q) {
         const uint64_t i = base + q * kThreads + threadIdx.x;
-        uint32_t b = 0;
-        if (i < ch.end) {
-          const T c = compensate(gv[q], rv[q], coeff, ef);
-          r[i] = c;
-          if (zero) zero[i] = T(0);
-          if (HIST) {
-            b = bin_of(c);
-            atomicAdd(&hist[b], 1u);
-          }
-        }
-        if (HIST && segmax && !ch.pad) {  // warp-uniform: base, q, chunk
-          const uint64_t s0 = base + q * kThreads + (threadIdx.x & ~31u);  // this warp's segment
-          const uint32_t m = __reduce_max_sync(0xffffffffu, b);
-          if ((threadIdx.x & 31) == 0 && s0 < ch.end)
-            segmax[static_cast<uint64_t>(ci) * kSegsPerChunk + (s0 - ch.begin) / 32] =
-                static_cast<uint16_t>(m);
-        }
+        if (i >= ch.end) continue;
+        const T c = compensate(gv[q], rv[q], coeff, ef);
+        r[i] = c;
+        if (zero) zero[i] = T(0);
+        if (HIST) atomicAdd(&hist[bin_of(c)], 1u);
       }
     }
   }
@@ -498,11 +476,14 @@ struct LaneRing {
   }
 };
 
-#ifndef COVAP_COLLECT_MINB  // register cap of collect: resident CTAs per SM (0: none)
-#define COVAP_COLLECT_MINB 0
+#ifndef COVAP_COLLECT_MASK  // collect: a vector's hits via a bit-mask loop (1) or unrolled (0)
+#define COVAP_COLLECT_MASK 0
+#endif
+#ifndef COVAP_COLLECT_DRAIN  // collect: warp iterations between ring drains
+#define COVAP_COLLECT_DRAIN 1
 #endif
 template <typename T>
-__global__ void __launch_bounds__(kThreads, COVAP_COLLECT_MINB) topk_collect_kernel(TopkArgs A) {
+__global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
   pdl_begin();
   using K = typename KeyOf<T>::K;
   constexpr int kU = kCollectUnroll<T>;
@@ -567,34 +548,7 @@ __global__ void __launch_bounds__(kThreads, COVAP_COLLECT_MINB) topk_collect_ker
     // kU / W vectors: element q of the lane is vector (q / W), lane (q % W).
     constexpr int W = 16 / static_cast<int>(sizeof(T));
     const uint32_t cbeg = static_cast<uint32_t>(ch.begin), cend = static_cast<uint32_t>(ch.end);
-    if (ch.pad == 0 && A.segmax) {
-      // Only the 32-element segments whose largest bin reaches b1 (see
-      // compensate_kernel): each lane owns one segment of the warp's group of
-      // 32 and, when it qualifies, reads its 32 elements as 16-byte vectors.
-      using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
-      constexpr int kSegVec = 32 / W;
-      const uint32_t nseg = (cend - cbeg + 31) / 32;
-      const uint16_t* sm = A.segmax + static_cast<uint64_t>(ci) * kSegsPerChunk;
-      for (uint32_t g0 = warp * 32; g0 < nseg; g0 += kWarps * 32) {
-        const uint32_t sg = g0 + lane;
-        if (sg < nseg && sm[sg] >= b1) {
-          const uint32_t e0 = cbeg + sg * 32;
-          V x[kSegVec];
-#pragma unroll
-          for (int j = 0; j < kSegVec; ++j)
-            x[j] = e0 + j * W < cend ? *reinterpret_cast<const V*>(r + e0 + j * W) : V{};
-#pragma unroll
-          for (int j = 0; j < kSegVec; ++j) {
-            const T* xs = reinterpret_cast<const T*>(&x[j]);
-#pragma unroll
-            for (int w = 0; w < W; ++w)
-              if (KeyOf<T>::key(xs[w]) >= k_cand && e0 + j * W < cend) hit(e0 + j * W + w, xs[w]);
-          }
-        }
-        take.drain(sel_cnt, A.list_idx, list_val, lo, false);
-        cand.drain(cand_cnt, A.cand_idx, cand_key, cb, false);
-      }
-    } else if (ch.pad == 0) {
+    if (ch.pad == 0) {
       using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
       for (uint32_t base = cbeg + warp * kSpan; base < cend; base += kWarps * kSpan) {
         V x[kU / W];
@@ -607,12 +561,39 @@ __global__ void __launch_bounds__(kThreads, COVAP_COLLECT_MINB) topk_collect_ker
         for (int j = 0; j < kU / W; ++j) {
           const uint32_t e0 = base + (j * 32 + lane) * W;
           const T* xs = reinterpret_cast<const T*>(&x[j]);
+          // one test per 16-byte vector on its largest key: hits are ~1 % of
+          // elements, so almost every vector is rejected with one compare
+          K m = KeyOf<T>::key(xs[0]);
 #pragma unroll
-          for (int w = 0; w < W; ++w)
-            if (KeyOf<T>::key(xs[w]) >= k_cand && e0 < cend) hit(e0 + w, xs[w]);
+          for (int w = 1; w < W; ++w) m = max(m, KeyOf<T>::key(xs[w]));
+          if (m >= k_cand && e0 < cend) {
+#if COVAP_COLLECT_MASK
+            // the vector's hits as a bit mask, handled in one loop: the hit
+            // path is inlined once and runs as often as the busiest lane needs
+            uint32_t hm = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) hm |= (KeyOf<T>::key(xs[w]) >= k_cand ? 1u : 0u) << w;
+            while (hm) {
+              const int w = __ffs(hm) - 1;
+              hm &= hm - 1;
+              T v = xs[0];
+#pragma unroll
+              for (int q = 1; q < W; ++q) v = w == q ? xs[q] : v;
+              hit(e0 + w, v);
+            }
+#else
+#pragma unroll
+            for (int w = 0; w < W; ++w)
+              if (KeyOf<T>::key(xs[w]) >= k_cand) hit(e0 + w, xs[w]);
+#endif
+          }
         }
-        take.drain(sel_cnt, A.list_idx, list_val, lo, false);
-        cand.drain(cand_cnt, A.cand_idx, cand_key, cb, false);
+        // drain the rings every COVAP_COLLECT_DRAIN iterations (overfull
+        // claims go straight to the global list, so any period is safe)
+        if (((base - cbeg) / (kWarps * kSpan)) % COVAP_COLLECT_DRAIN == COVAP_COLLECT_DRAIN - 1) {
+          take.drain(sel_cnt, A.list_idx, list_val, lo, false);
+          cand.drain(cand_cnt, A.cand_idx, cand_key, cb, false);
+        }
       }
     } else {  // scalar chunk: one element per lane
       for (uint32_t base = cbeg + warp * 32; base < cend; base += kWarps * 32) {
@@ -1168,28 +1149,28 @@ cudaError_t launch_dense(int dtype, int kind, const DenseArgs& a, int sms, cudaS
 
 cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uint32_t* hist,
                               const Chunk* chunks, uint32_t nchunks, int ef, double coeff,
-                              int sms, cudaStream_t s, bool pdl, uint16_t* segmax) {
+                              int sms, cudaStream_t s, bool pdl) {
   const int grid = static_cast<int>(nchunks < static_cast<uint32_t>(sms * 4) ? nchunks : sms * 4);
   if (grid == 0) return cudaSuccess;
   if (dtype == 1) {
     if (hist)
       return launch_pdl(pdl, compensate_kernel<double, true>, dim3(grid), dim3(kThreads), 0, s,
                         static_cast<const double*>(g), static_cast<double*>(r),
-                        static_cast<double*>(zero), hist, chunks, nchunks, ef, coeff, segmax);
+                        static_cast<double*>(zero), hist, chunks, nchunks, ef, coeff);
     else
       compensate_kernel<double, false><<<grid, kThreads, 0, s>>>(
           static_cast<const double*>(g), static_cast<double*>(r), static_cast<double*>(zero),
-          hist, chunks, nchunks, ef, coeff, nullptr);
+          hist, chunks, nchunks, ef, coeff);
   } else {
     const float c = static_cast<float>(coeff);
     if (hist)
       return launch_pdl(pdl, compensate_kernel<float, true>, dim3(grid), dim3(kThreads), 0, s,
                         static_cast<const float*>(g), static_cast<float*>(r),
-                        static_cast<float*>(zero), hist, chunks, nchunks, ef, c, segmax);
+                        static_cast<float*>(zero), hist, chunks, nchunks, ef, c);
     else
       compensate_kernel<float, false><<<grid, kThreads, 0, s>>>(
           static_cast<const float*>(g), static_cast<float*>(r), static_cast<float*>(zero), hist,
-          chunks, nchunks, ef, c, nullptr);
+          chunks, nchunks, ef, c);
   }
   return cudaGetLastError();
 }

@@ -56,7 +56,7 @@ cudaError_t launch_dense(int dtype, int kind, const DenseArgs& a, int sms, cudaS
 // NULL; with hist, the per-tensor histogram of the top kBinBits of |c|.
 cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uint32_t* hist,
                               const Chunk* chunks, uint32_t nchunks, int ef, double coeff,
-                              int sms, cudaStream_t s, bool pdl = false, uint16_t* segmax = nullptr);
+                              int sms, cudaStream_t s, bool pdl = false);
 
 // Top-k after the compensation pass filled hist1: the k[t] largest |c| of
 // every tensor (ties to the lower index) go to list_idx / list_val at
@@ -92,10 +92,6 @@ struct TopkArgs {
   uint32_t* cand2_idx;
   uint32_t* list_idx;
   void* list_val;
-  // per 32-element segment of each body chunk: its largest level-1 bin
-  // (written by compensate, read by collect to skip segments below the
-  // threshold bin); NULL: collect reads every element
-  const uint16_t* segmax;
   int pdl;  // programmatic dependent launch along the chain (small layouts)
 };
 // Layouts below this many elements run the top-k chain with programmatic

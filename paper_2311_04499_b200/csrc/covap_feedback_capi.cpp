@@ -48,7 +48,6 @@ struct covap_feedback {
   unsigned long long* d_sat = nullptr;
   // top-k
   uint32_t* hist = nullptr;
-  uint16_t* segmax = nullptr;  // top-k: per-segment largest bin (compensate -> collect)
   uint32_t* d_k = nullptr;
   uint32_t* thr = nullptr;
   uint32_t* need = nullptr;
@@ -186,7 +185,7 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
     case COVAP_FILTER_TOPK: {
       const bool pdl = f->total < fb::kTopkPdlMaxElems;
       CK(fb::launch_compensate(dt, grad, f->residual, zero, f->hist, f->chunks, f->nchunks,
-                               f->ef.enabled, coeff, f->sms, st, pdl, f->segmax));
+                               f->ef.enabled, coeff, f->sms, st, pdl));
       fb::TopkArgs a{};
       a.pdl = pdl ? 1 : 0;
       a.r = f->residual;
@@ -213,7 +212,6 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       a.cand2_idx = f->cand2_idx;
       a.list_idx = f->list_idx;
       a.list_val = f->list_val;
-      a.segmax = f->segmax;
       CK(fb::launch_topk(dt, a, f->sms, st));
       break;
     }
@@ -395,7 +393,6 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
     }
     if (filter->kind == COVAP_FILTER_TOPK) {
       f->hist = dalloc<uint32_t>(f, n_tensors * fb::kBins * 4);
-      f->segmax = dalloc<uint16_t>(f, std::max<uint64_t>(f->nchunks, 1) * (fb::kChunk / 32) * 2);
       CK(cudaMemset(f->hist, 0, n_tensors * fb::kBins * 4));
       std::vector<uint32_t> k32(f->k.begin(), f->k.end());
       f->d_k = dalloc<uint32_t>(f, n_tensors * 4);
