@@ -413,10 +413,13 @@ struct WarpStage {
 };
 
 constexpr int kWarps = kThreads / 32;
-// collect: elements per lane per warp iteration (1 KB of c per warp; 2 KB
-// measured slower on VGG-16: 259 -> 387 us, register-limited occupancy)
+// collect: elements per lane per warp iteration.  Round 1: 1 KB of c per
+// warp (2 KB measured slower, register-limited occupancy); round 2, with the
+// per-vector max test and the bit-mask hit loop: 2 KB per warp is faster
+// (ResNet-50 / VGG-16 / BERT-large top-k step 0.1364 / 0.6535 / 1.4496 ms ->
+// 0.1340 / 0.6396 / 1.4145 ms, profiles/r2_f4.md)
 #ifndef COVAP_COLLECT_BYTES  // bytes of c per lane per warp iteration
-#define COVAP_COLLECT_BYTES 32
+#define COVAP_COLLECT_BYTES 64
 #endif
 #ifndef COVAP_COLLECT_CTAS  // collect CTAs per SM
 #define COVAP_COLLECT_CTAS 4
@@ -477,7 +480,7 @@ struct LaneRing {
 };
 
 #ifndef COVAP_COLLECT_MASK  // collect: a vector's hits via a bit-mask loop (1) or unrolled (0)
-#define COVAP_COLLECT_MASK 0
+#define COVAP_COLLECT_MASK 1
 #endif
 #ifndef COVAP_COLLECT_DRAIN  // collect: warp iterations between ring drains
 #define COVAP_COLLECT_DRAIN 1
