@@ -167,6 +167,14 @@ covap_status covap_state_set_pipeline(covap_state* state, int groups);
 /* covap_sync_step_host's chunk schedule: chunks ramp geometrically from
  * ramp_min_elems (>= 8192) up to the body chunk at both ends (default 1 Mi). */
 covap_status covap_state_set_host_ramp(covap_state* state, uint64_t ramp_min_elems);
+/* Move the state's send buffer to NCCL-allocated memory registered as a
+ * SYMMETRIC window on comm (ncclMemAlloc + ncclCommWindowRegister with
+ * NCCL_WIN_COLL_SYMMETRIC, NCCL >= 2.27): the allreduce of the packed
+ * selected shards can then take NCCL's symmetric-memory / NVLS kernels over
+ * NVSwitch.  Collective: every rank calls it with its own state.  Blocks the
+ * device.  The window is deregistered when the state or the communicator is
+ * destroyed, whichever comes first.  Results are unchanged. */
+covap_status covap_state_use_symmetric(covap_state* state, covap_comm* comm);
 /* Zero the residual arena (stream-ordered). */
 covap_status covap_state_reset(covap_state* state, void* stream);
 

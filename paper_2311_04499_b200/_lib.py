@@ -118,6 +118,7 @@ _SIGS = {
     "covap_comm_destroy": ("void", [vp]),
     "covap_comm_size": (None, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
     "covap_allreduce": (None, [vp, vp, u64, i32, vp]),
+    "covap_state_use_symmetric": (None, [vp, vp]),
     "covap_comm_allreduce_mean": (None, [vp, i32, vp, vp, u64, vp]),
     "covap_comm_profile_exchange": (None, [vp, f64p, sz, f64, f64p, f64p]),
     "covap_settings_default": (None, [ctypes.POINTER(SettingsC)]),

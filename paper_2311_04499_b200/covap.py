@@ -413,6 +413,16 @@ class CompressorState:
         overlap the later groups' K1 (1 = serial)."""
         L.lib().covap_state_set_pipeline(self._h, int(groups))
 
+    def use_symmetric(self, comm: "Communicator"):
+        """Send buffer -> an NCCL symmetric window on ``comm`` (collective;
+        NVLS / symmetric-memory allreduce kernels at P > 1)."""
+        L.lib().covap_state_use_symmetric(self._h, comm.handle)
+        torch = _torch()
+        p, n = ctypes.c_void_p(), ctypes.c_uint64()
+        L.lib().covap_state_send(self._h, ctypes.byref(p), ctypes.byref(n))
+        self.send = torch.as_tensor(_CudaArray(p.value, n.value, self.dtype_code),
+                                    device=torch.device("cuda", self.device))
+
     def set_host_ramp(self, ramp_min_elems: int):
         """Smallest chunk of sync_host's geometric ramp at both ends of the step."""
         L.lib().covap_state_set_host_ramp(self._h, int(ramp_min_elems))
@@ -616,7 +626,7 @@ class CovapSync:
 
     def __init__(self, plan: BucketPlan, comm: Optional[Communicator] = None, dtype=None,
                  device: int = 0, ef: Optional[EfSchedule] = None,
-                 fuse_single_rank: bool = True, pipeline: int = 1):
+                 fuse_single_rank: bool = True, pipeline: int = 1, symmetric: bool = False):
         self.plan = plan
         self.comm = comm
         self.state = CompressorState(plan, dtype, device, ef)
@@ -625,6 +635,8 @@ class CovapSync:
             self.state.set_fused(False)
         if pipeline != 1:
             self.state.set_pipeline(pipeline)
+        if symmetric and comm is not None:
+            self.state.use_symmetric(comm)
 
     @property
     def world(self) -> int:

@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <exception>
 #include <new>
 #include <string>
@@ -58,11 +60,38 @@ struct covap_state {
   bool fuse_single_rank = true;                 // P = 1: run K1F instead of K1 -> C1 -> K2
   uint64_t ramp_min = 1u << 20;                 // host pipeline: smallest ramp chunk (elements)
   int pipeline = 1;                             // P > 1 sync step: bucket groups (1 = serial)
+  // send buffer from ncclMemAlloc, registered as a symmetric NCCL window on
+  // win_comm (covap_state_use_symmetric); NULL: plain cudaMalloc
+  ncclWindow_t win = nullptr;
+  covap_comm* win_comm = nullptr;
+  bool send_nccl_mem = false;
 };
 
 namespace covapb {
 thread_local std::string g_last_error;
 }  // namespace covapb
+
+namespace {
+// Communicators alive right now: a state holding a window on a communicator
+// that is already gone must not deregister it (the communicator did).
+std::mutex g_comms_mu;
+std::set<covap_comm*> g_live_comms;
+
+void drop_window(covap_state* s) {
+  if (!s->win) return;
+  std::lock_guard<std::mutex> lock(g_comms_mu);
+  if (s->win_comm && g_live_comms.count(s->win_comm)) {
+    auto& w = s->win_comm->windows;
+    const auto it = std::find(w.begin(), w.end(), s->win);
+    if (it != w.end()) {
+      ncclCommWindowDeregister(s->win_comm->nccl, s->win);
+      w.erase(it);
+    }
+  }
+  s->win = nullptr;
+  s->win_comm = nullptr;
+}
+}  // namespace
 
 namespace {
 
@@ -336,8 +365,13 @@ void covap_state_destroy(covap_state* s) {
   cudaGetDevice(&prev);
   cudaSetDevice(s->device);
   if (s->comm_stream) cudaStreamSynchronize(s->comm_stream);
+  cudaDeviceSynchronize();
+  drop_window(s);
   cudaFree(s->residual);
-  cudaFree(s->send);
+  if (s->send_nccl_mem)
+    ncclMemFree(s->send);
+  else
+    cudaFree(s->send);
   cudaFree(s->d_runs);
   for (auto e : s->ready) cudaEventDestroy(e);
   for (auto e : s->k1s) cudaEventDestroy(e);
@@ -463,6 +497,41 @@ covap_status covap_state_set_pipeline(covap_state* s, int groups) {
     need(s != nullptr, "NULL state");
     need(groups >= 1, "groups must be >= 1");
     s->pipeline = groups;
+  });
+}
+
+covap_status covap_state_use_symmetric(covap_state* s, covap_comm* c) {
+  return guarded([&] {
+    need(s && c, "NULL argument");
+    need(c->device == s->device, "communicator and state are on different devices");
+    need(!s->win, "the send buffer is already a symmetric window");
+    DeviceGuard dg(s->device);
+    CK(cudaDeviceSynchronize());  // nothing may still use the old buffer
+    const size_t bytes = (s->send_cap * s->esize + NCCL_WIN_REQUIRED_ALIGNMENT - 1) /
+                         NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    void* buf = nullptr;
+    NK(ncclMemAlloc(&buf, bytes));
+    const cudaError_t me = cudaMemset(buf, 0, bytes);  // alignment gaps stay zero forever
+    if (me != cudaSuccess) {
+      ncclMemFree(buf);
+      throw CudaError{me, "cudaMemset(symmetric send buffer)"};
+    }
+    ncclWindow_t win = nullptr;
+    const ncclResult_t r = ncclCommWindowRegister(c->nccl, buf, bytes, &win, NCCL_WIN_COLL_SYMMETRIC);
+    if (r != ncclSuccess) {
+      ncclMemFree(buf);
+      throw NcclError{r, "ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC)"};
+    }
+    if (s->send_nccl_mem)
+      ncclMemFree(s->send);
+    else
+      cudaFree(s->send);
+    s->send = buf;
+    s->send_nccl_mem = true;
+    s->win = win;
+    s->win_comm = c;
+    std::lock_guard<std::mutex> lock(g_comms_mu);
+    c->windows.push_back(win);
   });
 }
 
@@ -983,12 +1052,27 @@ covap_status covap_comm_create(const uint8_t id[128], int nranks, int rank, int 
       delete c;
       throw NcclError{r, "ncclCommInitRank"};
     }
+    {
+      std::lock_guard<std::mutex> lock(g_comms_mu);
+      g_live_comms.insert(c);
+    }
     *out = c;
   });
 }
 
 void covap_comm_destroy(covap_comm* c) {
   if (!c) return;
+  {
+    std::lock_guard<std::mutex> lock(g_comms_mu);
+    g_live_comms.erase(c);
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (ncclWindow_t w : c->windows) ncclCommWindowDeregister(c->nccl, w);
+    c->windows.clear();
+    if (prev >= 0) cudaSetDevice(prev);
+  }
   if (c->nccl) ncclCommDestroy(c->nccl);
   delete c;
 }

@@ -10,6 +10,7 @@
 #include <exception>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "covap/errors.hpp"
 #include "covap_c.h"
@@ -19,6 +20,9 @@ struct covap_comm {
   int nranks = 1;
   int rank = 0;
   int device = 0;
+  // NCCL windows registered on this communicator (symmetric send buffers,
+  // covap_state_use_symmetric): deregistered at the latest when it is destroyed
+  std::vector<ncclWindow_t> windows;
 };
 
 namespace covapb {

@@ -899,3 +899,33 @@ def test_selected_unpack_per_bucket_ragged(covap, sizes, cap, K):
             torch.cuda.synchronize()
             assert torch.equal(oa, ob), (s, dtype)
             assert torch.equal(a.residuals, b.residuals)
+
+
+@pytest.mark.parametrize("name,K", [("resnet50", 4), ("vgg16", 4)])
+def test_symmetric_send_window_same_results(covap, name, K):
+    """The send buffer moved to an NCCL symmetric window (ncclMemAlloc +
+    ncclCommWindowRegister, the NVLS / symmetric-kernel path at P > 1) gives
+    the same synchronised gradients and residuals as the plain buffer, through
+    the multi-rank step on a 1-rank communicator; destroying the communicator
+    before the state is safe."""
+    comm = covap.Communicator(covap.Communicator.unique_id(), 1, 0, 0)
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    a = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
+    try:
+        b = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False, symmetric=True)
+    except covap.NcclError as e:  # reported, not hidden: NCCL builds without window support
+        comm.close()
+        pytest.skip(f"NCCL refused a symmetric window on this box: {e}")
+    d = plan.total_numel()
+    g = torch.empty(d, device=DEV)
+    oa, ob = torch.empty(d, device=DEV), torch.empty(d, device=DEV)
+    for s in range(K + 1):
+        covap.generate(g, covap.stream_key(81, 0, s))
+        a.sync(g, oa)
+        b.sync(g, ob)
+        torch.cuda.synchronize()
+        assert torch.equal(oa, ob), s
+        assert torch.equal(a.state.residuals, b.state.residuals), s
+    comm.close()  # deregisters the window
+    del b
+    torch.cuda.synchronize()
