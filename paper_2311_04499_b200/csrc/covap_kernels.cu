@@ -67,9 +67,6 @@ namespace {
 #ifndef COVAP_K2_MIN_WAVES
 #define COVAP_K2_MIN_WAVES 0
 #endif
-#ifndef COVAP_K2_SMALL_BYTES  // selected-only unpack: below this many send bytes, the LDG/STG grid
-#define COVAP_K2_SMALL_BYTES 0
-#endif
 #ifndef COVAP_FILTER_THREADS  // threads per CTA of the K1 / K1F / K1F+SGD passes
 #define COVAP_FILTER_THREADS 256
 #endif
@@ -940,67 +937,6 @@ __global__ void __launch_bounds__(kThreads, 1) unpack_sel_kernel(const SelArgs<T
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
-// Small send ranges (a bucket's selected shard of a few MB in the overlapped
-// schedule): the TMA ring's fixed costs — mbarrier setup, the first bulk
-// load's round trip, the bulk-store drain — are most of such a kernel, so
-// below COVAP_K2_SMALL_BYTES the same gather runs as a plain grid of 16-byte
-// loads / stores, kSelB vectors in flight per thread.  A vector that lies
-// inside one run and the [a, b) clip is one 16-byte store; the rest (run
-// ends, clip edges, alignment gaps) go element by element.
-constexpr int kSelB = 4;
-template <typename T>
-__global__ void __launch_bounds__(kThreads) unpack_sel_small_kernel(const SelArgs<T> A) {
-  constexpr uint64_t W = 16 / sizeof(T);
-  using V = typename Vec16<T>::type;
-  pdl_launch_dependents();
-  pdl_wait();
-  const uint64_t nv = (A.o_hi - A.o_lo + W - 1) / W;  // vectors of the send range
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
-  for (uint64_t v0 = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; v0 < nv;
-       v0 += kSelB * stride) {
-    V x[kSelB];
-#pragma unroll
-    for (int q = 0; q < kSelB; ++q) {
-      const uint64_t v = v0 + q * stride, o = A.o_lo + v * W;
-      if (v < nv) {
-        if (o + W <= A.o_hi) {
-          x[q] = reinterpret_cast<const V*>(A.recv)[o / W];
-        } else {
-#pragma unroll
-          for (int w = 0; w < static_cast<int>(W); ++w)
-            lane(x[q], w) = o + w < A.o_hi ? A.recv[o + w] : T(0);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kSelB; ++q) {
-      const uint64_t v = v0 + q * stride, o = A.o_lo + v * W;
-      if (v >= nv) continue;
-      int j = run_by_dst(A.runs, A.nruns, o);
-      if (j >= A.nruns) continue;
-      Run R = A.runs[j];
-      const uint64_t d1 = R.dst + (R.end - R.begin);
-      const uint64_t e = R.begin + (o - R.dst);
-      if (o >= R.dst && o + W <= d1 && e >= A.a && e + W <= A.b && (R.dst - R.begin) % W == 0) {
-        V y = x[q];
-#pragma unroll
-        for (int w = 0; w < static_cast<int>(W); ++w) lane(y, w) = scale_of(lane(y, w), A.inv, A.mean);
-        *reinterpret_cast<V*>(A.out + e) = y;
-        continue;
-      }
-#pragma unroll
-      for (int w = 0; w < static_cast<int>(W); ++w) {  // edges: element by element
-        const uint64_t ow = o + w;
-        if (ow >= A.o_hi) break;
-        while (j < A.nruns && A.runs[j].dst + (A.runs[j].end - A.runs[j].begin) <= ow) ++j;
-        if (j >= A.nruns || A.runs[j].dst > ow) continue;  // an alignment gap
-        const uint64_t ew = A.runs[j].begin + (ow - A.runs[j].dst);
-        if (ew >= A.a && ew < A.b) A.out[ew] = scale_of(lane(x[q], w), A.inv, A.mean);
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------- mean of rows
 // allreduce_mean for P in-process workers (trainer.cpp:41-45): out[i] =
 // ((0 + x_0[i]) + x_1[i] + ... + x_{P-1}[i]) * inv, in worker order.
@@ -1266,26 +1202,9 @@ cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* run
       A.b = b;
       A.inv = static_cast<T>(inv);
       A.mean = mean;
-      cudaLaunchConfig_t cfg = {};
-      if ((A.o_hi - A.o_lo) * sizeof(T) < static_cast<uint64_t>(COVAP_K2_SMALL_BYTES)) {
-        const uint64_t nvec = (A.o_hi - A.o_lo + W - 1) / W;
-        const uint64_t want = (nvec + kThreads * kSelB - 1) / (kThreads * kSelB);
-        cfg.gridDim = dim3(static_cast<unsigned>(std::max<uint64_t>(
-            1, std::min<uint64_t>(want, static_cast<uint64_t>(sh->sms) * 8))));
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = 0;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = COVAP_PDL ? 1 : 0;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        A.te = 0;
-        const cudaError_t err = cudaLaunchKernelEx(&cfg, unpack_sel_small_kernel<T>, A);
-        return err != cudaSuccess ? err : cudaGetLastError();
-      }
       const unsigned grid = balance<T>(A.o_lo, (A.o_hi + W - 1) / W * W, sh->sms, kTileK2, &A.te,
                                        static_cast<uint64_t>(sh->sms) * COVAP_K2_MIN_WAVES);
+      cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = dim3(kThreads);
       cfg.dynamicSmemBytes = kSmemK2Sel;
