@@ -17,6 +17,7 @@ declare -A V=(
   [k2w4]="-DCOVAP_K2_MIN_WAVES=4"
   [k12w2]="-DCOVAP_K1_MIN_WAVES=2 -DCOVAP_K2_MIN_WAVES=2"
   [k2t16]="-DCOVAP_K2_TILE=16384 -DCOVAP_K2_STAGES=6"
+  [evf]="-DCOVAP_EVICT_FIRST=1"
 )
 if [ "$1" = "build" ]; then
   for name in "${!V[@]}"; do
@@ -34,14 +35,15 @@ if [ "$1" = "k12" ]; then  # graph-timed K1 / K2 of the multi-rank step per vari
   done
   exit 0
 fi
-for name in ${NAMES:-base nopdl k1t16}; do
+for name in ${NAMES:-base evf}; do
   lib=$ROOT/paper_2311_04499_b200/_variants/$name/libcovap_b200.so
-  for cfg in "--layout resnet50 --interval 1" "--layout resnet50 --interval 4" "--layout vgg16 --interval 4" "--layout bert_large --interval 1" "--layout bert_large --interval 4"; do
+  for cfg in "--layout resnet50 --interval 4" "--layout resnet50 --interval 1" "--layout vgg16 --interval 4" "--layout bert_large --interval 4"; do
     COVAP_LIB_PATH=$lib timeout 300 python $ROOT/bench.py $cfg --no-cpu-baseline --no-overhead --steps 30 --warmup 5 2>/dev/null | \
       python -c "
 import sys, json
-d = json.loads(sys.stdin.read()); r = d['roofline']; u = r.get('unfused_p1', {})
-print('$name', d['config']['layout'], 'K%d' % d['config']['interval'], 'value %.0f' % d['value'],
-      'k1f %.3f' % r['frac'], 'k1 %.3f' % u.get('k1_frac', 0), 'k2 %.3f' % u.get('k2_frac', 0))"
+d = json.loads(sys.stdin.read()); r = d['roofline']; u = r.get('unfused_p1', {}).get('graph', {})
+print('$name', d['config']['layout'], 'K%d' % d['details']['interval'], 'value %.0f' % d['value'],
+      'k1f %.3f' % r['frac'], 'k1 %.3f' % u.get('k1_frac', 0), 'k2 %.3f' % u.get('k2_frac', 0),
+      'e2e %.1f' % d['e2e']['value'])"
   done
 done
