@@ -152,8 +152,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-#ifndef COVAP_EVICT_FIRST  // L2 evict-first hint on the streaming bulk copies (A/B knob)
-#define COVAP_EVICT_FIRST 0
+// L2 evict-first policy on every bulk copy of the streaming passes: nothing a
+// sync step reads or writes is reused within the step (16N bytes against a
+// 126 MB L2), and marking it evict-first keeps the previous step's dirty
+// lines from crowding the L2 in back-to-back steps: ResNet-50 K=4 sync step
+// 1533-1547 -> 1557-1565 GB/s, K1F 0.938-0.947 -> 0.953-0.958 of the copy
+// peak; VGG-16 / BERT-large unchanged (profiles/r2_design.md).
+#ifndef COVAP_EVICT_FIRST
+#define COVAP_EVICT_FIRST 1
 #endif
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
