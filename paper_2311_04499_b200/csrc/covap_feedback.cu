@@ -20,6 +20,8 @@
 // the same sequence in single precision (the tests' fp32 restatement).
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "covap_feedback.h"
@@ -859,9 +861,11 @@ __global__ void randomk_draw_kernel(RandomkArgs A) {
     const uint64_t n = A.t_numel[t] - i;
     const uint64_t seed = seed_of(A, t);
     const uint64_t x = splitmix_out(seed + (i + 1) * 0x9e3779b97f4a7c15ULL);
-    const uint64_t threshold = (0ULL - n) % n;  // rng.hpp:29
-    if (x < threshold) A.reject[t] = 1;
+    // next_below's rejection bound (0 - n) % n (rng.hpp:29) is below n, so
+    // only x < n can be rejected (probability n / 2^64)
+    if (x < n && x < (0ULL - n) % n) A.reject[t] = 1;
     A.j[e] = static_cast<uint32_t>(i + x % n);
+    A.key[e] = static_cast<uint32_t>(A.t_begin[t] + i + x % n);
   }
 }
 
@@ -882,20 +886,51 @@ __global__ void randomk_replay_kernel(RandomkArgs A) {
       x = splitmix_out(state);
     } while (x < threshold);
     A.j[lo + i] = static_cast<uint32_t>(i + x % n);
+    A.key[lo + i] = static_cast<uint32_t>(A.t_begin[t] + i + x % n);
   }
 }
 
-// Per-position lists of the draws that target each position.
+// Two ways to find, for every draw, the earlier draws with the same target
+// (prv) and the last earlier draw that targeted its own position (src):
+//   hash  (up to 2^20 draws): per-position linked lists whose heads live in
+//         an open-addressed table of 2^tbits words (flat position + 1 : 32,
+//         last draw + 1 : 32; 0 = empty), emptied again by the resolve pass.
+//         ~2k words (4 MB at ResNet-50 size) stay in L2.
+//   sort  (more draws, where the table would not stay in L2: BERT-large link
+//         + chain 550 us): a radix sort of the draws by target, then one
+//         coalesced pass over the runs of equal targets.
+// Neither touches an N-sized array, so the selection that runs beside the
+// compensation pass takes little of its DRAM bandwidth.
+__device__ __forceinline__ uint32_t slot_of(uint32_t key, uint32_t tbits) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(key) * 0x9e3779b97f4a7c15ull) >> (64 - tbits));
+}
+
 __global__ void randomk_link_kernel(RandomkArgs A) {
+  const uint32_t mask = (1u << A.tbits) - 1u;
   for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
        e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t t = tensor_of_entry(A, e);
     const uint32_t i = static_cast<uint32_t>(e - A.list_off[t]);
-    // epoch-tagged list heads: an entry of another epoch reads as empty, so
-    // the heads never need clearing (one random write per draw less)
-    const unsigned long long old = atomicExch(&A.head[A.t_begin[t] + A.j[e]],
-                                              (static_cast<unsigned long long>(A.tag) << 32) | i);
-    A.nxt[e] = (old >> 32) == A.tag ? static_cast<uint32_t>(old) : kNone;
+    const uint32_t key = static_cast<uint32_t>(A.t_begin[t] + A.j[e]) + 1u;
+    const unsigned long long mine = (static_cast<unsigned long long>(key) << 32) | (i + 1u);
+    uint32_t h = slot_of(key, A.tbits);
+    uint32_t prev = kNone;
+    for (;;) {
+      const unsigned long long w = A.table[h];
+      const uint32_t k = static_cast<uint32_t>(w >> 32);
+      if (k != key && k != 0u) {
+        h = (h + 1u) & mask;
+        continue;
+      }
+      const unsigned long long got = atomicCAS(&A.table[h], w, mine);
+      if (got == w) {
+        prev = k == 0u ? kNone : static_cast<uint32_t>(w) - 1u;
+        break;
+      }
+      // lost a race on this slot: look at it again
+    }
+    A.slot[e] = h;
+    A.nxt[e] = prev;
   }
 }
 
@@ -903,17 +938,24 @@ __global__ void randomk_link_kernel(RandomkArgs A) {
 __device__ __forceinline__ uint32_t last_before(const RandomkArgs& A, uint32_t t, uint32_t p,
                                                 uint32_t before) {
   const uint64_t lo = A.list_off[t];
+  const uint32_t key = static_cast<uint32_t>(A.t_begin[t] + p) + 1u;
+  const uint32_t mask = (1u << A.tbits) - 1u;
+  uint32_t h = slot_of(key, A.tbits);
+  unsigned long long w;
+  for (;;) {
+    w = A.table[h];
+    const uint32_t k = static_cast<uint32_t>(w >> 32);
+    if (k == 0u) return kNone;
+    if (k == key) break;
+    h = (h + 1u) & mask;
+  }
   uint32_t best = kNone;
-  const unsigned long long h = A.head[A.t_begin[t] + p];
-  for (uint32_t m = (h >> 32) == A.tag ? static_cast<uint32_t>(h) : kNone; m != kNone;
-       m = A.nxt[lo + m])
+  for (uint32_t m = static_cast<uint32_t>(w) - 1u; m != kNone; m = A.nxt[lo + m])
     if (m < before && (best == kNone || m > best)) best = m;
   return best;
 }
 
-// prv[i] = last earlier draw with the same target; src[i] = last earlier
-// draw targeting position i itself.
-__global__ void randomk_chain_kernel(RandomkArgs A) {
+__global__ void randomk_chain_hash_kernel(RandomkArgs A) {
   for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
        e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t t = tensor_of_entry(A, e);
@@ -923,14 +965,37 @@ __global__ void randomk_chain_kernel(RandomkArgs A) {
   }
 }
 
+// The draws sorted by flat target (stable, so draws in order within a
+// target): the swap chains become neighbours.  prv[e] = the last earlier
+// draw with the same target (the previous entry of its run); src[lo + p] =
+// the last draw m < p whose target is position p itself (the last entry of
+// p's run below p; only positions p < k are themselves draws).  src was
+// filled with kNone before.  One coalesced pass instead of per-position
+// linked lists: the k draws never touch an N-sized table, so the selection
+// running beside the compensation pass costs it little DRAM bandwidth.
+__global__ void randomk_chain_kernel(RandomkArgs A) {
+  for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < A.total;
+       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t key = A.key_sorted[s], e = A.draw_sorted[s];
+    const uint32_t t = tensor_of_entry(A, e);
+    const uint64_t lo = A.list_off[t];
+    const uint32_t m = static_cast<uint32_t>(e - lo);
+    const bool run_prev = s > 0 && A.key_sorted[s - 1] == key;  // same target => same tensor
+    A.prv[e] = run_prev ? static_cast<uint32_t>(A.draw_sorted[s - 1] - lo) : kNone;
+    const uint64_t p = key - A.t_begin[t];
+    if (p < A.list_off[t + 1] - lo && m < p) {
+      const bool last = s + 1 == A.total || A.key_sorted[s + 1] != key ||
+                        A.draw_sorted[s + 1] - lo >= p;
+      if (last) A.src[lo + p] = m;
+    }
+  }
+}
+
 // Position i of the pool after the k swaps holds S_i = V(j_i, i), where
 // V(p, i) is p unless an earlier draw m targeted p (then W(m)), and W(m), the
 // content of position m when draw m starts, is m unless an earlier draw
-// targeted position m (then W of that draw).  kept[S] = c, r[S] = c - c.
-template <typename T>
-__global__ void randomk_gather_kernel(RandomkArgs A, T* __restrict__ r, T* __restrict__ kept,
-                                      int kept_mean, uint32_t* __restrict__ list_idx,
-                                      T* __restrict__ list_val) {
+// targeted position m (then W of that draw).  pos[i] = flat S_i.
+__global__ void randomk_resolve_kernel(RandomkArgs A) {
   for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < A.total;
        e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t t = tensor_of_entry(A, e);
@@ -945,12 +1010,71 @@ __global__ void randomk_gather_kernel(RandomkArgs A, T* __restrict__ r, T* __res
     } else {
       s = j;
     }
-    const uint64_t flat = A.t_begin[t] + s;
-    const T c = r[flat];
-    list_idx[e] = static_cast<uint32_t>(flat);
-    list_val[e] = c;
-    if (kept) kept[flat] = kept_value(c, kept_mean);
-    r[flat] = sub_rn(c, c);
+    A.pos[e] = static_cast<uint32_t>(A.t_begin[t] + s);
+    if (A.bits) atomicOr(&A.bits[(A.t_begin[t] + s) / 32], 1u << ((A.t_begin[t] + s) % 32));
+    if (A.tbits) A.table[A.slot[e]] = 0ull;  // the chain pass was the table's last reader
+  }
+}
+
+// Empty the sample bitmap again: the words of the previous selection drawn
+// into this buffer (its positions are still in pos).
+__global__ void randomk_unmark_kernel(const uint32_t* __restrict__ pos, uint64_t total,
+                                      uint32_t* __restrict__ bits) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    bits[pos[e] / 32] = 0u;
+}
+
+// Samples per filter tile (one warp per tile; tile ntiles = the scalar tail
+// [ntiles * te, n)), for the list offsets of the fused pass.
+__global__ void randomk_tile_count_kernel(const uint32_t* __restrict__ bits, uint64_t te,
+                                          uint64_t ntiles, uint64_t n, uint32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x / 32) + (threadIdx.x >> 5);
+       k <= ntiles; k += nw) {
+    const uint64_t e0 = k * te, e1 = k < ntiles ? min(e0 + te, n) : n;
+    uint32_t c = 0;
+    if (e1 > e0)
+      for (uint64_t q = e0 / 32 + lane; q <= (e1 - 1) / 32; q += 32) {
+        uint32_t w = bits[q];
+        if (q * 32 < e0) w &= ~0u << (e0 - q * 32);
+        if (q * 32 + 32 > e1) w &= (1u << (e1 - q * 32)) - 1u;
+        c += __popc(w);
+      }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[k] = c;
+  }
+}
+
+// The data pass of the selection: kept[S] = c, r[S] = c - c, list = (S, c).
+// Four draws in flight per thread (one dependent gather each).
+template <typename T>
+__global__ void randomk_gather_kernel(const uint32_t* __restrict__ pos, uint64_t total,
+                                      T* __restrict__ r, T* __restrict__ kept, int kept_mean,
+                                      uint32_t* __restrict__ list_idx, T* __restrict__ list_val) {
+  constexpr int kQ = 4;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t e0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e0 < total;
+       e0 += stride * kQ) {
+    uint32_t f[kQ];
+    T c[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const uint64_t e = e0 + q * stride;
+      f[q] = e < total ? pos[e] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) c[q] = e0 + q * stride < total ? r[f[q]] : T(0);
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const uint64_t e = e0 + q * stride;
+      if (e >= total) continue;
+      list_idx[e] = f[q];
+      list_val[e] = c[q];
+      if (kept) kept[f[q]] = kept_value(c[q], kept_mean);
+      r[f[q]] = sub_rn(c[q], c[q]);
+    }
   }
 }
 
@@ -1208,25 +1332,75 @@ cudaError_t launch_topk(int dtype, const TopkArgs& a, int sms, cudaStream_t s) {
 cudaError_t launch_randomk_select(const RandomkArgs& a, int sms, cudaStream_t s) {
   if (a.total == 0) return cudaSuccess;
   const int grid = grid_for(a.total, sms, 8);
+  int bits = 1;  // key bits to sort: flat positions < 2^bits
+  while (bits < 32 && (uint64_t(1) << bits) <= a.layout_n) ++bits;
   randomk_draw_kernel<<<grid, kThreads, 0, s>>>(a);
   randomk_replay_kernel<<<(a.ntensors + 63) / 64, 64, 0, s>>>(a);
-  randomk_link_kernel<<<grid, kThreads, 0, s>>>(a);
+  if (a.tbits) {
+    randomk_link_kernel<<<grid, kThreads, 0, s>>>(a);
+    randomk_chain_hash_kernel<<<grid, kThreads, 0, s>>>(a);
+    randomk_resolve_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  cudaError_t e = cudaMemsetAsync(a.src, 0xff, a.total * 4, s);  // kNone
+  if (e == cudaSuccess) {
+    size_t tmp = a.sort_tmp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(a.sort_tmp, tmp, a.key, a.key_sorted, a.draw_iota,
+                                        a.draw_sorted, static_cast<int>(a.total), 0, bits, s);
+  }
+  if (e != cudaSuccess) return e;
   randomk_chain_kernel<<<grid, kThreads, 0, s>>>(a);
+  randomk_resolve_kernel<<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_randomk_gather(int dtype, const RandomkArgs& a, void* r, void* kept,
-                                  int kept_mean, uint32_t* list_idx, void* list_val, int sms,
+size_t randomk_sort_bytes(uint64_t total) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr),
+                                  static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), static_cast<int>(total), 0, 32);
+  return b;
+}
+
+cudaError_t launch_randomk_unmark(const uint32_t* pos, uint64_t total, uint32_t* bits, int sms,
                                   cudaStream_t s) {
-  if (a.total == 0) return cudaSuccess;
-  const int grid = grid_for(a.total, sms, 8);
+  if (total == 0) return cudaSuccess;
+  randomk_unmark_kernel<<<grid_for(total, sms, 8), kThreads, 0, s>>>(pos, total, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_randomk_tile_offsets(const uint32_t* bits, uint64_t te, uint64_t ntiles,
+                                        uint64_t n, uint32_t* cnt, uint32_t* toff, void* tmp,
+                                        size_t tmp_bytes, int sms, cudaStream_t s) {
+  const uint64_t warps = ntiles + 1;
+  const int grid = static_cast<int>(std::min<uint64_t>((warps + kWarps - 1) / kWarps,
+                                                       static_cast<uint64_t>(sms) * 8));
+  randomk_tile_count_kernel<<<grid, kThreads, 0, s>>>(bits, te, ntiles, n, cnt);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, toff, static_cast<int>(ntiles + 1), s);
+}
+
+size_t randomk_scan_bytes(uint64_t ntiles) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const uint32_t*>(nullptr),
+                                static_cast<uint32_t*>(nullptr), static_cast<int>(ntiles + 1));
+  return b;
+}
+
+cudaError_t launch_randomk_gather(int dtype, const uint32_t* pos, uint64_t total, void* r,
+                                  void* kept, int kept_mean, uint32_t* list_idx, void* list_val,
+                                  int sms, cudaStream_t s) {
+  if (total == 0) return cudaSuccess;
+  const int grid = grid_for((total + 3) / 4, sms, 8);
   if (dtype == 1)
     randomk_gather_kernel<double><<<grid, kThreads, 0, s>>>(
-        a, static_cast<double*>(r), static_cast<double*>(kept), kept_mean, list_idx,
+        pos, total, static_cast<double*>(r), static_cast<double*>(kept), kept_mean, list_idx,
         static_cast<double*>(list_val));
   else
     randomk_gather_kernel<float><<<grid, kThreads, 0, s>>>(
-        a, static_cast<float*>(r), static_cast<float*>(kept), kept_mean, list_idx,
+        pos, total, static_cast<float*>(r), static_cast<float*>(kept), kept_mean, list_idx,
         static_cast<float*>(list_val));
   return cudaGetLastError();
 }

@@ -112,18 +112,45 @@ struct RandomkArgs {
   uint64_t step;
   int raw_seed;               // 1: draw from SplitMix64(seed) itself (randomk_compress)
   uint32_t* j;                // draw targets (local)
-  uint32_t* nxt;
+  // sort variant (tbits = 0)
+  uint32_t* key;              // draw targets (flat), the sort keys
+  const uint32_t* draw_iota;  // 0, 1, ..., total - 1 (the sort values)
+  uint32_t* key_sorted;
+  uint32_t* draw_sorted;
+  void* sort_tmp;
+  size_t sort_tmp_bytes;
+  uint64_t layout_n;          // elements in the layout (the sort key range)
   uint32_t* prv;
   uint32_t* src;
-  unsigned long long* head;   // per flat position: (tag << 32) | last draw targeting it
-  uint32_t tag;               // this selection's epoch (> 0): entries of other epochs are empty
+  // hash variant (tbits > 0): table of 2^tbits words, all 0 between
+  // selections; per draw its slot and the next draw of its target's list
+  unsigned long long* table;
+  uint32_t tbits;
+  uint32_t* slot;
+  uint32_t* nxt;
   int* reject;                // per tensor
+  uint32_t* pos;              // out: flat index S_e of every draw (data independent)
+  uint32_t* bits;             // out (may be NULL): bit S_e of the sample bitmap set
 };
+// The selection alone (draws, rejection replay, swap-chain resolution) ->
+// pos.  Depends only on (seed, step, numels), never on the gradient, so it
+// may run ahead of the step that uses it.
 cudaError_t launch_randomk_select(const RandomkArgs& a, int sms, cudaStream_t s);
-// list[e] = (flat index S_e, c); kept[S] = c; r[S] = c - c.
-cudaError_t launch_randomk_gather(int dtype, const RandomkArgs& a, void* r, void* kept,
-                                  int kept_mean, uint32_t* list_idx, void* list_val, int sms,
+size_t randomk_sort_bytes(uint64_t total);
+// Sample bitmap bookkeeping for the fused random-k pass (covap_kernels.cu
+// op 6): clear the words a previous selection set (its pos), and the list
+// offset of every filter tile (exclusive scan of the per-tile sample counts;
+// tile ntiles is the scalar tail).
+cudaError_t launch_randomk_unmark(const uint32_t* pos, uint64_t total, uint32_t* bits, int sms,
                                   cudaStream_t s);
+cudaError_t launch_randomk_tile_offsets(const uint32_t* bits, uint64_t te, uint64_t ntiles,
+                                        uint64_t n, uint32_t* cnt, uint32_t* toff, void* tmp,
+                                        size_t tmp_bytes, int sms, cudaStream_t s);
+size_t randomk_scan_bytes(uint64_t ntiles);
+// list[e] = (pos[e], c); kept[pos] = c; r[pos] = c - c.
+cudaError_t launch_randomk_gather(int dtype, const uint32_t* pos, uint64_t total, void* r,
+                                  void* kept, int kept_mean, uint32_t* list_idx, void* list_val,
+                                  int sms, cudaStream_t s);
 
 // Exchange side (the mean of the kept gradients over P ranks, trainer.cpp:402
 // and 35-47): out was zero-filled by the compensation pass.

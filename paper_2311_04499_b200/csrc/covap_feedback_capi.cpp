@@ -64,12 +64,28 @@ struct covap_feedback {
   void* acc = nullptr;  // rank-ordered scatter accumulator, zero between steps
   // random-k
   uint32_t* tensor_of = nullptr;
-  uint32_t *j = nullptr, *nxt = nullptr, *prv = nullptr, *src = nullptr;
-  unsigned long long* head = nullptr;  // epoch-tagged list heads, one per flat position
-  uint32_t rk_epoch = 0;               // random-k selections made (the head tag)
+  uint32_t *j = nullptr, *prv = nullptr, *src = nullptr;
+  uint32_t *key = nullptr, *draw_iota = nullptr, *key_sorted = nullptr, *draw_sorted = nullptr;
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  unsigned long long* table = nullptr;  // hash variant of the selection (tbits > 0)
+  uint32_t tbits = 0;
+  uint32_t *slot = nullptr, *nxt = nullptr;
   int* reject = nullptr;
   cudaStream_t side = nullptr;  // index sampling, concurrent with the compensation pass
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // Selections made ahead: pos[b] holds the flat sampled positions of step
+  // pos_step[b] (b = step & 1) once ev_pos[b] completes; ev_used[b] marks
+  // the gather that last read pos[b].
+  uint32_t* pos[2] = {nullptr, nullptr};
+  uint32_t* bits[2] = {nullptr, nullptr};  // sample bitmaps (n / 32 + 8 words), zero between uses
+  uint32_t* toff[2] = {nullptr, nullptr};  // list offset of every filter tile
+  uint64_t rk_te = 0, rk_ntiles = 0;       // the fused pass's tile geometry
+  uint32_t* rk_cnt = nullptr;
+  void* rk_tmp = nullptr;
+  size_t rk_tmp_bytes = 0;
+  uint64_t pos_step[2] = {~0ull, ~0ull};
+  cudaEvent_t ev_pos[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   // wire
   uint32_t* list_idx = nullptr;
   void* list_val = nullptr;
@@ -98,6 +114,10 @@ void release(covap_feedback* f) {
   for (void* p : f->owned) cudaFree(p);
   if (f->ev_fork) cudaEventDestroy(f->ev_fork);
   if (f->ev_join) cudaEventDestroy(f->ev_join);
+  for (int b = 0; b < 2; ++b) {
+    if (f->ev_pos[b]) cudaEventDestroy(f->ev_pos[b]);
+    if (f->ev_used[b]) cudaEventDestroy(f->ev_used[b]);
+  }
   if (f->side) cudaStreamDestroy(f->side);
   if (f->recv_a) cudaFree(f->recv_a);
   if (f->recv_b) cudaFree(f->recv_b);
@@ -121,8 +141,9 @@ double coeff_of(const covap_feedback* f) {
                        : 0.0;
 }
 
-fb::RandomkArgs randomk_args(covap_feedback* f) {
+fb::RandomkArgs randomk_args(covap_feedback* f, uint64_t step, uint32_t* pos) {
   fb::RandomkArgs a{};
+  a.pos = pos;
   a.t_begin = f->d_begin;
   a.t_numel = f->d_numel;
   a.list_off = f->d_list_off;
@@ -130,21 +151,40 @@ fb::RandomkArgs randomk_args(covap_feedback* f) {
   a.ntensors = static_cast<uint32_t>(f->numel.size());
   a.total = f->k_total;
   a.seed = f->filter.seed;
-  a.step = f->num_steps;
+  a.step = step;
   a.j = f->j;
-  a.nxt = f->nxt;
+  a.key = f->key;
+  a.draw_iota = f->draw_iota;
+  a.key_sorted = f->key_sorted;
+  a.draw_sorted = f->draw_sorted;
+  a.sort_tmp = f->sort_tmp;
+  a.sort_tmp_bytes = f->sort_tmp_bytes;
+  a.layout_n = f->total;
   a.prv = f->prv;
   a.src = f->src;
-  a.head = f->head;
-  a.tag = ++f->rk_epoch;
-  if (a.tag == 0) {  // 2^32 selections: clear the heads and start over
-    CK(cudaDeviceSynchronize());
-    CK(cudaMemset(f->head, 0, std::max<uint64_t>(f->total, 1) * 8));
-    CK(cudaDeviceSynchronize());
-    a.tag = f->rk_epoch = 1;
-  }
+  a.table = f->table;
+  a.tbits = f->tbits;
+  a.slot = f->slot;
+  a.nxt = f->nxt;
   a.reject = f->reject;
   return a;
+}
+
+#ifndef COVAP_RK_AHEAD  // random-k: draw step s + 1's selection during step s
+#define COVAP_RK_AHEAD 1
+#endif
+
+// Random-k selection of `step` into buffer b on the side stream: positions,
+// sample bitmap (the previous selection's words cleared first), per-tile
+// list offsets of the fused pass; ev_pos[b] marks completion.
+void randomk_select_marks(covap_feedback* f, uint64_t step, int b) {
+  CK(fb::launch_randomk_unmark(f->pos[b], f->k_total, f->bits[b], f->sms, f->side));
+  fb::RandomkArgs a = randomk_args(f, step, f->pos[b]);
+  a.bits = f->bits[b];
+  CK(fb::launch_randomk_select(a, f->sms, f->side));
+  CK(fb::launch_randomk_tile_offsets(f->bits[b], f->rk_te, f->rk_ntiles, f->total, f->rk_cnt,
+                                     f->toff[b], f->rk_tmp, f->rk_tmp_bytes, f->sms, f->side));
+  CK(cudaEventRecord(f->ev_pos[b], f->side));
 }
 
 // The error-feedback step.  kept: dense kept gradient (NULL = not wanted);
@@ -216,26 +256,41 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       break;
     }
     case COVAP_FILTER_RANDOMK: {
-      // The sampled indices depend only on (seed, step, t): they are drawn on
-      // a side stream while the compensation pass streams the gradient.
-      const fb::RandomkArgs a = randomk_args(f);
+      // The sampled positions depend only on (seed, step, numels), never on
+      // the gradient, so they are drawn on a side stream one step ahead: the
+      // selection of step s + 1 (draws -> positions -> sample bitmap ->
+      // per-tile list offsets) runs under step s's pass.  The step itself is
+      // ONE streaming pass (covap_kernels.cu op 6) that patches the sampled
+      // elements into its tiles: r = c - c, kept, the list in position order.
+      // A step that was not drawn ahead (the first, or after set_step /
+      // reset) draws its own first.  Under stream capture nothing is left
+      // pending across steps.
+      if (kept) need(kept == zero, "random-k: kept must be the zero-filled output");
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      CK(cudaStreamIsCapturing(st, &cap));
+      const bool ahead = COVAP_RK_AHEAD && cap == cudaStreamCaptureStatusNone;
+      const uint64_t s0 = f->num_steps;
+      const int b0 = static_cast<int>(s0 & 1), b1 = b0 ^ 1;
       CK(cudaEventRecord(f->ev_fork, st));
       CK(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
-      CK(fb::launch_randomk_select(a, f->sms, f->side));
-      CK(cudaEventRecord(f->ev_join, f->side));
-      // No histogram is needed, so the compensation pass is the TMA-bulk
-      // filter pass with an empty selection (r = c, zero-filled output):
-      // covap_kernels.cu's K1F / K1 pipeline, 0.9-1.0 of the copy peak.
-      if (zero)
-        CK(covapb::launch_filter_unpack(dt, grad, f->residual, zero, nullptr, 0, 0, f->total, coeff,
-                                        f->ef.enabled, 1.0, st));
-      else
-        CK(covapb::launch_filter_pack(dt, grad, f->residual, nullptr, nullptr, 0, 0, f->total, coeff,
-                                      f->ef.enabled, st));
-      CK(cudaStreamWaitEvent(st, f->ev_join, 0));
-      CK(fb::launch_randomk_gather(dt, a, f->residual, kept, kept_mean ? 1 : 0, f->list_idx,
-                                   f->list_val, f->sms,
-                                   st));
+      if (!ahead || f->pos_step[b0] != s0) {
+        if (ahead) CK(cudaStreamWaitEvent(f->side, f->ev_used[b0], 0));
+        randomk_select_marks(f, s0, b0);
+        f->pos_step[b0] = ahead ? s0 : ~0ull;
+      }
+      CK(cudaStreamWaitEvent(st, f->ev_pos[b0], 0));
+      CK(covapb::launch_filter_randomk(dt, grad, f->residual, zero, kept ? 1 : 0, kept_mean ? 1 : 0,
+                                       f->bits[b0], f->toff[b0], f->list_idx, f->list_val,
+                                       f->total, coeff, f->ef.enabled, st));
+      CK(cudaEventRecord(f->ev_used[b0], st));
+      if (ahead) {  // step s0 + 1, into the buffers step s0 - 1's pass read
+        CK(cudaStreamWaitEvent(f->side, f->ev_used[b1], 0));
+        randomk_select_marks(f, s0 + 1, b1);
+        f->pos_step[b1] = s0 + 1;
+      } else {  // join the side stream back into the capture
+        CK(cudaEventRecord(f->ev_join, f->side));
+        CK(cudaStreamWaitEvent(st, f->ev_join, 0));
+      }
       break;
     }
     default:
@@ -420,17 +475,50 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
                   static_cast<uint32_t>(t));
       f->tensor_of = dalloc<uint32_t>(f, f->k_total * 4);
       CK(cudaMemcpy(f->tensor_of, owner.data(), f->k_total * 4, cudaMemcpyHostToDevice));
+      need(f->k_total < 0x7fffffffull, "random-k: at most 2^31 - 1 samples per state");
       f->j = dalloc<uint32_t>(f, f->k_total * 4);
-      f->nxt = dalloc<uint32_t>(f, f->k_total * 4);
       f->prv = dalloc<uint32_t>(f, f->k_total * 4);
       f->src = dalloc<uint32_t>(f, f->k_total * 4);
-      f->head = dalloc<unsigned long long>(f, f->total * 8);
-      CK(cudaMemset(f->head, 0, std::max<uint64_t>(f->total, 1) * 8));  // tag 0: never current
+      f->key = dalloc<uint32_t>(f, f->k_total * 4);
+      // up to 2^20 draws: per-position lists in a hash table at load <= 1/2
+      // (<= 16 MB, L2-resident); more: a radix sort of the draws by target
+      f->tbits = 10;
+      while ((uint64_t(1) << f->tbits) < 2 * f->k_total) ++f->tbits;
+      if (f->tbits > 21) f->tbits = 0;
+      if (f->tbits) {
+        f->table = dalloc<unsigned long long>(f, (uint64_t(1) << f->tbits) * 8);
+        CK(cudaMemset(f->table, 0, (uint64_t(1) << f->tbits) * 8));
+        f->slot = dalloc<uint32_t>(f, f->k_total * 4);
+        f->nxt = dalloc<uint32_t>(f, f->k_total * 4);
+      } else {
+        f->key_sorted = dalloc<uint32_t>(f, f->k_total * 4);
+        f->draw_sorted = dalloc<uint32_t>(f, f->k_total * 4);
+        std::vector<uint32_t> iota(f->k_total);
+        for (uint64_t e = 0; e < f->k_total; ++e) iota[e] = static_cast<uint32_t>(e);
+        f->draw_iota = dalloc<uint32_t>(f, f->k_total * 4);
+        CK(cudaMemcpy(f->draw_iota, iota.data(), f->k_total * 4, cudaMemcpyHostToDevice));
+        f->sort_tmp_bytes = fb::randomk_sort_bytes(f->k_total);
+        f->sort_tmp = dalloc<void>(f, f->sort_tmp_bytes);
+      }
       f->reject = dalloc<int>(f, n_tensors * 4);
       CK(cudaMemset(f->reject, 0, n_tensors * 4));
       CK(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming));
+      CK(covapb::filter_tiles(f->dtype == COVAP_F64 ? 1 : 0, f->total, &f->rk_te, &f->rk_ntiles));
+      f->rk_cnt = dalloc<uint32_t>(f, (f->rk_ntiles + 1) * 4);
+      f->rk_tmp_bytes = fb::randomk_scan_bytes(f->rk_ntiles);
+      f->rk_tmp = dalloc<void>(f, f->rk_tmp_bytes);
+      for (int b = 0; b < 2; ++b) {
+        f->pos[b] = dalloc<uint32_t>(f, f->k_total * 4);
+        CK(cudaMemset(f->pos[b], 0, std::max<uint64_t>(f->k_total, 1) * 4));
+        f->bits[b] = dalloc<uint32_t>(f, (f->total / 32 + 8) * 4);
+        CK(cudaMemset(f->bits[b], 0, (f->total / 32 + 8) * 4));
+        f->toff[b] = dalloc<uint32_t>(f, ((f->rk_ntiles + 1) / 4 * 4 + 8) * 4);
+        CK(cudaMemset(f->toff[b], 0, ((f->rk_ntiles + 1) / 4 * 4 + 8) * 4));
+        CK(cudaEventCreateWithFlags(&f->ev_pos[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&f->ev_used[b], cudaEventDisableTiming));
+      }
     }
     CK(cudaDeviceSynchronize());
     *out = f;
@@ -638,12 +726,12 @@ covap_status covap_randomk_compress(int device, int dtype, const void* x, uint64
     const int dt = dtype == COVAP_F64 ? 1 : 0;
     CK(fb::launch_compensate(dt, x, f->residual, nullptr, nullptr, f->chunks, f->nchunks, 0, 0.0,
                              f->sms, s));
-    fb::RandomkArgs a = randomk_args(f);
+    fb::RandomkArgs a = randomk_args(f, 0, f->pos[0]);
     a.raw_seed = 1;
     a.seed = seed;
     CK(fb::launch_randomk_select(a, f->sms, s));
-    CK(fb::launch_randomk_gather(dt, a, f->residual, nullptr, 0, f->list_idx, f->list_val, f->sms,
-                                 s));
+    CK(fb::launch_randomk_gather(dt, f->pos[0], f->k_total, f->residual, nullptr, 0, f->list_idx,
+                                 f->list_val, f->sms, s));
     CK(fb::order_list(dt, fb::kRandomk, f->list_idx, f->list_val, f->k_total, indices, values, s));
     CK(cudaStreamSynchronize(s));
     *k = f->k_total;

@@ -36,6 +36,8 @@
 #include <algorithm>
 #include <mutex>
 
+#include <cub/cub.cuh>
+
 #include "covap_half.cuh"
 #include "covap_internal.h"
 
@@ -87,6 +89,13 @@ constexpr uint32_t kSmemK1Sgd = (3 * kStages + 3) * kTileK1;
 // buffer a residual tile, a kept tile and the tile's fp16 wire halves.
 constexpr uint32_t kStageFp16 = 2 * kTileK1 + kTileK1 / 2;
 constexpr uint32_t kSmemK1Fp16 = 2 * kStages * kTileK1 + 2 * kStageFp16;
+// K1 random-k (op 6): the K1F layout plus two out staging tiles (the sampled
+// kept values on zeros) and, per slot, the tile's window of the sample
+// bitmap and of the per-tile list offsets.
+constexpr uint32_t kBmWords = kTileK1 / 4 / 32 + 8;  // bitmap window, 16-byte aligned ends
+constexpr uint32_t kSlotRk = kBmWords * 4 + 16;
+constexpr uint32_t kSmemK1Rk = (2 * kStages + 5) * kTileK1 + kStages * kSlotRk;
+static_assert(kSmemK1Rk <= 227 * 1024, "op 6 shared memory");
 // K2: kStagesK2 recv slots + 2 staging tiles + 1 zero tile; K2+SGD adds a
 // params tile per slot.
 constexpr uint32_t kTileK2 = COVAP_K2_TILE;
@@ -287,11 +296,20 @@ struct Args {
   int zfill;       // K2: zero-fill unselected slots (0: K1 did it); K1 (op 0): out != NULL zero-fills
   uint16_t* wire;  // fp16 (op 5): half bits of the kept values, or NULL
   unsigned long long* sat;  // fp16: saturation count (compress.cpp:185-190), or NULL
+  // random-k (op 6): sample bitmap (bit e of word e / 32), per-tile list
+  // offsets (samples before each tile; entry ntiles: before the tail), the
+  // list; keep: out receives the sampled kept values (as (0 + c) when mean)
+  const uint32_t* bits;
+  const uint32_t* toff;
+  uint32_t* list_idx;
+  T* list_val;
+  int keep;
 };
 
 // Operations of the element path / the filter kernel:
 //   0 K1 pack, 1 K1F (one rank, out), 2 K2 unpack,
-//   3 K1F + SGD (one rank, params -= lr * update), 4 K2 + SGD.
+//   3 K1F + SGD (one rank, params -= lr * update), 4 K2 + SGD,
+//   5 fp16 filter, 6 random-k filter (see filter_kernel).
 // SGD restates trainer.cpp:408-409, params -= learning_rate * update, with
 // the multiply and the subtraction rounded separately.  Unselected elements
 // have update 0 and p - lr * 0 == p, so their parameters are not touched.
@@ -362,6 +380,85 @@ __device__ void edges(const Args<T>& A, uint64_t a16, uint64_t b16) {
   }
 }
 
+// ------------------------------------------------------------ random-k (op 6)
+//
+// The random-k filter under error feedback in one streaming pass
+// (compress.cpp:283-298, 323-344): every element gets r = c, out = 0 (the
+// compensation pass), except the sampled ones, which get r = c - c, out = the
+// kept value, and go to the wire list.  The sample positions are data
+// independent and arrive as a bitmap plus per-tile list offsets
+// (covap_feedback.cu, drawn a step ahead on a side stream), so the pass
+// patches its smem tiles before their bulk stores: no gather afterwards, and
+// the list comes out in position order (the same on every rank).
+
+// Sequential elements [a, a16) and [b16, b) (fewer than 2 x 4), thread 0.
+template <typename T>
+__device__ void rk_edges(const Args<T>& A, uint64_t a, uint64_t a16, uint64_t b16, uint64_t b,
+                         uint32_t tail_off) {
+  uint32_t slot = tail_off;
+  auto one = [&](uint64_t e) {
+    const T gv = A.g[e];
+    const T c = A.ef ? add_rn(gv, mul_rn(A.coeff, A.r[e])) : gv;
+    if ((A.bits[e / 32] >> (e % 32)) & 1u) {
+      A.r[e] = sub_rn(c, c);
+      if (A.out) A.out[e] = A.keep ? (A.mean ? add_rn(T(0), c) : c) : T(0);
+      A.list_idx[slot] = static_cast<uint32_t>(e);
+      A.list_val[slot] = c;
+      ++slot;
+    } else {
+      A.r[e] = c;
+      if (A.out) A.out[e] = T(0);
+    }
+  };
+  // the head precedes every tile, but op 6 launches start at 0 (no head)
+  for (uint64_t e = a; e < a16; ++e) one(e);
+  for (uint64_t e = b16; e < b; ++e) one(e);
+}
+
+// Patch tile [e0, e1) (staged compensated values st): sampled elements get
+// st = c - c, ot = kept value, and their list slots.  ot holds zeros except
+// where this tile writes it.  Block-wide; ends with the tile's writes done.
+template <typename T, int NT>
+__device__ __forceinline__ void rk_patch(const Args<T>& A, T* st, T* ot, const unsigned char* slot,
+                                         uint64_t e0, uint64_t e1, uint64_t kg) {
+  using Scan = cub::BlockScan<uint32_t, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  const uint32_t* bw = reinterpret_cast<const uint32_t*>(slot);
+  const uint32_t base = reinterpret_cast<const uint32_t*>(slot + kBmWords * 4)[kg & 3];
+  const uint64_t wa = e0 / 32, wb = (e1 - 1) / 32;
+  const uint32_t wlo = static_cast<uint32_t>(wa) & ~3u;
+  const uint32_t nw = static_cast<uint32_t>(wb - wa + 1);  // <= TE / 32 + 2 <= NT
+  uint32_t w = 0;
+  if (threadIdx.x < nw) {
+    const uint64_t q = wa + threadIdx.x;
+    w = bw[q - wlo];
+    if (q * 32 < e0) w &= ~0u << (e0 - q * 32);
+    if (q * 32 + 32 > e1) w &= (1u << (e1 - q * 32)) - 1u;  // e1 - 32q in [1, 31]
+  }
+  if (A.keep) {  // clear ot of the tile this staging buffer carried two tiles ago
+    using V = typename Vec16<T>::type;
+    constexpr uint32_t W = 16 / sizeof(T);
+    V z;
+#pragma unroll
+    for (int q = 0; q < static_cast<int>(W); ++q) lane(z, q) = T(0);
+    const uint32_t n = static_cast<uint32_t>(e1 - e0);
+    for (uint32_t v = threadIdx.x; v < n / W; v += NT) reinterpret_cast<V*>(ot)[v] = z;
+  }
+  uint32_t rank = 0;
+  Scan(tmp).ExclusiveSum(static_cast<uint32_t>(__popc(w)), rank);  // its barriers order the ot fill
+  rank += base;
+  for (; w; w &= w - 1) {
+    const uint64_t e = (wa + threadIdx.x) * 32 + (__ffs(w) - 1);
+    const uint32_t i = static_cast<uint32_t>(e - e0);
+    const T c = st[i];
+    st[i] = sub_rn(c, c);
+    if (A.keep) ot[i] = A.mean ? add_rn(T(0), c) : c;
+    A.list_idx[rank] = static_cast<uint32_t>(e);
+    A.list_val[rank] = c;
+    ++rank;
+  }
+}
+
 // ------------------------------------------------------------ K1 / K1F / K1F+SGD
 //
 // Input ring: kStages slots of (g, r[, params]) tiles, refilled as soon as the
@@ -384,8 +481,8 @@ __host__ __device__ constexpr int filter_threads() {
 template <typename T, int OP>
 __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const Args<T> A) {
   constexpr int NT = filter_threads<OP>();
-  static_assert(OP == 0 || OP == 1 || OP == 3 || OP == 5,
-                "filter_kernel ops: 0 pack, 1 K1F, 3 K1F+SGD, 5 fp16 filter");
+  static_assert(OP == 0 || OP == 1 || OP == 3 || OP == 5 || OP == 6,
+                "filter_kernel ops: 0 pack, 1 K1F, 3 K1F+SGD, 5 fp16 filter, 6 random-k filter");
   constexpr uint32_t TE = kTileK1 / sizeof(T);  // elements per tile
   using V = typename Vec16<T>::type;
   constexpr uint32_t W = 16 / sizeof(T);
@@ -395,11 +492,18 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
   T* pin = rin + kStages * TE;                          // kStages tiles (params, OP 3)
   T* stage = (OP == 3 ? pin + kStages * TE : pin);      // 2 staging tiles
   T* zero = stage + 2 * TE;                             // zero tile
+  T* ostage = zero + TE;                                // op 6: 2 out staging tiles
+  unsigned char* rkslot = reinterpret_cast<unsigned char*>(ostage + 2 * TE);  // op 6: kStages x kSlotRk
   __shared__ __align__(8) uint64_t bar[kStages];
 
   pdl_launch_dependents();
   const uint64_t a16 = (A.a + W - 1) / W * W;
   const uint64_t b16 = A.b / W * W;
+  if (OP == 6 && a16 >= b16) {  // nothing vector-sized
+    pdl_wait();
+    if (blockIdx.x == 0 && threadIdx.x == 0) rk_edges<T>(A, A.a, A.b, A.b, A.b, A.toff[0]);
+    return;
+  }
   if (a16 >= b16) {  // nothing vector-sized: element path only
     pdl_wait();
     if (blockIdx.x == 0) {
@@ -423,7 +527,11 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
   fence_async_smem();
   __syncthreads();
   pdl_wait();  // the previous kernel's writes (r, out, ...) are visible from here
-  if (blockIdx.x == 0) edges<T, OP>(A, a16, b16);
+  if (OP == 6) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) rk_edges<T>(A, A.a, a16, b16, A.b, A.toff[ntiles]);
+  } else if (blockIdx.x == 0) {
+    edges<T, OP>(A, a16, b16);
+  }
 
   auto tile_lo = [&](uint64_t k) { return a16 + (blockIdx.x + k * gridDim.x) * te; };
   auto issue = [&](uint64_t k) {  // thread 0 only
@@ -432,7 +540,18 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
     const uint32_t bytes = static_cast<uint32_t>((e1 - e0) * sizeof(T));
     bool with_params = false;
     if (OP == 3) with_params = classify<T>(A.runs, A.nruns, e0, e1).cls == kFull;
-    mbar_arrive_tx(&bar[s], (A.ef ? 2 : 1) * bytes + (with_params ? bytes : 0));
+    uint32_t rk_bytes = 0, wlo = 0, wbytes = 0;
+    if (OP == 6) {  // the tile's bitmap words and its list offset, 16-byte windows
+      wlo = static_cast<uint32_t>(e0 / 32) & ~3u;
+      wbytes = (((static_cast<uint32_t>((e1 + 31) / 32) + 3u) & ~3u) - wlo) * 4u;
+      rk_bytes = wbytes + 16;
+    }
+    mbar_arrive_tx(&bar[s], (A.ef ? 2 : 1) * bytes + (with_params ? bytes : 0) + rk_bytes);
+    if (OP == 6) {
+      const uint64_t kg = blockIdx.x + k * gridDim.x;
+      bulk_load(rkslot + s * kSlotRk, A.bits + wlo, wbytes, &bar[s]);
+      bulk_load(rkslot + s * kSlotRk + kBmWords * 4, A.toff + (kg & ~3ull), 16, &bar[s]);
+    }
     bulk_load(gin + s * TE, A.g + e0, bytes, &bar[s]);
     if (A.ef) bulk_load(rin + s * TE, A.r + e0, bytes, &bar[s]);
     if (with_params) bulk_load(pin + s * TE, A.out + e0, bytes, &bar[s]);
@@ -593,6 +712,8 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
         pos = end;
       }
     }
+    T* ot = ostage + (k & 1) * TE;
+    if (OP == 6) rk_patch<T, NT>(A, st, ot, rkslot + s * kSlotRk, e0, e1, blockIdx.x + k * gridDim.x);
     fence_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -606,6 +727,7 @@ __global__ void __launch_bounds__(filter_threads<OP>(), 1) filter_kernel(const A
       } else if (sel.cls == kNone) {
         bulk_store(A.r + e0, st, bytes);      // r = compensated (compress.cpp:79)
         if (OP == 1 || (OP == 0 && A.out)) bulk_store(A.out + e0, zero, bytes);  // compress.cpp:91
+        if (OP == 6 && A.out) bulk_store(A.out + e0, A.keep ? ot : zero, bytes);
       }
       bulk_commit();  // one group per tile (possibly empty)
       if (k + kStages < my) issue(k + kStages);  // input slot s is consumed
@@ -1062,6 +1184,8 @@ cudaError_t shape(DeviceShape** out) {
         (e = opt_in(filter_kernel<double, 3>, kSmemK1Sgd)) ||
         (e = opt_in(filter_kernel<float, 5>, kSmemK1Fp16)) ||
         (e = opt_in(filter_kernel<double, 5>, kSmemK1Fp16)) ||
+        (e = opt_in(filter_kernel<float, 6>, kSmemK1Rk)) ||
+        (e = opt_in(filter_kernel<double, 6>, kSmemK1Rk)) ||
         (e = opt_in(unpack_kernel<float, false>, kSmemK2)) ||
         (e = opt_in(unpack_kernel<float, true>, kSmemK2Sgd)) ||
         (e = opt_in(unpack_kernel<double, false>, kSmemK2)) ||
@@ -1124,6 +1248,11 @@ Args<T> make_args(const void* g, void* r, void* send, void* out, const void* rec
   A.zfill = 1;
   A.wire = nullptr;
   A.sat = nullptr;
+  A.bits = nullptr;
+  A.toff = nullptr;
+  A.list_idx = nullptr;
+  A.list_val = nullptr;
+  A.keep = 0;
   return A;
 }
 
@@ -1154,13 +1283,14 @@ cudaError_t pass(int op, const Args<T>& A, cudaStream_t s) {
   DeviceShape* sh;
   cudaError_t e = shape(&sh);
   if (e) return e;
-  const bool k1 = op == 0 || op == 1 || op == 3 || op == 5;
+  const bool k1 = op == 0 || op == 1 || op == 3 || op == 5 || op == 6;
   Args<T> B = A;
   const uint64_t min_tiles = static_cast<uint64_t>(sh->sms) * (k1 ? COVAP_K1_MIN_WAVES : COVAP_K2_MIN_WAVES);
   const unsigned grid = balance<T>(A.a, A.b, sh->sms, k1 ? kTileK1 : kTileK2, &B.te, min_tiles);
   if (op == 5) B.te = (B.te + 7) / 8 * 8;  // wire tiles: 16-byte multiples of halves
   switch (op) {
     case 5: return launch(filter_kernel<T, 5>, grid, kSmemK1Fp16, s, B, filter_threads<5>());
+    case 6: return launch(filter_kernel<T, 6>, grid, kSmemK1Rk, s, B, filter_threads<6>());
     case 0: return launch(filter_kernel<T, 0>, grid, kSmemK1, s, B, filter_threads<0>());
     case 1: return launch(filter_kernel<T, 1>, grid, kSmemK1, s, B, filter_threads<1>());
     case 3: return launch(filter_kernel<T, 3>, grid, kSmemK1Sgd, s, B, filter_threads<3>());
@@ -1274,6 +1404,39 @@ cudaError_t launch_filter_fp16(int dtype, const void* g, void* r, void* kept, in
     A.wire = wire;
     A.sat = sat;
     return pass<T>(5, A, s);
+  };
+  return dtype == 0 ? go(float(0)) : go(double(0));
+}
+
+cudaError_t filter_tiles(int dtype, uint64_t n, uint64_t* te, uint64_t* ntiles) {
+  DeviceShape* sh;
+  const cudaError_t e = shape(&sh);
+  if (e) return e;
+  const uint64_t W = dtype == 0 ? 4 : 2, b16 = n / W * W;
+  uint64_t t = 0;
+  if (dtype == 0)
+    balance<float>(0, n, sh->sms, kTileK1, &t, static_cast<uint64_t>(sh->sms) * COVAP_K1_MIN_WAVES);
+  else
+    balance<double>(0, n, sh->sms, kTileK1, &t, static_cast<uint64_t>(sh->sms) * COVAP_K1_MIN_WAVES);
+  *te = t;
+  *ntiles = b16 == 0 ? 0 : (b16 + t - 1) / t;
+  return cudaSuccess;
+}
+
+cudaError_t launch_filter_randomk(int dtype, const void* g, void* r, void* out, int keep,
+                                  int kept_mean, const uint32_t* bits, const uint32_t* toff,
+                                  uint32_t* list_idx, void* list_val, uint64_t n, double coeff,
+                                  int ef, cudaStream_t s) {
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    Args<T> A = make_args<T>(g, r, nullptr, out, nullptr, nullptr, 0, 0, n, coeff, ef, 1.0,
+                             kept_mean, 0.0);
+    A.bits = bits;
+    A.toff = toff;
+    A.list_idx = list_idx;
+    A.list_val = static_cast<T*>(list_val);
+    A.keep = keep;
+    return pass<T>(6, A, s);
   };
   return dtype == 0 ? go(float(0)) : go(double(0));
 }

@@ -113,6 +113,7 @@ def layout_buckets(covap, name):
     (4, 0.0, "resnet50", 3),
     (2, 0.01, "resnet50", 2),
     (3, 0.01, "resnet50", 2),
+    (3, 0.5, "resnet50", 2),  # 12.8 M samples: the sort variant of the selection
     (2, 0.001, "tablev", 1),
     (3, 0.05, "tablev", 1),
     (1, 0.0, "resnet50", 3),
@@ -348,3 +349,49 @@ def test_sync_one_rank_signed_zero_mean(covap, orc, kind, dtype):
     want = oracle_mean(orc, [k])
     assert np.all(bits(want)[gh == 0] == 0)  # +0.0, not -0.0
     np.testing.assert_array_equal(bits(out.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("kind", [2, 3])
+def test_unsynchronised_steps_and_step_jumps(covap, orc, kind):
+    """Random-k draws step s + 1's selection on a side stream during step s
+    (covap_feedback_capi.cpp, ef_step): consecutive steps issued without a
+    host synchronisation, on a user stream, and after num_steps jumps
+    (set_step forwards and back, reset) must all select exactly what the
+    reference selects for that step.  Top-k runs the same sequence (its
+    mark / expand collect pass keeps a per-chunk hit bitmap across launches)."""
+    sizes = [3, 5000, 70001, 1, 123457]
+    n = sum(sizes)
+    ef = (1, 0.3, 2, 0.2)
+    fb = F().ErrorFeedback(sizes, schedule(covap, ef), make_filter(kind, 1, 0.02, 11))
+    r = np.zeros(n, np.float32)
+    stream = torch.cuda.Stream()
+    steps = [0, 1, 2, 3, 7, 8, 2, 3, 3, 0, 1]
+    gs = []
+    for i, s in enumerate(steps):
+        key = orc.stream_key(23, 0, i)
+        g = torch.empty(n, dtype=torch.float32, device=DEV)
+        covap.generate(g, key, 0)
+        gs.append((g, orc.generate(key, n, kind=0, dtype=np.float32)))
+    torch.cuda.synchronize()
+    kepts, res = [], []
+    with torch.cuda.stream(stream):
+        for i, s in enumerate(steps):
+            if fb.num_steps != s:
+                fb.num_steps = s
+            kept = torch.empty(n, dtype=torch.float32, device=DEV)
+            fb.step(gs[i][0], kept=kept, stream=stream)
+            kepts.append(kept)
+            res.append(fb.residuals.clone())
+    torch.cuda.synchronize()
+    for i, s in enumerate(steps):
+        want, _, _ = orc.feedback_step(kind, s, gs[i][1], r, tensors_of(sizes), 1,
+                                       coeff_of(orc, ef, s), k_fraction=0.02, seed=11)
+        np.testing.assert_array_equal(bits(kepts[i].cpu().numpy()), bits(want), err_msg=f"#{i} step {s}")
+        np.testing.assert_array_equal(bits(res[i].cpu().numpy()), bits(r), err_msg=f"#{i} step {s}")
+    fb.reset()
+    r[:] = 0
+    for s in range(3):
+        kept = fb.step(gs[s][0]).cpu().numpy()
+        want, _, _ = orc.feedback_step(kind, s, gs[s][1], r, tensors_of(sizes), 1,
+                                       coeff_of(orc, ef, s), k_fraction=0.02, seed=11)
+        np.testing.assert_array_equal(bits(kept), bits(want), err_msg=f"after reset, step {s}")
