@@ -63,24 +63,20 @@ __global__ void ptr_kernel(ncclWindow_t w, ncclDevComm dc, void** out) {
   out[2] = dc.lsaMultimem.mcBasePtr ? ncclGetLsaMultimemPointer(w, 0, dc) : nullptr;
 }
 
-static int driver_multicast(int dev) {
+static int driver_multicast_try(int dev, CUmemAllocationHandleType ht, const char* hname) {
   CUdevice d;
   CU(cuDeviceGet(&d, dev));
-  int mc = 0;
-  CU(cuDeviceGetAttribute(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, d));
-  int fab = 0;
-  cuDeviceGetAttribute(&fab, CU_DEVICE_ATTRIBUTE_HANDLE_TYPE_FABRIC_SUPPORTED, d);
-  printf("multicast_supported=%d fabric_handles=%d\n", mc, fab);
-  if (!mc) return 0;
   const size_t n = 1 << 20;  // floats
   CUmulticastObjectProp mp{};
   mp.numDevices = 1;
   mp.size = n * 4;
-  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
-  size_t gran = 0;
+  mp.handleTypes = ht;
+  size_t gran = 0, gmin = 0;
   CU(cuMulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
-  mp.size = (mp.size + gran - 1) / gran * gran;
-  printf("multicast granularity %zu, size %zu\n", gran, mp.size);
+  CU(cuMulticastGetGranularity(&gmin, &mp, CU_MULTICAST_GRANULARITY_MINIMUM));
+  mp.size = (mp.size + gmin - 1) / gmin * gmin;
+  printf("[%s] multicast granularity recommended %zu minimum %zu, size %zu\n", hname, gran, gmin,
+         mp.size);
   CUmemGenericAllocationHandle mh, ph;
   CU(cuMulticastCreate(&mh, &mp));
   CU(cuMulticastAddDevice(mh, d));
@@ -88,13 +84,13 @@ static int driver_multicast(int dev) {
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = dev;
-  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  ap.requestedHandleTypes = ht;
   CU(cuMemCreate(&ph, mp.size, &ap, 0));
   CU(cuMulticastBindMem(mh, 0, ph, 0, mp.size, 0));
   CUdeviceptr uc, mcp;
-  CU(cuMemAddressReserve(&uc, mp.size, gran, 0, 0));
+  CU(cuMemAddressReserve(&uc, mp.size, gmin, 0, 0));
   CU(cuMemMap(uc, mp.size, 0, ph, 0));
-  CU(cuMemAddressReserve(&mcp, mp.size, gran, 0, 0));
+  CU(cuMemAddressReserve(&mcp, mp.size, gmin, 0, 0));
   CU(cuMemMap(mcp, mp.size, 0, mh, 0));
   CUmemAccessDesc acc{};
   acc.location = ap.location;
@@ -111,9 +107,8 @@ static int driver_multicast(int dev) {
   RT(cudaMemcpy(o, (void*)uc, n * 4, cudaMemcpyDeviceToHost));
   size_t bad = 0;
   for (size_t i = 0; i < n; ++i) bad += o[i] != h[i] * 2.f;
-  printf("driver multicast 1 device: ld_reduce + st through the multicast VA: %s (%zu bad)\n",
-         bad ? "WRONG" : "ok", bad);
-  // time it: 4 MB read-reduce + 4 MB multicast store
+  printf("[%s] driver multicast 1 device: ld_reduce + st through the multicast VA: %s (%zu bad)\n",
+         hname, bad ? "WRONG" : "ok", bad);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -124,8 +119,23 @@ static int driver_multicast(int dev) {
   cudaEventSynchronize(e1);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  printf("multimem ld_reduce+st 4 MB: %.2f us per launch\n", ms * 1000 / 20);
+  printf("[%s] multimem ld_reduce+st 4 MB: %.2f us per launch\n", hname, ms * 1000 / 20);
   return 0;
+}
+
+static int driver_multicast(int dev) {
+  CUdevice d;
+  CU(cuDeviceGet(&d, dev));
+  int mc = 0;
+  CU(cuDeviceGetAttribute(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, d));
+  int fab = 0;
+  cuDeviceGetAttribute(&fab, CU_DEVICE_ATTRIBUTE_HANDLE_TYPE_FABRIC_SUPPORTED, d);
+  printf("multicast_supported=%d fabric_handles=%d\n", mc, fab);
+  if (!mc) return 0;
+  int rc = driver_multicast_try(dev, CU_MEM_HANDLE_TYPE_NONE, "none");
+  rc |= driver_multicast_try(dev, CU_MEM_HANDLE_TYPE_FABRIC, "fabric");
+  rc |= driver_multicast_try(dev, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, "posix_fd");
+  return rc;
 }
 
 static int nccl_devcomm(int dev) {
