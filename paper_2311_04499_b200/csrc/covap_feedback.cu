@@ -352,166 +352,116 @@ __global__ void __launch_bounds__(kThreads)
   pdl_release();
 }
 
-// Block-wide slot reservation in two lists: thread counts na, nb (< 2^16
-// per block); returns the thread's first slot in each.  One atomic per list.
-__device__ __forceinline__ void block_reserve(uint32_t na, uint32_t nb, uint32_t* ca,
-                                              uint32_t* cb, uint32_t& sa, uint32_t& sb) {
-  using Scan = cub::BlockScan<uint32_t, kThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ uint32_t s_base[2];
-  uint32_t pre = 0, tot = 0;
-  Scan(tmp).ExclusiveSum(na | (nb << 16), pre, tot);
-  if (threadIdx.x == 0) {
-    s_base[0] = (tot & 0xffffu) ? atomicAdd(ca, tot & 0xffffu) : 0u;
-    s_base[1] = (tot >> 16) ? atomicAdd(cb, tot >> 16) : 0u;
-  }
-  __syncthreads();
-  sa = s_base[0] + (pre & 0xffffu);
-  sb = s_base[1] + (pre >> 16);
-  __syncthreads();
-}
-
-// Per-warp staging of (index, payload) pairs appended by ballot, written to
-// a global list 32 at a time with one atomic per 32 entries: no block
-// barriers on the streaming path, and no contention on the list counters.
-template <typename V, uint32_t RING = 64>
-struct WarpStage {
-  uint32_t* idx;  // shared ring of RING entries
-  V* val;
-  uint32_t n = 0, done = 0;  // appended / written, warp-uniform
-
-  __device__ __forceinline__ void push(bool p, uint32_t i, V v) {
-    const unsigned m = __ballot_sync(0xffffffffu, p);
-    if (p) {
-      const uint32_t s = (n + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))) & (RING - 1);
-      idx[s] = i;
-      val[s] = v;
-    }
-    n += __popc(m);
-    __syncwarp();
-  }
-  __device__ __forceinline__ void put(uint32_t slot, uint32_t i, V v) {
-    idx[slot & (RING - 1)] = i;
-    val[slot & (RING - 1)] = v;
-  }
-  // Writes full groups of 32 (all = true: everything pending).
-  __device__ __forceinline__ void flush(uint32_t* counter, uint32_t* gidx, V* gval, uint64_t off,
-                                        bool all) {
-    const uint32_t lane = threadIdx.x & 31;
-    while (n - done >= 32 || (all && n > done)) {
-      const uint32_t c = n - done < 32 ? n - done : 32;
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(counter, c);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (lane < c) {
-        const uint32_t s = (done + lane) & (RING - 1);
-        gidx[off + base + lane] = idx[s];
-        gval[off + base + lane] = val[s];
-      }
-      done += c;
-      __syncwarp();
-    }
-  }
-};
-
 constexpr int kWarps = kThreads / 32;
-// collect: elements per lane per warp iteration.  Round 1: 1 KB of c per
-// warp (2 KB measured slower, register-limited occupancy); round 2, with the
-// per-vector max test and the bit-mask hit loop: 2 KB per warp is faster
-// (ResNet-50 / VGG-16 / BERT-large top-k step 0.1364 / 0.6535 / 1.4496 ms ->
-// 0.1340 / 0.6396 / 1.4145 ms, profiles/r2_f4.md)
-#ifndef COVAP_COLLECT_BYTES  // bytes of c per lane per warp iteration
-#define COVAP_COLLECT_BYTES 64
-#endif
 #ifndef COVAP_COLLECT_CTAS  // collect CTAs per SM
 #define COVAP_COLLECT_CTAS 4
 #endif
+
+// collect.  Per warp iteration (4 16-byte vectors per lane) a vector is a
+// hit when its largest key reaches the candidate bin (one compare per
+// vector: hits are ~1 % of elements); the warp then compacts its hit vectors into
+// a per-warp shared FIFO (one warp scan per iteration) and handles them 32 at
+// a time, one vector per lane: the per-hit work (classification, residual /
+// kept stores, list appends, the level-2 histogram) runs lane-parallel with
+// one list reservation per batch, instead of once per hit for the whole warp
+// (round 2: a per-lane shared-memory ring claimed hit by hit, ResNet-50 45 ->
+// 30 us, profiles/r2_f4.md).  Each CTA walks one contiguous run of chunks, so
+// the FIFO and the level-2 histogram are flushed only where the tensor
+// changes (round-robin chunks, or groups of 4 / 16, measured slower).
+// 32-bit flat indices (the state checks N < 2^32); body chunks are 16-byte
+// aligned (covap_feedback_create cuts every tensor's unaligned head and tail
+// into chunks of their own, flagged scalar).
+constexpr uint32_t kFifo = 160;  // hit vectors per warp: 31 pending + 4 x 32 new fit
+
 template <typename T>
-constexpr int kCollectUnroll = COVAP_COLLECT_BYTES / static_cast<int>(sizeof(T));
-
-// Per-warp ring fed lane by lane: a lane with a hit claims a slot with a
-// shared-memory atomic (hits are ~1% of elements, so the common path is one
-// compare per element and no warp-wide scan); the warp drains full groups of
-// 32 to the global list at the end of each iteration.  A claim that finds the
-// ring full (only when most elements are hits) goes straight to the global
-// list with its own atomic.  List order is irrelevant downstream.
-template <typename V, uint32_t RING>
-struct LaneRing {
-  uint32_t* idx;       // shared, RING entries
-  V* val;
-  uint32_t* n;         // shared claim counter of this warp
-  uint32_t done = 0;   // drained (warp-uniform)
-
-  __device__ __forceinline__ void claim(uint32_t i, V v, uint32_t* gcnt, uint32_t* gidx, V* gval,
-                                        uint64_t off) {
-    const uint32_t slot = atomicAdd(n, 1u);
-    if (slot - done < RING) {
-      idx[slot & (RING - 1)] = i;
-      val[slot & (RING - 1)] = v;
-    } else {
-      const uint32_t g = atomicAdd(gcnt, 1u);
-      gidx[off + g] = i;
-      gval[off + g] = v;
-    }
-  }
-  // Warp-collective: drain groups of 32 (all: everything pending).
-  __device__ __forceinline__ void drain(uint32_t* gcnt, uint32_t* gidx, V* gval, uint64_t off,
-                                        bool all) {
-    const uint32_t lane = threadIdx.x & 31;
-    __syncwarp();
-    uint32_t m = *n;
-    if (m - done > RING) {  // overflowed claims were written directly
-      m = done + RING;
-      __syncwarp();
-      if (lane == 0) *n = m;
-    }
-    while (m - done >= 32 || (all && m > done)) {
-      const uint32_t c = m - done < 32 ? m - done : 32;
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(gcnt, c);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (lane < c) {
-        const uint32_t s = (done + lane) & (RING - 1);
-        gidx[off + base + lane] = idx[s];
-        gval[off + base + lane] = val[s];
-      }
-      done += c;
-    }
-    __syncwarp();
-  }
-};
-
-#ifndef COVAP_COLLECT_MASK  // collect: a vector's hits via a bit-mask loop (1) or unrolled (0)
-#define COVAP_COLLECT_MASK 1
-#endif
-#ifndef COVAP_COLLECT_DRAIN  // collect: warp iterations between ring drains
-#define COVAP_COLLECT_DRAIN 1
-#endif
-template <typename T>
-__global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
+__global__ void __launch_bounds__(kThreads, COVAP_COLLECT_CTAS) topk_collect_kernel(TopkArgs A) {
   pdl_begin();
   using K = typename KeyOf<T>::K;
-  constexpr int kU = kCollectUnroll<T>;
-  constexpr uint32_t kRing = 128;
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  constexpr int W = 16 / static_cast<int>(sizeof(T));
+  constexpr int kV = 4;  // vectors per lane per iteration
   __shared__ uint32_t hist2[kDigits];
-  __shared__ uint32_t s_ti[kWarps][kRing], s_ci[kWarps][kRing];
-  __shared__ T s_tv[kWarps][kRing];
-  __shared__ K s_ck[kWarps][kRing];
-  __shared__ uint32_t s_n[kWarps][2];
+  __shared__ V s_v[kWarps][kFifo];
+  __shared__ uint32_t s_e[kWarps][kFifo];
   T* __restrict__ r = static_cast<T*>(A.r);
   T* __restrict__ kept = static_cast<T*>(A.kept);
   T* __restrict__ list_val = static_cast<T*>(A.list_val);
   K* __restrict__ cand_key = static_cast<K*>(A.cand_key);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  LaneRing<T, kRing> take{s_ti[warp], s_tv[warp], &s_n[warp][0]};
-  LaneRing<K, kRing> cand{s_ci[warp], s_ck[warp], &s_n[warp][1]};
+  V* const fv = s_v[warp];
+  uint32_t* const fe = s_e[warp];
   for (int b = threadIdx.x; b < kDigits; b += kThreads) hist2[b] = 0;
-  if (lane < 2) s_n[warp][lane] = 0;
   __syncthreads();
-  uint32_t cur = kNone;
-  auto flush_hist = [&]() {
+  // the current tensor's parameters: bin > b1 taken (key >= k_take), bin ==
+  // b1 candidate (key >= k_cand); list / candidate offsets
+  uint32_t t = kNone;
+  K k_cand = 0, k_take = 0;
+  uint64_t lo = 0, cb = 0;
+  // Lane-parallel hit handling: this lane's nw elements x[0..nw) at flat
+  // indices e0 + w (nw = 0: idle lane); one reservation per list per call.
+  auto handle = [&](const T* x, uint32_t e0, int nw) {
+    uint32_t nt = 0, nc = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      if (w < nw) {
+        const K key = KeyOf<T>::key(x[w]);
+        nt += key >= k_take;
+        nc += key >= k_cand && key < k_take;
+      }
+    }
+    uint32_t pre = nt | (nc << 16);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+    pre -= nt | (nc << 16);  // exclusive
+    uint32_t bt = 0, bc = 0;
+    if (lane == 0) {
+      if (tot & 0xffffu) bt = atomicAdd(A.sel_cnt + t, tot & 0xffffu);
+      if (tot >> 16) bc = atomicAdd(A.cand_cnt + t, tot >> 16);
+    }
+    uint32_t st = __shfl_sync(0xffffffffu, bt, 0) + (pre & 0xffffu);
+    uint32_t sc = __shfl_sync(0xffffffffu, bc, 0) + (pre >> 16);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      if (w < nw) {
+        const K key = KeyOf<T>::key(x[w]);
+        const uint32_t i = e0 + w;
+        if (key >= k_take) {
+          if (kept) kept[i] = kept_value(x[w], A.kept_mean);
+          r[i] = sub_rn(x[w], x[w]);
+          A.list_idx[lo + st] = i;
+          list_val[lo + st] = x[w];
+          ++st;
+        } else if (key >= k_cand) {
+          A.cand_idx[cb + sc] = i;
+          cand_key[cb + sc] = key;
+          atomicAdd(&hist2[digit2_of<T>(key)], 1u);
+          ++sc;
+        }
+      }
+    }
+  };
+  uint32_t head = 0, pend = 0;  // FIFO [head, head + pend) mod kFifo, warp-uniform
+  auto pop32 = [&](uint32_t m) {  // handle min(m, 32) queued vectors
+    uint32_t q = head + lane;
+    if (q >= kFifo) q -= kFifo;
+    const bool act = static_cast<uint32_t>(lane) < m;
+    const V v = act ? fv[q] : V{};
+    const uint32_t e0 = act ? fe[q] : 0u;
+    handle(reinterpret_cast<const T*>(&v), e0, act ? W : 0);
+    const uint32_t n = m < 32 ? m : 32;
+    head += n;
+    if (head >= kFifo) head -= kFifo;
+    pend -= n;
+    __syncwarp();
+  };
+  auto end_tensor = [&]() {  // the FIFO's last entries, then the histogram
+    if (pend) pop32(pend);
     __syncthreads();
-    uint32_t* dst = A.hist2 + static_cast<uint64_t>(cur) * kDigits;
+    uint32_t* dst = A.hist2 + static_cast<uint64_t>(t) * kDigits;
     for (int b = threadIdx.x; b < kDigits; b += kThreads) {
       const uint32_t v = hist2[b];
       if (v) {
@@ -521,100 +471,73 @@ __global__ void __launch_bounds__(kThreads) topk_collect_kernel(TopkArgs A) {
     }
     __syncthreads();
   };
-  constexpr uint32_t kSpan = 32 * kU;  // elements per warp iteration
-  for (uint32_t ci = blockIdx.x; ci < A.nchunks; ci += gridDim.x) {
+  const uint32_t per = (A.nchunks + gridDim.x - 1) / gridDim.x;
+  const uint32_t c_lo = min(A.nchunks, blockIdx.x * per), c_hi = min(A.nchunks, c_lo + per);
+  constexpr uint32_t kSpan = 32 * kV * W;  // elements per warp iteration
+  for (uint32_t ci = c_lo; ci < c_hi; ++ci) {
     const Chunk ch = A.chunks[ci];
-    const uint32_t t = ch.tensor;
-    if (t != cur) {
-      if (cur != kNone) flush_hist();
-      cur = t;
+    if (ch.tensor != t) {
+      if (t != kNone) end_tensor();
+      t = ch.tensor;
+      const uint32_t b1 = A.thr[t];
+      k_cand = static_cast<K>(b1) << (KeyOf<T>::kBits - kBinBits);
+      k_take = static_cast<K>(b1 + 1) << (KeyOf<T>::kBits - kBinBits);
+      lo = A.list_off[t];
+      cb = A.t_begin[t];
     }
-    // bin > b1: taken (key >= k_take); bin == b1: candidate (key >= k_cand)
-    const uint32_t b1 = A.thr[t];
-    const K k_cand = static_cast<K>(b1) << (KeyOf<T>::kBits - kBinBits);
-    const K k_take = static_cast<K>(b1 + 1) << (KeyOf<T>::kBits - kBinBits);
-    const uint64_t lo = A.list_off[t], cb = A.t_begin[t];
-    uint32_t* sel_cnt = A.sel_cnt + t;
-    uint32_t* cand_cnt = A.cand_cnt + t;
-    auto hit = [&](uint32_t i, T c) {  // key >= k_cand
-      const K key = KeyOf<T>::key(c);
-      if (key >= k_take) {
-        take.claim(i, c, sel_cnt, A.list_idx, list_val, lo);
-        if (kept) kept[i] = kept_value(c, A.kept_mean);
-        r[i] = sub_rn(c, c);
-      } else {
-        cand.claim(i, key, cand_cnt, A.cand_idx, cand_key, cb);
-        atomicAdd(&hist2[digit2_of<T>(key)], 1u);
-      }
-    };
-    // 32-bit flat indices (the state checks N < 2^32).  Body chunks are
-    // 16-byte aligned (covap_feedback_create cuts every tensor's unaligned
-    // head and tail into chunks of their own, flagged scalar), so a lane loads
-    // kU / W vectors: element q of the lane is vector (q / W), lane (q % W).
-    constexpr int W = 16 / static_cast<int>(sizeof(T));
     const uint32_t cbeg = static_cast<uint32_t>(ch.begin), cend = static_cast<uint32_t>(ch.end);
     if (ch.pad == 0) {
-      using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
       for (uint32_t base = cbeg + warp * kSpan; base < cend; base += kWarps * kSpan) {
-        V x[kU / W];
+        V x[kV];
 #pragma unroll
-        for (int j = 0; j < kU / W; ++j) {
+        for (int j = 0; j < kV; ++j) {
           const uint32_t e0 = base + (j * 32 + lane) * W;
           x[j] = e0 < cend ? *reinterpret_cast<const V*>(r + e0) : V{};
         }
+        uint32_t vm = 0;  // this lane's hit vectors
 #pragma unroll
-        for (int j = 0; j < kU / W; ++j) {
-          const uint32_t e0 = base + (j * 32 + lane) * W;
+        for (int j = 0; j < kV; ++j) {
           const T* xs = reinterpret_cast<const T*>(&x[j]);
-          // one test per 16-byte vector on its largest key: hits are ~1 % of
-          // elements, so almost every vector is rejected with one compare
           K m = KeyOf<T>::key(xs[0]);
 #pragma unroll
           for (int w = 1; w < W; ++w) m = max(m, KeyOf<T>::key(xs[w]));
-          if (m >= k_cand && e0 < cend) {
-#if COVAP_COLLECT_MASK
-            // the vector's hits as a bit mask, handled in one loop: the hit
-            // path is inlined once and runs as often as the busiest lane needs
-            uint32_t hm = 0;
+          if (m >= k_cand && base + (j * 32 + lane) * W < cend) vm |= 1u << j;
+        }
+        const uint32_t cnt = __popc(vm);
+        uint32_t pre = cnt;
 #pragma unroll
-            for (int w = 0; w < W; ++w) hm |= (KeyOf<T>::key(xs[w]) >= k_cand ? 1u : 0u) << w;
-            while (hm) {
-              const int w = __ffs(hm) - 1;
-              hm &= hm - 1;
-              T v = xs[0];
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+          if (lane >= o) pre += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+        if (tot == 0) continue;
+        uint32_t q = head + pend + pre - cnt;  // pend <= 31, tot <= 128: q < 2 kFifo
 #pragma unroll
-              for (int q = 1; q < W; ++q) v = w == q ? xs[q] : v;
-              hit(e0 + w, v);
-            }
-#else
-#pragma unroll
-            for (int w = 0; w < W; ++w)
-              if (KeyOf<T>::key(xs[w]) >= k_cand) hit(e0 + w, xs[w]);
-#endif
+        for (int j = 0; j < kV; ++j) {
+          if (vm >> j & 1u) {
+            const uint32_t sl = q >= kFifo ? q - kFifo : q;
+            fv[sl] = x[j];
+            fe[sl] = base + (j * 32 + lane) * W;
+            ++q;
           }
         }
-        // drain the rings every COVAP_COLLECT_DRAIN iterations (overfull
-        // claims go straight to the global list, so any period is safe)
-        if (((base - cbeg) / (kWarps * kSpan)) % COVAP_COLLECT_DRAIN == COVAP_COLLECT_DRAIN - 1) {
-          take.drain(sel_cnt, A.list_idx, list_val, lo, false);
-          cand.drain(cand_cnt, A.cand_idx, cand_key, cb, false);
-        }
+        pend += tot;
+        __syncwarp();
+        while (pend >= 32) pop32(32);
       }
     } else {  // scalar chunk: one element per lane
       for (uint32_t base = cbeg + warp * 32; base < cend; base += kWarps * 32) {
         const uint32_t e = base + lane;
-        if (e < cend) {
-          const T c = r[e];
-          if (KeyOf<T>::key(c) >= k_cand) hit(e, c);
-        }
-        take.drain(sel_cnt, A.list_idx, list_val, lo, false);
-        cand.drain(cand_cnt, A.cand_idx, cand_key, cb, false);
+        T c = T(0);
+        if (e < cend) c = r[e];
+        handle(&c, e, e < cend ? 1 : 0);
       }
     }
-    take.drain(sel_cnt, A.list_idx, list_val, lo, true);
-    cand.drain(cand_cnt, A.cand_idx, cand_key, cb, true);
   }
-  if (cur != kNone) flush_hist();
+  // every CTA takes part in the barriers of end_tensor (chunk runs are per
+  // CTA, so all its warps see the same tensors)
+  if (t != kNone) end_tensor();
   pdl_release();
 }
 
