@@ -54,9 +54,10 @@ cudaError_t launch_dense(int dtype, int kind, const DenseArgs& a, int sms, cudaS
 
 // Compensation pass of the sparsifiers: r = c; zero[i] = 0 when zero is not
 // NULL; with hist, the per-tensor histogram of the top kBinBits of |c|.
+// vec: 16-byte vector loop over the body chunks (small layouts).
 cudaError_t launch_compensate(int dtype, const void* g, void* r, void* zero, uint32_t* hist,
                               const Chunk* chunks, uint32_t nchunks, int ef, double coeff,
-                              int sms, cudaStream_t s, bool pdl = false);
+                              int sms, cudaStream_t s, bool pdl = false, bool vec = false);
 
 // Top-k after the compensation pass filled hist1: the k[t] largest |c| of
 // every tensor (ties to the lower index) go to list_idx / list_val at

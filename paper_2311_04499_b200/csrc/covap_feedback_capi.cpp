@@ -223,9 +223,11 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       break;
     }
     case COVAP_FILTER_TOPK: {
+      // small layouts: programmatic dependent launch along the chain and the
+      // 16-byte vector compensation loop (both measured, profiles/r2_f4.md)
       const bool pdl = f->total < fb::kTopkPdlMaxElems;
       CK(fb::launch_compensate(dt, grad, f->residual, zero, f->hist, f->chunks, f->nchunks,
-                               f->ef.enabled, coeff, f->sms, st, pdl));
+                               f->ef.enabled, coeff, f->sms, st, pdl, pdl));
       fb::TopkArgs a{};
       a.pdl = pdl ? 1 : 0;
       a.r = f->residual;
