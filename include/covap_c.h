@@ -363,6 +363,21 @@ void covap_peer_destroy(covap_peer* peer);
 covap_status covap_peer_export(covap_peer* peer, uint8_t* blob, size_t cap, size_t* len);
 covap_status covap_peer_import(covap_peer* peer, const uint8_t* blobs, size_t len);
 covap_status covap_peer_attach_local(covap_peer** peers, int nranks);
+/* The same collective with its buffers and flag block in one NCCL symmetric
+ * window on `comm` (NCCL 2.28 device API: ncclMemAlloc +
+ * ncclCommWindowRegister, peer addresses from the window) instead of CUDA
+ * IPC: collective over comm's ranks, attached on return, rank = comm's rank.
+ * multimem != 0 also binds the window to an NVSwitch multicast object
+ * (ncclDevCommCreate with lsaMultimem) and the reduction of modes 0 / 1 runs
+ * in the switch: multimem.ld_reduce of slice r, multimem.st of its sum to
+ * every rank — the summation order is then the switch's, not the rank order
+ * (|d| <= 1e-6 sum_w |x_w|, as for NCCL at P > 2); fails when the
+ * communicator has no multicast (one GPU, or ranks off one NVLink domain).
+ * The peer must be destroyed before comm, or it keeps only its memory. */
+covap_status covap_peer_create_nccl(covap_state* state, covap_comm* comm, int multimem,
+                                    covap_peer** out);
+/* *on = 1 when the peer reduces through NVSwitch multicast. */
+covap_status covap_peer_multimem(const covap_peer* peer, int* on);
 /* max_ctas: cap the collective's grid (0 = one CTA per SM); timeout_s: bound
  * of every spin-wait (0 = keep). */
 covap_status covap_peer_set_limits(covap_peer* peer, int max_ctas, double timeout_s);

@@ -861,12 +861,34 @@ class PeerGroup:
     calls ``export()``, the blobs are gathered (torch.distributed), every
     rank calls ``import_(blobs)``; ranks of one process use ``attach_local``."""
 
-    def __init__(self, state: CompressorState, nranks: int, rank: int):
-        h = ctypes.c_void_p()
-        L.lib().covap_peer_create(state.handle, int(nranks), int(rank), ctypes.byref(h))
+    def __init__(self, state: CompressorState, nranks: int, rank: int, _handle=None):
+        h = _handle
+        if h is None:
+            h = ctypes.c_void_p()
+            L.lib().covap_peer_create(state.handle, int(nranks), int(rank), ctypes.byref(h))
         self._h = h
         self.state = state
         self.nranks, self.rank = int(nranks), int(rank)
+
+    @staticmethod
+    def from_nccl(state: CompressorState, comm: "Communicator", multimem: bool = False) -> "PeerGroup":
+        """The buffers in an NCCL symmetric window on ``comm`` (no CUDA IPC
+        rendezvous; collective over comm's ranks).  ``multimem``: reduce in
+        the NVSwitch (multimem.ld_reduce / multimem.st) — switch summation
+        order, the NCCL tolerance; raises where the communicator has no
+        multicast.  Destroy the group before the communicator."""
+        h = ctypes.c_void_p()
+        L.lib().covap_peer_create_nccl(state.handle, comm.handle, int(bool(multimem)),
+                                       ctypes.byref(h))
+        g = PeerGroup(state, comm.nranks, comm.rank, _handle=h)
+        g._comm = comm  # keep the communicator alive as long as the group
+        return g
+
+    @property
+    def multimem(self) -> bool:
+        on = ctypes.c_int32()
+        L.lib().covap_peer_multimem(self._h, ctypes.byref(on))
+        return bool(on.value)
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -1071,6 +1071,8 @@ void covap_comm_destroy(covap_comm* c) {
     cudaDeviceSynchronize();
     for (ncclWindow_t w : c->windows) ncclCommWindowDeregister(c->nccl, w);
     c->windows.clear();
+    for (covapb::NcclPeerMem* m : c->peer_mems) covapb::nccl_peer_mem_release(c->nccl, m);
+    c->peer_mems.clear();
     if (prev >= 0) cudaSetDevice(prev);
   }
   if (c->nccl) ncclCommDestroy(c->nccl);
@@ -1290,6 +1292,12 @@ struct covap_peer {
   // and launch j + 2 is packed only after this rank passed launch j + 1's
   // arrival barrier, which every peer reaches only after finishing launch j.
   uint64_t launches = 0;
+  // NCCL transport (covap_peer_create_nccl): the buffers and flag block live
+  // in one NCCL symmetric window; mc[k] = buffer k's NVSwitch multicast
+  // address when multimem was requested (NULL otherwise).
+  covapb::NcclPeerMem* nmem = nullptr;
+  covap_comm* ncomm = nullptr;
+  void* mc[2] = {nullptr, nullptr};
 };
 
 extern "C" {
@@ -1329,6 +1337,70 @@ covap_status covap_peer_create(covap_state* s, int nranks, int rank, covap_peer*
   return st;
 }
 
+covap_status covap_peer_create_nccl(covap_state* s, covap_comm* c, int multimem,
+                                    covap_peer** out) {
+  covap_peer* p = nullptr;
+  const covap_status st = guarded([&] {
+    need(s && c && out, "NULL argument");
+    need(c->device == s->device, "communicator and state are on different devices");
+    need(c->nranks >= 1 && c->nranks <= covapb::kMaxPeers, "peer collective supports 1..8 ranks");
+    DeviceGuard dg(s->device);
+    p = new covap_peer;
+    p->device = s->device;
+    p->P = c->nranks;
+    p->rank = c->rank;
+    p->esize = s->esize;
+    p->cap = s->send_cap + 64;  // room for the last vector
+    p->cmax = (p->cap + covapb::kPeerChunk - 1) / covapb::kPeerChunk;
+    // one window: [buffer 0 | buffer 1 | flag block], 4 KB-aligned parts
+    const size_t a = 4096;
+    const size_t bb = (p->cap * p->esize + a - 1) / a * a;
+    const size_t fbytes = covapb::peer_flag_words(p->cmax) * sizeof(uint64_t);
+    const size_t bytes = (2 * bb + fbytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) /
+                         NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    void* peers[covapb::kMaxPeers] = {};
+    void* mc = nullptr;
+    const char* what = "";
+    if (covapb::nccl_peer_mem_create(c->nccl, p->P, bytes, multimem, &p->nmem, peers, &mc, &what))
+      throw covap::Error(std::string("NCCL peer window: ") + what);
+    p->ncomm = c;
+    {
+      std::lock_guard<std::mutex> lock(g_comms_mu);
+      c->peer_mems.push_back(p->nmem);
+    }
+    for (int q = 0; q < p->P; ++q) {
+      char* b = static_cast<char*>(peers[q]);
+      p->peer_bufs[0][q] = b;
+      p->peer_bufs[1][q] = b + bb;
+      p->peer_flags[q] = reinterpret_cast<uint64_t*>(b + 2 * bb);
+    }
+    p->bufs[0] = p->peer_bufs[0][p->rank];
+    p->bufs[1] = p->peer_bufs[1][p->rank];
+    p->flags = p->peer_flags[p->rank];
+    if (mc) {
+      p->mc[0] = mc;
+      p->mc[1] = static_cast<char*>(mc) + bb;
+    }
+    CK(cudaMalloc(reinterpret_cast<void**>(&p->counter), sizeof(unsigned)));
+    CK(cudaMemset(p->counter, 0, sizeof(unsigned)));
+    CK(cudaMalloc(reinterpret_cast<void**>(&p->queue), 2 * sizeof(unsigned)));
+    CK(cudaMemset(p->queue, 0, 2 * sizeof(unsigned)));
+    CK(cudaMalloc(reinterpret_cast<void**>(&p->err), sizeof(int)));
+    CK(cudaMemset(p->err, 0, sizeof(int)));
+    p->attached = true;
+    *out = p;
+  });
+  if (st != COVAP_OK && p) covap_peer_destroy(p);
+  return st;
+}
+
+covap_status covap_peer_multimem(const covap_peer* p, int* on) {
+  return guarded([&] {
+    need(p && on, "NULL argument");
+    *on = p->mc[0] != nullptr;
+  });
+}
+
 void covap_peer_destroy(covap_peer* p) {
   if (!p) return;
   int prev = -1;
@@ -1336,9 +1408,20 @@ void covap_peer_destroy(covap_peer* p) {
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
   for (void* q : p->opened) cudaIpcCloseMemHandle(q);
-  cudaFree(p->bufs[0]);
-  cudaFree(p->bufs[1]);
-  cudaFree(p->flags);
+  if (p->nmem) {  // NCCL window: released here unless its communicator went first
+    std::lock_guard<std::mutex> lock(g_comms_mu);
+    ncclComm_t live = nullptr;
+    if (g_live_comms.count(p->ncomm)) {
+      live = p->ncomm->nccl;
+      auto& v = p->ncomm->peer_mems;
+      v.erase(std::remove(v.begin(), v.end(), p->nmem), v.end());
+    }
+    covapb::nccl_peer_mem_destroy(live, p->nmem);
+  } else {
+    cudaFree(p->bufs[0]);
+    cudaFree(p->bufs[1]);
+    cudaFree(p->flags);
+  }
   cudaFree(p->queue);
   cudaFree(p->counter);
   cudaFree(p->err);
@@ -1349,6 +1432,7 @@ void covap_peer_destroy(covap_peer* p) {
 covap_status covap_peer_export(covap_peer* p, uint8_t* blob, size_t cap, size_t* len) {
   return guarded([&] {
     need(p && len, "NULL argument");
+    need(!p->nmem, "an NCCL-window peer is attached at creation (nothing to export)");
     constexpr size_t h = sizeof(cudaIpcMemHandle_t);
     *len = 3 * h;
     if (!blob) return;
@@ -1367,6 +1451,7 @@ covap_status covap_peer_import(covap_peer* p, const uint8_t* blobs, size_t len) 
     need(p && blobs, "NULL argument");
     constexpr size_t h = sizeof(cudaIpcMemHandle_t);
     need(len == 3 * h, "blob length mismatch");
+    need(!p->nmem, "an NCCL-window peer is attached at creation (nothing to import)");
     DeviceGuard dg(p->device);
     for (int q = 0; q < p->P; ++q) {
       if (q == p->rank) continue;
@@ -1390,6 +1475,7 @@ covap_status covap_peer_attach_local(covap_peer** peers, int nranks) {
     need(peers != nullptr && nranks >= 1 && nranks <= covapb::kMaxPeers, "bad peer list");
     for (int i = 0; i < nranks; ++i) {
       need(peers[i] && peers[i]->P == nranks && peers[i]->rank == i, "peer i must be rank i");
+      need(!peers[i]->nmem, "an NCCL-window peer is attached at creation");
     }
     for (int i = 0; i < nranks; ++i) {
       for (int q = 0; q < nranks; ++q) {
@@ -1443,6 +1529,7 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
     const int par = static_cast<int>(p->launches & 1);
     void* buf = p->bufs[par];
     if (p->mode == 2) {  // K1 + collective + unpack in one kernel
+      need(!p->mc[0], "the whole-step kernel (mode 2) has no multimem variant: use mode 0 or 1");
       covapb::PeerStepArgs a{};
       for (int q = 0; q < p->P; ++q) {
         a.bufs[q] = p->peer_bufs[par][q];
@@ -1496,6 +1583,7 @@ covap_status covap_peer_sync_step(covap_state* s, covap_peer* p, const void* gra
       a.n_out = n;
       a.inv = 1.0 / static_cast<double>(p->P);
       a.zfill = 0;  // K1 zeroed the unselected output
+      a.mc = p->mc[par];
       CK(covapb::launch_peer_allreduce(s->dtype, a, p->max_ctas, st));
       ++p->launches;
     }

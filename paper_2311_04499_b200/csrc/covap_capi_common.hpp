@@ -15,6 +15,10 @@
 #include "covap/errors.hpp"
 #include "covap_c.h"
 
+namespace covapb {
+struct NcclPeerMem;
+}
+
 struct covap_comm {
   ncclComm_t nccl = nullptr;
   int nranks = 1;
@@ -23,6 +27,9 @@ struct covap_comm {
   // NCCL windows registered on this communicator (symmetric send buffers,
   // covap_state_use_symmetric): deregistered at the latest when it is destroyed
   std::vector<ncclWindow_t> windows;
+  // peer-collective memory on this communicator (covap_peer_create_nccl):
+  // its window / device communicator released at the latest then
+  std::vector<covapb::NcclPeerMem*> peer_mems;
 };
 
 namespace covapb {

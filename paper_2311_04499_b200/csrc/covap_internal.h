@@ -107,8 +107,29 @@ struct PeerArgs {
   uint64_t n_out;   // device elements of out
   double inv;
   int zfill;        // fused: zero the unselected slots too (0: K1 already did)
+  // NVLS: the multicast address of this launch's send buffers (NULL: none).
+  // Phase 1 then reduces slice r in the switch (multimem.ld_reduce) and
+  // stores the sum to every rank's buffer (multimem.st); phase 2 reads only
+  // the local buffer.  The switch's summation order is not the rank order:
+  // the |d| <= 1e-6 sum|x_w| tolerance applies, as for NCCL at P > 2.
+  void* mc;
 };
 cudaError_t launch_peer_allreduce(int dtype, const PeerArgs& args, int max_ctas, cudaStream_t s);
+
+// Peer memory from NCCL instead of CUDA IPC: `bytes` of ncclMemAlloc memory
+// registered as a symmetric window on comm (collective over its ranks), every
+// rank's address of it (the window's load/store-accessible peer pointers)
+// and, with want_multimem, its multicast address through an NCCL device
+// communicator with multimem on the NVLink team.  0 on success; else a
+// description in *what.
+struct NcclPeerMem;
+int nccl_peer_mem_create(struct ncclComm* comm, int nranks, size_t bytes, int want_multimem,
+                         NcclPeerMem** out, void** peers, void** mc, const char** what);
+// Deregisters (comm != NULL: still alive) and frees.
+void nccl_peer_mem_destroy(struct ncclComm* comm, NcclPeerMem* m);
+// The window / device communicator only (comm going away first); the
+// memory stays until nccl_peer_mem_destroy(NULL, m).
+void nccl_peer_mem_release(struct ncclComm* comm, NcclPeerMem* m);
 
 // The whole multi-rank step as ONE kernel per rank over peer memory
 // (covap_peer.cu, peer_step_kernel): K1 packs the selected shards chunk by

@@ -27,6 +27,9 @@
 
 #include <algorithm>
 
+#include <nccl.h>
+#include <nccl_device.h>
+
 #include "covap_internal.h"
 
 namespace covapb {
@@ -90,6 +93,61 @@ __device__ __forceinline__ double2 vzero<double2>() {
   return make_double2(0.0, 0.0);
 }
 
+// NVLS: loads through a multicast address reduce the P ranks' copies in the
+// NVSwitch; stores through it write every rank's copy.  The same memory is
+// also accessed through its unicast address (K1's packing, the unpack), so a
+// proxy fence orders the two views around the flag exchanges.
+__device__ __forceinline__ void fence_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+__device__ __forceinline__ float4 mm_ld_add(const float4* p) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ double2 mm_ld_add(const double2* p) {
+  double2 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];"
+               : "=d"(v.x)
+               : "l"(reinterpret_cast<const double*>(p))
+               : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];"
+               : "=d"(v.y)
+               : "l"(reinterpret_cast<const double*>(p) + 1)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float mm_ld_add(const float* p) {
+  float v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double mm_ld_add(const double* p) {
+  double v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mm_st(float4* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st(double2* p, double2 v) {
+  asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(reinterpret_cast<double*>(p)),
+               "d"(v.x)
+               : "memory");
+  asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(reinterpret_cast<double*>(p) + 1),
+               "d"(v.y)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st(float* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void mm_st(double* p, double v) {
+  asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 // Wait until flags[slot * 8 + q] >= epoch for every q < P (bounded).
 __device__ __forceinline__ bool wait_all(const uint64_t* flags, int slot, int P, uint64_t epoch,
                                          uint64_t timeout_ns, int* err) {
@@ -135,6 +193,25 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
   // kAllB vectors per thread per round, so each rank's loads of a round are
   // in flight together (the loop is latency-bound otherwise)
   constexpr int kAllB = 4;
+  if (args.mc) {  // NVLS: the switch sums slice r and stores it to every rank
+    fence_alias();
+    V* const mcv = static_cast<V*>(args.mc);
+    for (uint64_t v0 = v_lo + blockIdx.x * kPeerThreads + threadIdx.x; v0 < v_hi;
+         v0 += kAllB * stride) {
+      V x[kAllB];
+#pragma unroll
+      for (int b = 0; b < kAllB; ++b)
+        if (v0 + b * stride < v_hi) x[b] = mm_ld_add(mcv + v0 + b * stride);
+#pragma unroll
+      for (int b = 0; b < kAllB; ++b)
+        if (v0 + b * stride < v_hi) mm_st(mcv + v0 + b * stride, x[b]);
+    }
+    if (r == P - 1 && blockIdx.x == 0)
+      for (uint64_t e = nvec * W + threadIdx.x; e < L; e += kPeerThreads) {
+        T* const mce = static_cast<T*>(args.mc);
+        mm_st(mce + e, mm_ld_add(mce + e));
+      }
+  } else {
   for (uint64_t v0 = v_lo + blockIdx.x * kPeerThreads + threadIdx.x; v0 < v_hi;
        v0 += kAllB * stride) {
     V acc[kAllB];
@@ -164,6 +241,7 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
       for (int p = 0; p < P; ++p) acc = add_rn(acc, bufs[p][e]);
       bufs[r][e] = acc;
     }
+  }
 
   // ---- grid barrier, then phase-1 flag exchange ------------------------
   __syncthreads();
@@ -179,6 +257,7 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
   }
   __syncthreads();
   if (!ok) return;
+  if (args.mc) fence_alias();  // the switch's stores, read through the unicast view
 
   // ---- phase 2 (fused): unpack straight from the slice owners -----------
   if (args.fused) {
@@ -188,6 +267,7 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
     // the owner of send element o: its vector's slice; the scalar tail is
     // the last rank's (phase 1)
     auto owner = [&](uint64_t o) -> int {
+      if (args.mc) return r;  // every rank holds every reduced slice
       const uint64_t v = o / W;
       return v >= nvec ? P - 1 : static_cast<int>(v / per);
     };
@@ -243,6 +323,7 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(const Peer
   }
 
   // ---- phase 2: gather the other ranks' reduced slices -----------------
+  if (args.mc) return;  // the switch already stored them here
   for (int q = 1; q < P; ++q) {
     const int src = (r + q) % P;  // stagger the peers each rank reads first
     const uint64_t lo = umin(nvec, per * src), hi = umin(nvec, per * (src + 1));
@@ -565,6 +646,85 @@ cudaError_t launch_peer_step(int dtype, const PeerStepArgs& args, int max_ctas, 
   else
     peer_step_kernel<double><<<grid, kStepThreads, 0, s>>>(args);
   return cudaGetLastError();
+}
+
+
+
+// ------------------------------------------------------- NCCL peer memory
+//
+// The peer collective's buffers as an NCCL symmetric window (NCCL 2.28's
+// device API): NCCL maps every rank's allocation into every peer over NVLink
+// (and, with multimem, binds them to one NVSwitch multicast object), so the
+// kernels above get their peer / multicast addresses without CUDA IPC.
+
+struct NcclPeerMem {
+  void* base = nullptr;
+  ncclWindow_t win = nullptr;
+  ncclDevComm dc{};
+  bool has_dc = false;
+};
+
+namespace {
+__global__ void nccl_peer_ptrs_kernel(ncclWindow_t w, ncclDevComm dc, int has_dc, int P,
+                                      void** out) {
+  if (threadIdx.x != 0) return;
+  for (int p = 0; p < P; ++p) out[p] = ncclGetPeerPointer(w, 0, p);
+  out[P] = has_dc && dc.lsaMultimem.mcBasePtr ? ncclGetLsaMultimemPointer(w, 0, dc) : nullptr;
+}
+}  // namespace
+
+void nccl_peer_mem_release(ncclComm* comm, NcclPeerMem* m) {
+  if (!m || !comm) return;
+  if (m->has_dc) ncclDevCommDestroy(comm, &m->dc);
+  if (m->win) ncclCommWindowDeregister(comm, m->win);
+  m->has_dc = false;
+  m->win = nullptr;
+}
+
+void nccl_peer_mem_destroy(ncclComm* comm, NcclPeerMem* m) {
+  if (!m) return;
+  nccl_peer_mem_release(comm, m);
+  if (m->base) ncclMemFree(m->base);
+  delete m;
+}
+
+int nccl_peer_mem_create(ncclComm* comm, int nranks, size_t bytes, int want_multimem,
+                         NcclPeerMem** out, void** peers, void** mc, const char** what) {
+  NcclPeerMem* m = new NcclPeerMem;
+  auto fail = [&](const char* msg) {
+    *what = msg;
+    nccl_peer_mem_destroy(comm, m);
+    return 1;
+  };
+  if (ncclMemAlloc(&m->base, bytes) != ncclSuccess) return fail("ncclMemAlloc");
+  if (cudaMemset(m->base, 0, bytes) != cudaSuccess) return fail("cudaMemset(peer window)");
+  if (ncclCommWindowRegister(comm, m->base, bytes, &m->win, NCCL_WIN_COLL_SYMMETRIC) !=
+      ncclSuccess)
+    return fail("ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC)");
+  if (want_multimem) {
+    ncclDevCommRequirements req{};
+    req.lsaMultimem = true;
+    if (ncclDevCommCreate(comm, &req, &m->dc) != ncclSuccess)
+      return fail("ncclDevCommCreate(lsaMultimem): no NVSwitch multicast for this communicator");
+    m->has_dc = true;
+    if (m->dc.lsaSize != nranks) return fail("multimem needs every rank in one NVLink domain");
+  }
+  void** d_out = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&d_out), (kMaxPeers + 1) * sizeof(void*)) != cudaSuccess)
+    return fail("cudaMalloc");
+  nccl_peer_ptrs_kernel<<<1, 32>>>(m->win, m->dc, m->has_dc ? 1 : 0, nranks, d_out);
+  void* h[kMaxPeers + 1] = {};
+  const cudaError_t e = cudaMemcpy(h, d_out, (nranks + 1) * sizeof(void*), cudaMemcpyDeviceToHost);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return fail("peer pointer query kernel");
+  for (int p = 0; p < nranks; ++p) {
+    if (!h[p]) return fail("a rank's window is not load/store-accessible (not on this NVLink domain)");
+    peers[p] = h[p];
+  }
+  *mc = h[nranks];
+  if (want_multimem && !*mc) return fail("the window has no multicast address");
+  *out = m;
+  return 0;
 }
 
 }  // namespace covapb

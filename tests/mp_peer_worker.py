@@ -11,6 +11,9 @@ one-GPU stand-in for one process per GPU.  Rendezvous over gloo
                       between PROCESSES;
   --collective nccl   Communicator.from_torch_distributed + covap_sync_step
                       (K1 -> ncclAllReduce -> K2; needs one GPU per rank).
+  --collective peer_nccl  the peer kernels with their buffers in an NCCL
+                      symmetric window (PeerGroup.from_nccl; --multimem: the
+                      reduction in the NVSwitch); one GPU per rank.
 
 Steps run back to back with no host synchronisation between them (the
 schedule the ADVICE race needs: empty phases between same-parity steps), each
@@ -35,7 +38,8 @@ def main():
     ap.add_argument("--interval", type=int, default=4)
     ap.add_argument("--mode", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--collective", choices=["peer", "nccl"], default="peer")
+    ap.add_argument("--collective", choices=["peer", "nccl", "peer_nccl"], default="peer")
+    ap.add_argument("--multimem", action="store_true")
     ap.add_argument("--seed", type=int, default=21)
     ap.add_argument("--timeout", type=float, default=120.0)
     ap.add_argument("--max-ctas", type=int, default=0)
@@ -54,7 +58,7 @@ def main():
 
         dev_index = int(os.environ.get("COVAP_MP_DEVICE", "-1"))
         if dev_index < 0:
-            dev_index = rank if a.collective == "nccl" else 0
+            dev_index = rank if a.collective in ("nccl", "peer_nccl") else 0
         torch.cuda.set_device(dev_index)
         dev = torch.device("cuda", dev_index)
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -67,6 +71,14 @@ def main():
         if a.collective == "peer":
             state = covap.CompressorState(plan, torch.float32, dev_index, ef)
             group = covap.PeerGroup.from_torch_distributed(state)
+            group.set_limits(max_ctas=a.max_ctas, timeout_s=a.timeout)
+            group.set_fused(a.mode)
+            sync_fn = lambda g, o: group.sync(g, o, stream)  # noqa: E731
+        elif a.collective == "peer_nccl":
+            comm = covap.Communicator.from_torch_distributed(dev_index)
+            state = covap.CompressorState(plan, torch.float32, dev_index, ef)
+            group = covap.PeerGroup.from_nccl(state, comm, multimem=a.multimem)
+            verdict["multimem"] = group.multimem
             group.set_limits(max_ctas=a.max_ctas, timeout_s=a.timeout)
             group.set_fused(a.mode)
             sync_fn = lambda g, o: group.sync(g, o, stream)  # noqa: E731
@@ -92,7 +104,7 @@ def main():
                 outs[s].copy_(out)
         stream.synchronize()
         verdict["wall_s"] = time.perf_counter() - t0
-        if a.collective == "peer":
+        if a.collective in ("peer", "peer_nccl"):
             group.check()  # raises if any spin-wait timed out
         got = [o.cpu().numpy() for o in outs]
         got_r = state.residuals.cpu().numpy()
@@ -110,9 +122,9 @@ def main():
                                  rs[w], tensors, keep, 1, coeff) for w in range(world)]
             mean = orc.allreduce_mean(np.stack(pays)) if len(pays[0]) else pays[0]
             want = orc.decompress(mean, tensors, keep, d, np.float32)
-            if a.collective == "nccl" and world > 2:
-                # NCCL's summation order differs from the rank order: the
-                # stated bound |d| <= 1e-6 * sum_w |x_w|
+            if (a.collective == "nccl" and world > 2) or (a.multimem and world > 1):
+                # NCCL's (or the NVSwitch's) summation order differs from the
+                # rank order: the stated bound |d| <= 1e-6 * sum_w |x_w|
                 absx = orc.decompress(np.sum(np.abs(np.stack(pays)).astype(np.float64), axis=0),
                                       tensors, keep, d, np.float64)
                 bad = np.abs(got[s].astype(np.float64) - want) > 1e-6 * absx / world + 0.0

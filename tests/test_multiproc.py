@@ -101,3 +101,42 @@ def test_nccl_sync_across_processes(tmp_path, layout, K, P, steps):
         pytest.skip(f"NCCL needs one GPU per rank: {torch.cuda.device_count()} < {P}")
     launch(tmp_path, P, ["--collective", "nccl", "--layout", layout, "--interval", str(K),
                          "--steps", str(steps)])
+
+
+# The peer kernels over NCCL symmetric-window memory instead of CUDA IPC
+# (covap_peer_create_nccl).  P = 1 runs on any box (a 1-rank communicator:
+# the window, its peer pointer and the kernels' flag protocol on it); P > 1
+# needs one GPU per rank, as NCCL does.  multimem: the reduction in the
+# NVSwitch (multimem.ld_reduce / multimem.st), within the NCCL tolerance.
+NCCL_PEER_CASES = [("resnet50", 4, 1, 0, False), ("resnet50", 4, 1, 1, False),
+                   ("resnet50", 8, 1, 2, False), ("resnet50", 4, 2, 1, False),
+                   ("resnet50", 8, 2, 0, False), ("vgg16", 4, 4, 1, False),
+                   ("resnet50", 4, 2, 1, True), ("resnet50", 8, 2, 0, True),
+                   ("vgg16", 4, 4, 1, True), ("bert_large", 4, 8, 1, True)]
+
+
+@pytest.mark.parametrize("layout,K,P,mode,mm", NCCL_PEER_CASES,
+                         ids=[f"{c[0]}-K{c[1]}-P{c[2]}-mode{c[3]}" + ("-multimem" if c[4] else "")
+                              for c in NCCL_PEER_CASES])
+def test_peer_over_nccl_window_across_processes(tmp_path, layout, K, P, mode, mm):
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"NCCL needs one GPU per rank: {torch.cuda.device_count()} < {P}")
+    vs = launch(tmp_path, P, ["--collective", "peer_nccl", "--layout", layout, "--interval",
+                              str(K), "--mode", str(mode), "--steps", "6"]
+                + (["--multimem"] if mm else []))
+    assert all(v.get("multimem", False) == mm for v in vs)
+
+
+def test_peer_multimem_refused_without_multicast(tmp_path):
+    """One rank has no NVSwitch multicast team: asking for multimem must fail
+    loudly at creation, not fall back."""
+    import paper_2311_04499_b200 as covap
+    plan = covap.plan_for(covap.load_layout("resnet50"), covap.CovapConfig(interval=4))
+    comm = covap.Communicator(covap.Communicator.unique_id(), 1, 0, 0)
+    state = covap.CompressorState(plan, torch.float32, 0)
+    with pytest.raises(covap.Error, match="multicast"):
+        covap.PeerGroup.from_nccl(state, comm, multimem=True)
+    g = covap.PeerGroup.from_nccl(state, comm)  # the plain window still works
+    assert not g.multimem
+    del g
+    comm.close()
