@@ -229,6 +229,10 @@ __global__ void __launch_bounds__(kThreads) dense_kernel(DenseArgs A) {
 // ---------------------------------------------------------- compensate
 
 constexpr int kCompVec = 4;
+#ifndef COVAP_COMP_PARTS  // compensation pass: work units per chunk
+#define COVAP_COMP_PARTS 8
+#endif
+constexpr uint32_t kCompParts = COVAP_COMP_PARTS;
 
 template <typename T, bool HIST>
 __global__ void __launch_bounds__(kThreads)
@@ -256,8 +260,16 @@ __global__ void __launch_bounds__(kThreads)
   };
   using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   constexpr int W = 16 / static_cast<int>(sizeof(T));
-  for (uint32_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
-    const Chunk ch = chunks[ci];
+  // Work units of kChunk / kCompParts elements, round-robin over the CTAs:
+  // finer than chunks so the last wave leaves fewer SMs idle.
+  constexpr uint32_t kParts = kCompParts;
+  constexpr uint64_t kPlen = kChunk / kParts;
+  for (uint32_t u = blockIdx.x; u < nchunks * kParts; u += gridDim.x) {
+    Chunk ch = chunks[u / kParts];
+    const uint64_t ub = ch.begin + (u % kParts) * kPlen;
+    if (ub >= ch.end) continue;
+    ch.begin = ub;
+    ch.end = ch.end < ub + kPlen ? ch.end : ub + kPlen;
     if (HIST && ch.tensor != cur) {
       if (cur != kNone) flush();
       cur = ch.tensor;
