@@ -423,6 +423,10 @@ constexpr int kWarps = kThreads / 32;
 // 32-bit flat indices (the state checks N < 2^32); body chunks are 16-byte
 // aligned (covap_feedback_create cuts every tensor's unaligned head and tail
 // into chunks of their own, flagged scalar).
+#ifndef COVAP_COLLECT_PARTS  // collect: work units per chunk
+#define COVAP_COLLECT_PARTS 4
+#endif
+constexpr uint32_t kCollectParts = COVAP_COLLECT_PARTS;
 constexpr uint32_t kFifo = 160;  // hit vectors per warp: 31 pending + 4 x 32 new fit
 
 template <typename T>
@@ -523,11 +527,19 @@ __global__ void __launch_bounds__(kThreads, COVAP_COLLECT_CTAS) topk_collect_ker
     }
     __syncthreads();
   };
-  const uint32_t per = (A.nchunks + gridDim.x - 1) / gridDim.x;
-  const uint32_t c_lo = min(A.nchunks, blockIdx.x * per), c_hi = min(A.nchunks, c_lo + per);
+  // one contiguous run of work units (a chunk / kCollectParts each) per CTA
+  constexpr uint32_t kParts = kCollectParts;
+  constexpr uint64_t kPlen = kChunk / kParts;
+  const uint32_t nu = A.nchunks * kParts;
+  const uint32_t per = (nu + gridDim.x - 1) / gridDim.x;
+  const uint32_t u_lo = min(nu, blockIdx.x * per), u_hi = min(nu, u_lo + per);
   constexpr uint32_t kSpan = 32 * kV * W;  // elements per warp iteration
-  for (uint32_t ci = c_lo; ci < c_hi; ++ci) {
-    const Chunk ch = A.chunks[ci];
+  for (uint32_t u = u_lo; u < u_hi; ++u) {
+    Chunk ch = A.chunks[u / kParts];
+    const uint64_t ub = ch.begin + (u % kParts) * kPlen;
+    if (ub >= ch.end) continue;
+    ch.begin = ub;
+    ch.end = ch.end < ub + kPlen ? ch.end : ub + kPlen;
     if (ch.tensor != t) {
       if (t != kNone) end_tensor();
       t = ch.tensor;
