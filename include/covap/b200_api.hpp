@@ -355,6 +355,7 @@ class Comm {
   static std::vector<std::uint8_t> unique_id();
   Comm(const std::vector<std::uint8_t>& id, int nranks, int rank, int device);
   covap_comm* get() const { return c_.get(); }
+  const std::shared_ptr<covap_comm>& shared() const { return c_; }
 
  private:
   std::shared_ptr<covap_comm> c_;
@@ -377,6 +378,25 @@ class Sync {
   State state_;
   covap_comm* comm_;
   std::size_t n_buckets_;
+};
+
+// One rank's synchronisation with C1 as the NVLink peer collective
+// (covap_peer_*) on `state`: the send buffers in an NCCL symmetric window on
+// comm (collective over its ranks), reduced in rank order — bit-identical to
+// allreduce_mean for any P — or, with multimem, in the NVSwitch (the NCCL
+// tolerance).  mode: 0 all-gather then unpack, 1 the unpack fused into the
+// collective kernel (default), 2 the whole step as one kernel.
+class PeerSync {
+ public:
+  PeerSync(State& state, const Comm& comm, bool multimem = false, int mode = 1);
+  void step(const void* grad, void* out, void* stream);  // covap_peer_sync_step
+  bool multimem() const;
+  void check_timeouts() const;                          // covap_peer_check
+
+ private:
+  covap_state* state_;
+  std::shared_ptr<covap_comm> comm_;  // outlives the peer
+  std::shared_ptr<covap_peer> p_;
 };
 
 // The CCR-driven choice of K on a live job (PAPER §IV-B, sim.cpp:164-216,

@@ -146,6 +146,26 @@ Comm::Comm(const std::vector<std::uint8_t>& id, int nranks, int rank, int device
   c_.reset(c, covap_comm_destroy);
 }
 
+PeerSync::PeerSync(State& state, const Comm& comm, bool multimem, int mode)
+    : state_(state.get()), comm_(comm.shared()) {
+  covap_peer* p = nullptr;
+  check(covap_peer_create_nccl(state_, comm_.get(), multimem ? 1 : 0, &p));
+  p_.reset(p, covap_peer_destroy);
+  check(covap_peer_set_fused(p, mode));
+}
+
+void PeerSync::step(const void* grad, void* out, void* stream) {
+  check(covap_peer_sync_step(state_, p_.get(), grad, out, stream));
+}
+
+bool PeerSync::multimem() const {
+  int on = 0;
+  check(covap_peer_multimem(p_.get(), &on));
+  return on != 0;
+}
+
+void PeerSync::check_timeouts() const { check(covap_peer_check(p_.get())); }
+
 Sync::Sync(const Plan& plan, const Comm* comm, int dtype, int device, const EfSchedule& ef)
     : state_(plan, dtype, device, ef), comm_(comm ? comm->get() : nullptr),
       n_buckets_(plan.info().n_buckets) {}

@@ -1012,15 +1012,18 @@ __global__ void randomk_unmark_kernel(const uint32_t* __restrict__ pos, uint64_t
     bits[pos[e] / 32] = 0u;
 }
 
-// Samples per filter tile (one warp per tile; tile ntiles = the scalar tail
-// [ntiles * te, n)), for the list offsets of the fused pass.
+// Samples per filter tile (one warp per tile), for the list offsets of the
+// fused pass — its tiles exactly: tile k < ntiles is [k te, min(k te + te,
+// b16)), the 16-byte-vector part, and tile ntiles the scalar tail [b16, n)
+// the pass handles element by element.
 __global__ void randomk_tile_count_kernel(const uint32_t* __restrict__ bits, uint64_t te,
-                                          uint64_t ntiles, uint64_t n, uint32_t* __restrict__ cnt) {
+                                          uint64_t ntiles, uint64_t b16, uint64_t n,
+                                          uint32_t* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x / 32) + (threadIdx.x >> 5);
        k <= ntiles; k += nw) {
-    const uint64_t e0 = k * te, e1 = k < ntiles ? min(e0 + te, n) : n;
+    const uint64_t e0 = k < ntiles ? k * te : b16, e1 = k < ntiles ? min(e0 + te, b16) : n;
     uint32_t c = 0;
     if (e1 > e0)
       for (uint64_t q = e0 / 32 + lane; q <= (e1 - 1) / 32; q += 32) {
@@ -1359,12 +1362,12 @@ cudaError_t launch_randomk_unmark(const uint32_t* pos, uint64_t total, uint32_t*
 }
 
 cudaError_t launch_randomk_tile_offsets(const uint32_t* bits, uint64_t te, uint64_t ntiles,
-                                        uint64_t n, uint32_t* cnt, uint32_t* toff, void* tmp,
-                                        size_t tmp_bytes, int sms, cudaStream_t s) {
+                                        uint64_t b16, uint64_t n, uint32_t* cnt, uint32_t* toff,
+                                        void* tmp, size_t tmp_bytes, int sms, cudaStream_t s) {
   const uint64_t warps = ntiles + 1;
   const int grid = static_cast<int>(std::min<uint64_t>((warps + kWarps - 1) / kWarps,
                                                        static_cast<uint64_t>(sms) * 8));
-  randomk_tile_count_kernel<<<grid, kThreads, 0, s>>>(bits, te, ntiles, n, cnt);
+  randomk_tile_count_kernel<<<grid, kThreads, 0, s>>>(bits, te, ntiles, b16, n, cnt);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, toff, static_cast<int>(ntiles + 1), s);

@@ -145,8 +145,8 @@ size_t randomk_sort_bytes(uint64_t total);
 cudaError_t launch_randomk_unmark(const uint32_t* pos, uint64_t total, uint32_t* bits, int sms,
                                   cudaStream_t s);
 cudaError_t launch_randomk_tile_offsets(const uint32_t* bits, uint64_t te, uint64_t ntiles,
-                                        uint64_t n, uint32_t* cnt, uint32_t* toff, void* tmp,
-                                        size_t tmp_bytes, int sms, cudaStream_t s);
+                                        uint64_t b16, uint64_t n, uint32_t* cnt, uint32_t* toff,
+                                        void* tmp, size_t tmp_bytes, int sms, cudaStream_t s);
 size_t randomk_scan_bytes(uint64_t ntiles);
 // list[e] = (pos[e], c); kept[pos] = c; r[pos] = c - c.
 cudaError_t launch_randomk_gather(int dtype, const uint32_t* pos, uint64_t total, void* r,

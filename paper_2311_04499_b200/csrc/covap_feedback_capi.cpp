@@ -182,8 +182,10 @@ void randomk_select_marks(covap_feedback* f, uint64_t step, int b) {
   fb::RandomkArgs a = randomk_args(f, step, f->pos[b]);
   a.bits = f->bits[b];
   CK(fb::launch_randomk_select(a, f->sms, f->side));
-  CK(fb::launch_randomk_tile_offsets(f->bits[b], f->rk_te, f->rk_ntiles, f->total, f->rk_cnt,
-                                     f->toff[b], f->rk_tmp, f->rk_tmp_bytes, f->sms, f->side));
+  const uint64_t W = 16 / f->esize;  // the fused pass's vector part ends at b16
+  CK(fb::launch_randomk_tile_offsets(f->bits[b], f->rk_te, f->rk_ntiles, f->total / W * W,
+                                     f->total, f->rk_cnt, f->toff[b], f->rk_tmp,
+                                     f->rk_tmp_bytes, f->sms, f->side));
   CK(cudaEventRecord(f->ev_pos[b], f->side));
 }
 

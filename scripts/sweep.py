@@ -22,14 +22,15 @@ import torch  # noqa: E402
 import paper_2311_04499_b200 as covap  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--max-mb", type=int, default=1024)
+ap.add_argument("--max-mb", type=int, default=512)  # 16 x 1 GB buckets exceed the 2^32-element state
+ap.add_argument("--min-mb", type=int, default=1)
 ap.add_argument("--out", default="gpurun_out/sweep.md")
 a = ap.parse_args()
 with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "MEASURED_PEAKS.json")) as f:
     peak = json.load(f)["hbm_gbs"]
 
 rows = []
-mb = 1
+mb = a.min_mb
 while mb <= a.max_mb:
     elems = mb * (1 << 20) // 4
     model = covap.ModelSpec([covap.LayerSpec(f"l{i}", elems) for i in range(16)],

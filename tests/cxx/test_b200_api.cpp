@@ -159,3 +159,35 @@ TEST_CASE("covap settings, resolve_interval and the CCR controller (host)") {
   CHECK(o.total_ms == 37);
   CHECK(o.bubbles.size() == 2);
 }
+
+TEST_CASE("peer collective over an NCCL window equals the NCCL step (one rank)") {
+  const ModelSpec model = small_model();
+  const std::uint32_t K = 3;
+  const EfSchedule ef{true, 0.3, 2, 0.2};
+  b200::Plan dplan(model, K);
+  const b200::Comm comm(b200::Comm::unique_id(), 1, 0, 0);
+  const std::uint64_t n = dplan.info().device_numel;
+  for (int mode = 0; mode <= 2; ++mode) {
+    b200::Sync ref(dplan, &comm, COVAP_F32, 0, ef);
+    b200::State st(dplan, COVAP_F32, 0, ef);
+    b200::PeerSync peer(st, comm, false, mode);
+    CHECK_FALSE(peer.multimem());
+    Dev g(n * 4), oa(n * 4), ob(n * 4);
+    for (std::uint64_t s = 0; s < 2 * K + 1; ++s) {
+      const std::vector<double> d = gaussian(n, 900 + s);
+      std::vector<float> f(d.begin(), d.end());
+      REQUIRE(covap_memcpy(g.p, f.data(), n * 4, 0, nullptr) == COVAP_OK);
+      ref.step(g.p, oa.p, nullptr);
+      peer.step(g.p, ob.p, nullptr);
+      std::vector<float> xa(n), xb(n);
+      REQUIRE(covap_memcpy(xa.data(), oa.p, n * 4, 1, nullptr) == COVAP_OK);
+      REQUIRE(covap_memcpy(xb.data(), ob.p, n * 4, 1, nullptr) == COVAP_OK);
+      REQUIRE(covap_stream_synchronize(nullptr) == COVAP_OK);
+      CHECK(std::memcmp(xa.data(), xb.data(), n * 4) == 0);
+    }
+    peer.check_timeouts();
+  }
+  // one rank has no NVSwitch multicast team: refused, not a silent fallback
+  b200::State st(dplan, COVAP_F32, 0, ef);
+  CHECK_THROWS_AS(b200::PeerSync(st, comm, true), covap::Error);
+}

@@ -186,8 +186,13 @@ def oracle_mean(orc, kept_rows):
 
 @pytest.mark.parametrize("kind", [2, 3, 4])
 @pytest.mark.parametrize("P", [1, 2, 3, 4])
-def test_virtual_rank_sync_matches_rank_ordered_mean(covap, orc, kind, P):
-    sizes = [4097, 1, 30000, 65536, 513]
+@pytest.mark.parametrize("sizes", [[4097, 1, 30000, 65536, 513], [4097, 1, 30000, 65536, 511, 1]],
+                         ids=["ragged", "tail-tensor"])
+def test_virtual_rank_sync_matches_rank_ordered_mean(covap, orc, kind, P, sizes):
+    """The wire of every rank, combined in rank order.  'tail-tensor': 100 146
+    elements end in a 1-element tensor, so random-k always samples inside the
+    streaming pass's 2-element scalar tail (whose list slots follow every
+    tile's)."""
     n = sum(sizes)
     ef = (1, 0.3, 2, 0.2)
     ranks = [F().ErrorFeedback(sizes, schedule(covap, ef), make_filter(kind, 1, 0.02, 11))
