@@ -77,15 +77,15 @@ struct covap_feedback {
   // Selections made ahead: pos[b] holds the flat sampled positions of step
   // pos_step[b] (b = step & 1) once ev_pos[b] completes; ev_used[b] marks
   // the gather that last read pos[b].
-  uint32_t* pos[2] = {nullptr, nullptr};
-  uint32_t* bits[2] = {nullptr, nullptr};  // sample bitmaps (n / 32 + 8 words), zero between uses
-  uint32_t* toff[2] = {nullptr, nullptr};  // list offset of every filter tile
+  uint32_t* pos[3] = {};
+  uint32_t* bits[3] = {};  // sample bitmaps (n / 32 + 8 words), zero between uses
+  uint32_t* toff[3] = {};  // list offset of every filter tile
   uint64_t rk_te = 0, rk_ntiles = 0;       // the fused pass's tile geometry
   uint32_t* rk_cnt = nullptr;
   void* rk_tmp = nullptr;
   size_t rk_tmp_bytes = 0;
-  uint64_t pos_step[2] = {~0ull, ~0ull};
-  cudaEvent_t ev_pos[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  uint64_t pos_step[3] = {~0ull, ~0ull, ~0ull};
+  cudaEvent_t ev_pos[3] = {}, ev_used[3] = {};
   // wire
   uint32_t* list_idx = nullptr;
   void* list_val = nullptr;
@@ -114,7 +114,7 @@ void release(covap_feedback* f) {
   for (void* p : f->owned) cudaFree(p);
   if (f->ev_fork) cudaEventDestroy(f->ev_fork);
   if (f->ev_join) cudaEventDestroy(f->ev_join);
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < 3; ++b) {
     if (f->ev_pos[b]) cudaEventDestroy(f->ev_pos[b]);
     if (f->ev_used[b]) cudaEventDestroy(f->ev_used[b]);
   }
@@ -170,9 +170,11 @@ fb::RandomkArgs randomk_args(covap_feedback* f, uint64_t step, uint32_t* pos) {
   return a;
 }
 
-#ifndef COVAP_RK_AHEAD  // random-k: draw step s + 1's selection during step s
+#ifndef COVAP_RK_AHEAD  // random-k: steps drawn ahead (0, 1 or 2) on the side stream
 #define COVAP_RK_AHEAD 1
 #endif
+static_assert(COVAP_RK_AHEAD >= 0 && COVAP_RK_AHEAD <= 2, "COVAP_RK_AHEAD");
+constexpr int kRkBufs = COVAP_RK_AHEAD + 1;  // selection buffers in rotation
 
 // Random-k selection of `step` into buffer b on the side stream: positions,
 // sample bitmap (the previous selection's words cleared first), per-tile
@@ -274,7 +276,7 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       CK(cudaStreamIsCapturing(st, &cap));
       const bool ahead = COVAP_RK_AHEAD && cap == cudaStreamCaptureStatusNone;
       const uint64_t s0 = f->num_steps;
-      const int b0 = static_cast<int>(s0 & 1), b1 = b0 ^ 1;
+      const int b0 = static_cast<int>(s0 % kRkBufs);
       CK(cudaEventRecord(f->ev_fork, st));
       CK(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
       if (!ahead || f->pos_step[b0] != s0) {
@@ -287,10 +289,15 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
                                        f->bits[b0], f->toff[b0], f->list_idx, f->list_val,
                                        f->total, coeff, f->ef.enabled, st));
       CK(cudaEventRecord(f->ev_used[b0], st));
-      if (ahead) {  // step s0 + 1, into the buffers step s0 - 1's pass read
-        CK(cudaStreamWaitEvent(f->side, f->ev_used[b1], 0));
-        randomk_select_marks(f, s0 + 1, b1);
-        f->pos_step[b1] = s0 + 1;
+      if (ahead) {  // steps s0 + 1 .. s0 + AHEAD, each into the buffers the pass
+                    // AHEAD + 1 steps before it read
+        for (uint64_t t = s0 + 1; t <= s0 + COVAP_RK_AHEAD; ++t) {
+          const int bt = static_cast<int>(t % kRkBufs);
+          if (f->pos_step[bt] == t) continue;
+          CK(cudaStreamWaitEvent(f->side, f->ev_used[bt], 0));
+          randomk_select_marks(f, t, bt);
+          f->pos_step[bt] = t;
+        }
       } else {  // join the side stream back into the capture
         CK(cudaEventRecord(f->ev_join, f->side));
         CK(cudaStreamWaitEvent(st, f->ev_join, 0));
@@ -513,7 +520,7 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
       f->rk_cnt = dalloc<uint32_t>(f, (f->rk_ntiles + 1) * 4);
       f->rk_tmp_bytes = fb::randomk_scan_bytes(f->rk_ntiles);
       f->rk_tmp = dalloc<void>(f, f->rk_tmp_bytes);
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < kRkBufs; ++b) {
         f->pos[b] = dalloc<uint32_t>(f, f->k_total * 4);
         CK(cudaMemset(f->pos[b], 0, std::max<uint64_t>(f->k_total, 1) * 4));
         f->bits[b] = dalloc<uint32_t>(f, (f->total / 32 + 8) * 4);
