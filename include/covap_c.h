@@ -261,6 +261,10 @@ covap_status covap_step_finish(covap_state* state, void* stream);
  * padded plan (COVAP_PLAN_PAD_BUCKETS). */
 covap_status covap_bucket_ready_local(covap_state* state, covap_comm* comm, size_t bucket,
                                       const void* bucket_grad, void* bucket_out, void* stream);
+/* The stream covap_bucket_ready[_local] runs a bucket's allreduce and unpack
+ * on (the state's side stream): work recorded on it after the call completes
+ * after that bucket's unpack — e.g. the event a CUDA-aware future records. */
+covap_status covap_state_side_stream(covap_state* state, void** stream);
 covap_status covap_dense_bucket_ready_local(covap_state* state, covap_comm* comm, size_t bucket,
                                             void* bucket_grad, void* bucket_out, void* stream);
 /* Dense baseline (no compression, trainer.cpp:387-389): bucket b is

@@ -704,6 +704,14 @@ class CovapSync:
     def finish(self, stream=None):
         L.lib().covap_step_finish(self.state.handle, _stream_ptr(stream, self.device))
 
+    def side_stream(self):
+        """The stream bucket_ready() runs each bucket's allreduce and unpack on,
+        as a torch ExternalStream."""
+        import torch
+        p = ctypes.c_void_p()
+        L.lib().covap_state_side_stream(self.state.handle, ctypes.byref(p))
+        return torch.cuda.ExternalStream(p.value, device=torch.device("cuda", self.device))
+
     def last_comm_ms(self) -> List[float]:
         n = len(self.plan.buckets)
         d = (ctypes.c_double * n)()

@@ -897,6 +897,13 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
   });
 }
 
+covap_status covap_state_side_stream(covap_state* s, void** stream) {
+  return guarded([&] {
+    need(s && stream, "NULL argument");
+    *stream = s->comm_stream;
+  });
+}
+
 covap_status covap_state_set_timeline(covap_state* s, int on) {
   return guarded([&] {
     need(s != nullptr, "NULL state");

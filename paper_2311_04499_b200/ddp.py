@@ -5,7 +5,9 @@ DDP hands the hook one ``GradBucket`` at a time, in bucket index order, as
 backward produces them.  The hook runs the B200 path on the bucket's own
 buffer: K1 (filter_pack) on the producing stream, the allreduce of the
 bucket's selected shard and K2 (unpack, x1/P) on the side stream
-(``covap_bucket_ready_local``); the last bucket closes the step
+(``covap_bucket_ready_local``); the future the hook returns is CUDA-aware and
+completes on the stream that finishes the bucket, so DDP's wait orders its
+use of the bucket after the unpack; the last bucket closes the step
 (``covap_step_finish``).  DDP's buckets are the reference's buckets: the plan
 is built with one "layer" per DDP bucket and a 1-byte cap, so
 ``allocate_buckets`` reproduces them and the median / sharding / selection
@@ -75,6 +77,7 @@ class CovapDDPHook:
         assert [b.numel for b in self.plan.buckets] == self._sizes
         self.sync = CovapSync(self.plan, self.comm, _torch().float32, self.device, self.config.ef,
                               fuse_single_rank=self.fuse_single_rank)
+        self._side = self.sync.side_stream()
 
     # -- the hook ---------------------------------------------------------
     @staticmethod
@@ -100,9 +103,17 @@ class CovapDDPHook:
             raise TypeError("the COVAP hook handles contiguous fp32 gradient buckets")
         stream = torch.cuda.current_stream(state.device)
         state.sync.bucket_ready_local(idx, buf, buf, stream)
+        # A CUDA-aware future completed on the stream that finishes this
+        # bucket: DDP's wait() makes its stream wait for this bucket's unpack
+        # (side stream) or fused pass (producing stream) — nothing here relies
+        # on finish() ordering the streams.
+        fut = torch.futures.Future(devices=[torch.device("cuda", state.device)])
+        if state.world == 1 and state.fuse_single_rank:
+            fut.set_result(buf)
+        else:
+            with torch.cuda.stream(state._side):
+                fut.set_result(buf)
         if bucket.is_last():
             state.sync.finish(stream)
             state.iterations += 1
-        fut = torch.futures.Future()
-        fut.set_result(buf)
         return fut
