@@ -22,7 +22,7 @@ import torch  # noqa: E402
 import paper_2311_04499_b200 as covap  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--max-mb", type=int, default=512)  # 16 x 1 GB buckets exceed the 2^32-element state
+ap.add_argument("--max-mb", type=int, default=1024)
 ap.add_argument("--min-mb", type=int, default=1)
 ap.add_argument("--out", default="gpurun_out/sweep.md")
 a = ap.parse_args()
