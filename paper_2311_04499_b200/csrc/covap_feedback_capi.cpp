@@ -81,6 +81,7 @@ struct covap_feedback {
   uint32_t* bits[3] = {};  // sample bitmaps (n / 32 + 8 words), zero between uses
   uint32_t* toff[3] = {};  // list offset of every filter tile
   uint64_t rk_te = 0, rk_ntiles = 0;       // the fused pass's tile geometry
+  int rk_free = 0;                         // SMs the pass leaves to the selection chain
   uint32_t* rk_cnt = nullptr;
   void* rk_tmp = nullptr;
   size_t rk_tmp_bytes = 0;
@@ -170,6 +171,9 @@ fb::RandomkArgs randomk_args(covap_feedback* f, uint64_t step, uint32_t* pos) {
   return a;
 }
 
+#ifndef COVAP_RK_SORT_FREE_SMS  // random-k, sort variant: SMs left to the selection chain
+#define COVAP_RK_SORT_FREE_SMS 24
+#endif
 #ifndef COVAP_RK_AHEAD  // random-k: steps drawn ahead (0, 1 or 2) on the side stream
 #define COVAP_RK_AHEAD 1
 #endif
@@ -287,7 +291,7 @@ void ef_step(covap_feedback* f, const void* grad, void* kept, void* zero, bool w
       CK(cudaStreamWaitEvent(st, f->ev_pos[b0], 0));
       CK(covapb::launch_filter_randomk(dt, grad, f->residual, zero, kept ? 1 : 0, kept_mean ? 1 : 0,
                                        f->bits[b0], f->toff[b0], f->list_idx, f->list_val,
-                                       f->total, coeff, f->ef.enabled, st));
+                                       f->total, coeff, f->ef.enabled, st, f->rk_free));
       CK(cudaEventRecord(f->ev_used[b0], st));
       if (ahead) {  // steps s0 + 1 .. s0 + AHEAD, each into the buffers the pass
                     // AHEAD + 1 steps before it read
@@ -516,7 +520,14 @@ covap_status covap_feedback_create(const uint64_t* numels, size_t n_tensors, int
       CK(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming));
-      CK(covapb::filter_tiles(f->dtype == COVAP_F64 ? 1 : 0, f->total, &f->rk_te, &f->rk_ntiles));
+      // Large selections sort their draws (cub onesweep), whose CTAs need
+      // shared memory the streaming pass holds on every SM it runs on: the
+      // pass leaves some SMs to the chain then (VGG-16 random-k 0.516 ->
+      // 0.471 ms with 32, BERT-large 1.166 -> 1.134 with 16; the hash
+      // variant co-runs without shared memory and gains nothing).
+      f->rk_free = f->tbits ? 0 : COVAP_RK_SORT_FREE_SMS;
+      CK(covapb::filter_tiles(f->dtype == COVAP_F64 ? 1 : 0, f->total, &f->rk_te, &f->rk_ntiles,
+                              f->rk_free));
       f->rk_cnt = dalloc<uint32_t>(f, (f->rk_ntiles + 1) * 4);
       f->rk_tmp_bytes = fb::randomk_scan_bytes(f->rk_ntiles);
       f->rk_tmp = dalloc<void>(f, f->rk_tmp_bytes);

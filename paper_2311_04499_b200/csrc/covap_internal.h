@@ -53,13 +53,15 @@ cudaError_t launch_filter_fp16(int dtype, const void* g, void* r, void* kept, in
 // entry (e, c) at toff[tile] + their rank in the tile (position order); the
 // others get r = c, out = 0.  out may be NULL.  bits: n / 32 + 8 words;
 // toff: filter_tiles()'s ntiles + 1 entries, padded to a multiple of 4 + 4.
+// free_sms: SMs the pass leaves to work beside it (its grid is the rest).
 cudaError_t launch_filter_randomk(int dtype, const void* g, void* r, void* out, int keep,
                                   int kept_mean, const uint32_t* bits, const uint32_t* toff,
                                   uint32_t* list_idx, void* list_val, uint64_t n, double coeff,
-                                  int ef, cudaStream_t s);
+                                  int ef, cudaStream_t s, int free_sms = 0);
 // Tile geometry of the filter passes over [0, n): tile te elements, ntiles
-// vector tiles (elements from ntiles * te on are the scalar tail).
-cudaError_t filter_tiles(int dtype, uint64_t n, uint64_t* te, uint64_t* ntiles);
+// vector tiles (elements from ntiles * te on are the scalar tail).  free_sms:
+// as launch_filter_randomk's (the geometry depends on the grid).
+cudaError_t filter_tiles(int dtype, uint64_t n, uint64_t* te, uint64_t* ntiles, int free_sms = 0);
 // K2 + SGD: selected -> params -= lr * f(recv); unselected untouched.
 cudaError_t launch_unpack_sgd(int dtype, const void* recv, void* params, const Run* runs,
                               int nruns, uint64_t a, uint64_t b, double inv, int mean, double lr,

@@ -1208,6 +1208,9 @@ cudaError_t shape(DeviceShape** out) {
 // few-MB pass still spreads over every SM instead of giving a handful of
 // CTAs one full-size tile each.
 constexpr uint64_t kMinTileBytes = 4096;
+// free_sms: SMs a pass leaves idle (the random-k pass, for the selection
+// chain running beside it on a side stream).
+inline int grid_sms(int sms, int free_sms) { return sms > free_sms ? sms - free_sms : 1; }
 template <typename T>
 unsigned balance(uint64_t a, uint64_t b, int sms, uint32_t tile_bytes, uint64_t* te,
                  uint64_t min_tiles = 0) {
@@ -1278,7 +1281,7 @@ cudaError_t launch(void (*kernel)(const Args<T>), unsigned grid, unsigned smem, 
 // One of the streaming passes over [a, b): filter ops 0/1/3, unpack (2) or
 // unpack + SGD (4), fp32 or fp64.
 template <typename T>
-cudaError_t pass(int op, const Args<T>& A, cudaStream_t s) {
+cudaError_t pass(int op, const Args<T>& A, cudaStream_t s, int free_sms = 0) {
   if (A.b <= A.a) return cudaSuccess;
   DeviceShape* sh;
   cudaError_t e = shape(&sh);
@@ -1286,7 +1289,8 @@ cudaError_t pass(int op, const Args<T>& A, cudaStream_t s) {
   const bool k1 = op == 0 || op == 1 || op == 3 || op == 5 || op == 6;
   Args<T> B = A;
   const uint64_t min_tiles = static_cast<uint64_t>(sh->sms) * (k1 ? COVAP_K1_MIN_WAVES : COVAP_K2_MIN_WAVES);
-  const unsigned grid = balance<T>(A.a, A.b, sh->sms, k1 ? kTileK1 : kTileK2, &B.te, min_tiles);
+  const unsigned grid = balance<T>(A.a, A.b, grid_sms(sh->sms, free_sms),
+                                   k1 ? kTileK1 : kTileK2, &B.te, min_tiles);
   if (op == 5) B.te = (B.te + 7) / 8 * 8;  // wire tiles: 16-byte multiples of halves
   switch (op) {
     case 5: return launch(filter_kernel<T, 5>, grid, kSmemK1Fp16, s, B, filter_threads<5>());
@@ -1408,16 +1412,18 @@ cudaError_t launch_filter_fp16(int dtype, const void* g, void* r, void* kept, in
   return dtype == 0 ? go(float(0)) : go(double(0));
 }
 
-cudaError_t filter_tiles(int dtype, uint64_t n, uint64_t* te, uint64_t* ntiles) {
+cudaError_t filter_tiles(int dtype, uint64_t n, uint64_t* te, uint64_t* ntiles, int free_sms) {
   DeviceShape* sh;
   const cudaError_t e = shape(&sh);
   if (e) return e;
   const uint64_t W = dtype == 0 ? 4 : 2, b16 = n / W * W;
   uint64_t t = 0;
   if (dtype == 0)
-    balance<float>(0, n, sh->sms, kTileK1, &t, static_cast<uint64_t>(sh->sms) * COVAP_K1_MIN_WAVES);
+    balance<float>(0, n, grid_sms(sh->sms, free_sms), kTileK1, &t,
+                   static_cast<uint64_t>(sh->sms) * COVAP_K1_MIN_WAVES);
   else
-    balance<double>(0, n, sh->sms, kTileK1, &t, static_cast<uint64_t>(sh->sms) * COVAP_K1_MIN_WAVES);
+    balance<double>(0, n, grid_sms(sh->sms, free_sms), kTileK1, &t,
+                    static_cast<uint64_t>(sh->sms) * COVAP_K1_MIN_WAVES);
   *te = t;
   *ntiles = b16 == 0 ? 0 : (b16 + t - 1) / t;
   return cudaSuccess;
@@ -1426,7 +1432,7 @@ cudaError_t filter_tiles(int dtype, uint64_t n, uint64_t* te, uint64_t* ntiles) 
 cudaError_t launch_filter_randomk(int dtype, const void* g, void* r, void* out, int keep,
                                   int kept_mean, const uint32_t* bits, const uint32_t* toff,
                                   uint32_t* list_idx, void* list_val, uint64_t n, double coeff,
-                                  int ef, cudaStream_t s) {
+                                  int ef, cudaStream_t s, int free_sms) {
   auto go = [&](auto tag) {
     using T = decltype(tag);
     Args<T> A = make_args<T>(g, r, nullptr, out, nullptr, nullptr, 0, 0, n, coeff, ef, 1.0,
@@ -1436,7 +1442,7 @@ cudaError_t launch_filter_randomk(int dtype, const void* g, void* r, void* out, 
     A.list_idx = list_idx;
     A.list_val = static_cast<T*>(list_val);
     A.keep = keep;
-    return pass<T>(6, A, s);
+    return pass<T>(6, A, s, free_sms);
   };
   return dtype == 0 ? go(float(0)) : go(double(0));
 }
