@@ -163,6 +163,10 @@ covap_status covap_state_set_fused(covap_state* state, int fuse_single_rank);
  * group's allreduce on the state's comm stream overlapping K1 of the later
  * groups and followed by its own K2.  1 (default) = one K1, one allreduce,
  * one K2.  Results are identical either way. */
+/* The overlapped multi-rank schedules (covap_bucket_ready, the pipelined
+ * sync step) launch K1 / K2 on all SMs but n, which stay free for the
+ * allreduce kernels running beside them (default 0).  Results unchanged. */
+covap_status covap_state_set_free_sms(covap_state* state, int n);
 covap_status covap_state_set_pipeline(covap_state* state, int groups);
 /* covap_sync_step_host's chunk schedule: chunks ramp geometrically from
  * ramp_min_elems (>= 8192) up to the body chunk at both ends (default 1 Mi). */

@@ -132,6 +132,7 @@ _SIGS = {
     "covap_peer_attach_local": (None, [ctypes.POINTER(vp), i32]),
     "covap_peer_create_nccl": (None, [vp, vp, i32, ctypes.POINTER(vp)]),
     "covap_state_side_stream": (None, [vp, ctypes.POINTER(vp)]),
+    "covap_state_set_free_sms": (None, [vp, i32]),
     "covap_peer_multimem": (None, [vp, ctypes.POINTER(i32)]),
     "covap_peer_set_limits": (None, [vp, i32, f64]),
     "covap_peer_set_fused": (None, [vp, i32]),

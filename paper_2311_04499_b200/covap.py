@@ -408,6 +408,11 @@ class CompressorState:
         """One rank: fused K1F pass (default) or the multi-rank K1 -> C1 -> K2 path."""
         L.lib().covap_state_set_fused(self._h, 1 if fuse_single_rank else 0)
 
+    def set_free_sms(self, n: int):
+        """The overlapped multi-rank schedules run K1 / K2 on all SMs but n,
+        which stay free for the allreduce kernels beside them."""
+        L.lib().covap_state_set_free_sms(self._h, int(n))
+
     def set_pipeline(self, groups: int):
         """Multi-rank sync step as `groups` bucket groups whose allreduces
         overlap the later groups' K1 (1 = serial)."""
@@ -626,7 +631,8 @@ class CovapSync:
 
     def __init__(self, plan: BucketPlan, comm: Optional[Communicator] = None, dtype=None,
                  device: int = 0, ef: Optional[EfSchedule] = None,
-                 fuse_single_rank: bool = True, pipeline: int = 1, symmetric: bool = False):
+                 fuse_single_rank: bool = True, pipeline: int = 1, symmetric: bool = False,
+                 free_sms: int = 0):
         self.plan = plan
         self.comm = comm
         self.state = CompressorState(plan, dtype, device, ef)
@@ -635,6 +641,8 @@ class CovapSync:
             self.state.set_fused(False)
         if pipeline != 1:
             self.state.set_pipeline(pipeline)
+        if free_sms:
+            self.state.set_free_sms(free_sms)
         if symmetric and comm is not None:
             self.state.use_symmetric(comm)
 

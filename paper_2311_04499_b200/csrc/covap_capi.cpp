@@ -48,6 +48,7 @@ struct covap_state {
   std::vector<uint64_t> phase_off;
   covapb::Run* d_full = nullptr;  // {[0, N), dst 0}: the dense (uncompressed) mean
   cudaStream_t comm_stream = nullptr;
+  int free_sms = 0;  // SMs K1 / K2 leave to the collective in the overlapped schedules
   cudaStream_t h2d_stream = nullptr;  // host-buffer pipeline (covap_sync_step_host)
   cudaStream_t d2h_stream = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_k;  // per-chunk event pools (reused cyclically)
@@ -492,6 +493,14 @@ covap_status covap_state_set_fused(covap_state* s, int fuse_single_rank) {
   });
 }
 
+covap_status covap_state_set_free_sms(covap_state* s, int n) {
+  return guarded([&] {
+    need(s != nullptr, "NULL state");
+    need(n >= 0, "free SMs must be >= 0");
+    s->free_sms = n;
+  });
+}
+
 covap_status covap_state_set_pipeline(covap_state* s, int groups) {
   return guarded([&] {
     need(s != nullptr, "NULL state");
@@ -719,6 +728,7 @@ covap_status covap_sync_step(covap_state* s, covap_comm* comm, const void* grad,
       // pass (K1F) that writes (0 + c) * 1 straight to the selected slots.
       k1f_range(s, grad, out, 1.0, 0, n, st);
     } else if (s->pipeline > 1 && s->plan.buckets.size() > 1) {
+      const covapb::ScopedFreeSms reserve(s->free_sms);  // SMs for the overlapped allreduces
       // Pipelined: consecutive bucket groups of about n / G elements; group
       // g's allreduce (comm stream) overlaps K1 of groups > g (compute
       // stream), and its K2 follows as soon as its allreduce is done.  Every
@@ -880,6 +890,7 @@ covap_status covap_bucket_ready(covap_state* s, covap_comm* comm, size_t bucket,
     // K1 also zero-fills the bucket's unselected output, so the side stream
     // only carries the allreduce of the selected range and its unpack — and
     // nothing at all for a bucket with no selected shard this step.
+    const covapb::ScopedFreeSms reserve(s->free_sms);  // SMs for the side stream's allreduce
     k1_range(s, grad, nullptr, a, b, st, out);
     CK(cudaEventRecord(s->ready[bucket], st));
     CK(cudaStreamWaitEvent(s->comm_stream, s->ready[bucket], 0));

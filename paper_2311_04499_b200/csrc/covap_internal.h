@@ -82,6 +82,14 @@ cudaError_t launch_generate(int dtype, void* out, uint64_t n, uint64_t key, int 
                             uint64_t begin, cudaStream_t s);
 // K3: spin emulator.
 cudaError_t launch_spin(double us, int blocks, cudaStream_t s);
+// SMs the calling thread's following K1 / K2 launches leave idle (0: none);
+// returns the previous value.
+int set_free_sms(int n);
+struct ScopedFreeSms {
+  int prev;
+  explicit ScopedFreeSms(int n) : prev(set_free_sms(n)) {}
+  ~ScopedFreeSms() { set_free_sms(prev); }
+};
 cudaError_t launch_busy(double us, double slice_us, cudaStream_t s);
 
 uint64_t stream_key(uint64_t seed, uint64_t rank, uint64_t step);

@@ -1208,9 +1208,15 @@ cudaError_t shape(DeviceShape** out) {
 // few-MB pass still spreads over every SM instead of giving a handful of
 // CTAs one full-size tile each.
 constexpr uint64_t kMinTileBytes = 4096;
-// free_sms: SMs a pass leaves idle (the random-k pass, for the selection
-// chain running beside it on a side stream).
-inline int grid_sms(int sms, int free_sms) { return sms > free_sms ? sms - free_sms : 1; }
+// free_sms: SMs a pass leaves idle — the random-k pass, for the selection
+// chain running beside it on a side stream; K1 / K2 of the overlapped
+// multi-rank schedules (set_free_sms, this thread's launches), for the
+// collective's kernels running beside them.
+thread_local int t_free_sms = 0;
+inline int grid_sms(int sms, int free_sms) {
+  const int f = free_sms > t_free_sms ? free_sms : t_free_sms;
+  return sms > f ? sms - f : 1;
+}
 template <typename T>
 unsigned balance(uint64_t a, uint64_t b, int sms, uint32_t tile_bytes, uint64_t* te,
                  uint64_t min_tiles = 0) {
@@ -1364,7 +1370,8 @@ cudaError_t launch_unpack(int dtype, const void* recv, void* out, const Run* run
       A.b = b;
       A.inv = static_cast<T>(inv);
       A.mean = mean;
-      const unsigned grid = balance<T>(A.o_lo, (A.o_hi + W - 1) / W * W, sh->sms, kTileK2, &A.te,
+      const unsigned grid = balance<T>(A.o_lo, (A.o_hi + W - 1) / W * W, grid_sms(sh->sms, 0),
+                                       kTileK2, &A.te,
                                        static_cast<uint64_t>(sh->sms) * COVAP_K2_MIN_WAVES);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
@@ -1445,6 +1452,12 @@ cudaError_t launch_filter_randomk(int dtype, const void* g, void* r, void* out, 
     return pass<T>(6, A, s, free_sms);
   };
   return dtype == 0 ? go(float(0)) : go(double(0));
+}
+
+int set_free_sms(int n) {
+  const int prev = t_free_sms;
+  t_free_sms = n > 0 ? n : 0;
+  return prev;
 }
 
 cudaError_t launch_mean_rows(int dtype, const void* rows, void* out, uint64_t P, uint64_t n,

@@ -38,7 +38,8 @@ class CovapDDPHook:
     """State object for ``DistributedDataParallel.register_comm_hook``."""
 
     def __init__(self, config: CovapConfig, comm: Optional[Communicator] = None,
-                 device: Optional[int] = None, warmup: int = 2, fuse_single_rank: bool = True):
+                 device: Optional[int] = None, warmup: int = 2, fuse_single_rank: bool = True,
+                 free_sms: int = 0):
         torch = _torch()
         self.config = config
         self.comm = comm
@@ -47,6 +48,8 @@ class CovapDDPHook:
         # one rank: the fused K1F pass on the producing stream (default), or the
         # multi-rank schedule (K1 here, allreduce + unpack on the side stream)
         self.fuse_single_rank = bool(fuse_single_rank)
+        # SMs the multi-rank schedule's K1 / K2 leave to the allreduce kernels
+        self.free_sms = int(free_sms)
         self.sync: Optional[CovapSync] = None
         self.plan: Optional[BucketPlan] = None
         self.iterations = 0
@@ -76,7 +79,7 @@ class CovapDDPHook:
                                shard=-1, pad=True)
         assert [b.numel for b in self.plan.buckets] == self._sizes
         self.sync = CovapSync(self.plan, self.comm, _torch().float32, self.device, self.config.ef,
-                              fuse_single_rank=self.fuse_single_rank)
+                              fuse_single_rank=self.fuse_single_rank, free_sms=self.free_sms)
         self._side = self.sync.side_stream()
 
     # -- the hook ---------------------------------------------------------

@@ -31,6 +31,8 @@ for N in 2 4 8; do
   run $N multimem --collective peer --peer-window --multimem --no-real-model --no-overhead
   run $N symmetric --symmetric --no-real-model --no-overhead
   run $N pipeline4 --pipeline 4 --no-real-model --no-overhead
+  run $N pipeline4_free16 --pipeline 4 --free-sms 16 --no-real-model --no-overhead
+  run $N overlap_free16 --free-sms 16 --no-real-model
   run $N bert --layout bert_large --interval 4 --no-real-model
 done
 if [ "$G" -ge 2 ]; then

@@ -60,6 +60,8 @@ def main():
     ap.add_argument("--trace", default="",
                     help="directory: for each COVAP mode also record one step's per-bucket "
                          "timeline (CUDA events, paper_2311_04499_b200.trace) -> Chrome trace")
+    ap.add_argument("--free-sms", type=int, default=0,
+                    help="side schedule: SMs K1 / K2 leave to the collective / backward")
     ap.add_argument("--schedules", default="fused,side",
                     help="COVAP hook schedules at one rank: 'fused' (K1F on the producing stream) "
                          "and/or 'side' (the multi-rank schedule through a 1-rank NCCL "
@@ -96,7 +98,8 @@ def main():
             if mode != "dense":
                 k, sc = mode
                 hook = CovapDDPHook(covap.CovapConfig(interval=k), comm1 if sc == "side" else None,
-                                    0, warmup=2, fuse_single_rank=sc == "fused")
+                                    0, warmup=2, fuse_single_rank=sc == "fused",
+                                    free_sms=args.free_sms)
                 model.register_comm_hook(hook, CovapDDPHook.hook)
             opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9)
 

@@ -410,9 +410,13 @@ def test_multi_rank_code_path_on_one_gpu(covap, name, K):
     b = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
     c = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False)
     e = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False, pipeline=3)
+    # the overlapped schedules with SMs left free for the collective
+    f = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False, free_sms=40)
+    h = covap.CovapSync(plan, comm, torch.float32, 0, fuse_single_rank=False, pipeline=3,
+                        free_sms=20)
     d = plan.total_numel()
     g = torch.empty(d, device=DEV)
-    o_ref, o_a, o_b, o_e = (torch.empty(d, device=DEV) for _ in range(4))
+    o_ref, o_a, o_b, o_e, o_f, o_h = (torch.empty(d, device=DEV) for _ in range(6))
     hin = torch.empty(d, pin_memory=True)
     hout = torch.empty(d, pin_memory=True)
     for s in range(K + 1):
@@ -425,10 +429,14 @@ def test_multi_rank_code_path_on_one_gpu(covap, name, K):
         b.finish()
         c.sync_host(hin, hout, chunk_elems=1 << 20)
         e.sync(g, o_e)  # pipelined bucket groups
+        for bk in range(len(plan.buckets)):
+            f.bucket_ready(bk, g, o_f)
+        f.finish()
+        h.sync(g, o_h)
         torch.cuda.synchronize()
-        for o in (o_a, o_b, hout.to(DEV), o_e):
+        for o in (o_a, o_b, hout.to(DEV), o_e, o_f, o_h):
             assert torch.equal(o, o_ref)
-        for st in (a, b, c, e):
+        for st in (a, b, c, e, f, h):
             assert torch.equal(st.state.residuals, ref.state.residuals)
         durs = b.last_comm_ms()
         for bk in range(len(plan.buckets)):
