@@ -245,7 +245,12 @@ covap_status covap_sync_step(covap_state* state, covap_comm* comm, const void* g
  * quarter at both ends); chunk c's H2D copy, its
  * kernels (+ the allreduce of its slice of the send buffer) and its D2H copy
  * run on three streams, so PCIe traffic in both directions overlaps.
- * dev_grad / dev_out are device staging buffers of N elements (may alias). */
+ * dev_grad / dev_out are device staging buffers of N elements (may alias).
+ * A call with the same chunking, stream and staging buffers as the previous
+ * one chains onto it: its uploads start as soon as the previous step is done
+ * with each chunk of the staging buffers, overlapping the previous step's
+ * downloads (so do not reuse the staging buffers for other work between
+ * such calls).  host_out is complete once `stream` has passed the call. */
 covap_status covap_sync_step_host(covap_state* state, covap_comm* comm, const void* host_grad,
                                   void* host_out, void* dev_grad, void* dev_out,
                                   uint64_t chunk_elems, void* stream);

@@ -51,7 +51,13 @@ struct covap_state {
   int free_sms = 0;  // SMs K1 / K2 leave to the collective in the overlapped schedules
   cudaStream_t h2d_stream = nullptr;  // host-buffer pipeline (covap_sync_step_host)
   cudaStream_t d2h_stream = nullptr;
-  std::vector<cudaEvent_t> ev_in, ev_k;  // per-chunk event pools (reused cyclically)
+  std::vector<cudaEvent_t> ev_in, ev_k, ev_out;  // per-chunk event pools (reused cyclically)
+  // The previous covap_sync_step_host call's chunking, stream and device
+  // buffers: a call with the same ones chains onto it chunk by chunk.
+  std::vector<uint64_t> host_cuts;
+  cudaStream_t host_stream = nullptr;
+  const void* host_dev_grad = nullptr;
+  const void* host_dev_out = nullptr;
   cudaEvent_t done = nullptr;
   std::vector<cudaEvent_t> ready, arrive, end;  // per bucket
   std::vector<cudaEvent_t> k1s, k2e;            // timeline: K1 start, K2 end, per bucket
@@ -382,6 +388,7 @@ void covap_state_destroy(covap_state* s) {
   if (s->done) cudaEventDestroy(s->done);
   for (auto e : s->ev_in) cudaEventDestroy(e);
   for (auto e : s->ev_k) cudaEventDestroy(e);
+  for (auto e : s->ev_out) cudaEventDestroy(e);
   if (s->h2d_stream) cudaStreamDestroy(s->h2d_stream);
   if (s->d2h_stream) cudaStreamDestroy(s->d2h_stream);
   if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
@@ -426,9 +433,11 @@ covap_status covap_state_create(const covap_plan* plan, int dtype, int device,
     CK(cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking));
     s->ev_in.resize(kChunkEvents);
     s->ev_k.resize(kChunkEvents);
+    s->ev_out.resize(kChunkEvents);
     for (int i = 0; i < kChunkEvents; ++i) {
       CK(cudaEventCreateWithFlags(&s->ev_in[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&s->ev_k[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&s->ev_out[i], cudaEventDisableTiming));
     }
     CK(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
     const size_t nb = s->plan.buckets.size();
@@ -822,13 +831,31 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
     const int P = world(comm);
     const auto& ph = phase_of(s->plan, s->num_steps);
     const double inv = 1.0 / static_cast<double>(P);
-    // Step boundary: the copy streams start after everything already on `stream`.
-    CK(cudaEventRecord(s->done, st));
-    CK(cudaStreamWaitEvent(s->h2d_stream, s->done, 0));
+    // Step boundary.  A call that repeats the previous one's chunking,
+    // stream and device buffers chains onto it chunk by chunk: chunk c's H2D
+    // waits only until the previous step's kernels are done with chunk c of
+    // dev_grad, so this step's uploads overlap the previous step's downloads
+    // (the kernels still follow the previous step's last download, through
+    // the wait on `stream` at its end).  Otherwise the copy streams start
+    // after everything already on `stream`.
+    const bool chained = s->host_cuts == cuts && s->host_stream == st &&
+                         s->host_dev_grad == dev_grad && s->host_dev_out == dev_out;
+    if (!chained) {
+      CK(cudaEventRecord(s->done, st));
+      CK(cudaStreamWaitEvent(s->h2d_stream, s->done, 0));
+    }
     for (size_t c = 0; c + 1 < cuts.size(); ++c) {
       const uint64_t a = cuts[c], b = cuts[c + 1];
       if (b <= a) continue;
       cudaEvent_t ein = s->ev_in[c % kChunkEvents], ek = s->ev_k[c % kChunkEvents];
+      cudaEvent_t eout = s->ev_out[c % kChunkEvents];
+      // (a pool event reused by a later chunk was recorded later on the same
+      // stream: waiting on it over-synchronises, never under-)
+      if (chained) {
+        CK(cudaStreamWaitEvent(s->h2d_stream, ek, 0));  // kernels done with dev_grad chunk c
+        if (dev_grad == dev_out)  // and, aliased, the download of its outputs
+          CK(cudaStreamWaitEvent(s->h2d_stream, eout, 0));
+      }
       CK(cudaMemcpyAsync(static_cast<char*>(dev_grad) + a * es,
                          static_cast<const char*>(host_grad) + a * es, (b - a) * es,
                          cudaMemcpyHostToDevice, s->h2d_stream));
@@ -859,9 +886,14 @@ covap_status covap_sync_step_host(covap_state* s, covap_comm* comm, const void* 
       CK(cudaMemcpyAsync(static_cast<char*>(host_out) + a * es,
                          static_cast<const char*>(dev_out) + a * es, (b - a) * es,
                          cudaMemcpyDeviceToHost, s->d2h_stream));
+      CK(cudaEventRecord(eout, s->d2h_stream));
     }
     CK(cudaEventRecord(s->done, s->d2h_stream));
     CK(cudaStreamWaitEvent(st, s->done, 0));
+    s->host_cuts = cuts;
+    s->host_stream = st;
+    s->host_dev_grad = dev_grad;
+    s->host_dev_out = dev_out;
     ++s->num_steps;
   });
 }

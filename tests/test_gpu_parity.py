@@ -373,6 +373,38 @@ def test_fused_single_rank_pass_equals_k1_k2(covap, dtype, name, K):
         assert torch.equal(a.residuals, b.residuals)
 
 
+@pytest.mark.parametrize("name,K,chunk,alias", [("resnet50", 4, 0, True), ("resnet50", 1, 1 << 20, False),
+                                                ("vgg16", 4, 3 << 20, True)])
+def test_host_pipeline_back_to_back(covap, name, K, chunk, alias):
+    """Consecutive covap_sync_step_host calls chain chunk by chunk (uploads of
+    step s + 1 overlap downloads of step s): issued back to back with no host
+    synchronisation, every step's host output still equals the device step's —
+    with the staging buffers aliased (an upload must wait for that chunk's
+    download) and separate."""
+    plan = covap.plan_for(covap.load_layout(name), covap.CovapConfig(interval=K))
+    a = covap.CovapSync(plan, None, torch.float32, 0)
+    b = covap.CovapSync(plan, None, torch.float32, 0)
+    d = plan.total_numel()
+    steps = K + 3
+    g = torch.empty(d, device=DEV)
+    outs = [torch.empty(d, device=DEV) for _ in range(steps)]
+    hins = [torch.empty(d, pin_memory=True) for _ in range(steps)]
+    houts = [torch.empty(d, pin_memory=True) for _ in range(steps)]
+    dg = torch.empty(d, device=DEV)
+    do = dg if alias else torch.empty(d, device=DEV)
+    for s in range(steps):
+        covap.generate(g, covap.stream_key(29, 0, s))
+        hins[s].copy_(g)
+        a.sync(g, outs[s])
+    torch.cuda.synchronize()
+    for s in range(steps):  # back to back
+        b.sync_host(hins[s], houts[s], dg, do, chunk_elems=chunk)
+    torch.cuda.synchronize()
+    for s in range(steps):
+        assert torch.equal(outs[s].cpu(), houts[s]), s
+    assert torch.equal(a.state.residuals, b.state.residuals)
+
+
 @pytest.mark.parametrize("name,K,chunk", [("resnet50", 1, 0), ("resnet50", 4, 1 << 20),
                                           ("vgg16", 4, 3 << 20), ("tablev", 19, 1 << 21)])
 def test_host_pipeline_equals_device_sync(covap, name, K, chunk):
