@@ -74,18 +74,31 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 
 template <typename T>
 struct KeyOf;
+// key: the |x| bit pattern (order == magnitude order); bits / value: the
+// whole pattern with the sign, as the candidate lists store it so the later
+// passes need not gather x again.
 template <>
 struct KeyOf<float> {
   using K = uint32_t;
-  static constexpr int kBits = 31;  // |x| bit pattern: order == magnitude order
-  static __device__ __forceinline__ K key(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+  static constexpr int kBits = 31;
+  static constexpr K kMask = 0x7fffffffu;
+  static __device__ __forceinline__ K key(float x) { return __float_as_uint(x) & kMask; }
+  static __device__ __forceinline__ K bits(float x) { return __float_as_uint(x); }
+  static __device__ __forceinline__ float value(K b) { return __uint_as_float(b); }
 };
 template <>
 struct KeyOf<double> {
   using K = uint64_t;
   static constexpr int kBits = 63;
+  static constexpr K kMask = 0x7fffffffffffffffull;
   static __device__ __forceinline__ K key(double x) {
-    return static_cast<uint64_t>(__double_as_longlong(x)) & 0x7fffffffffffffffull;
+    return static_cast<uint64_t>(__double_as_longlong(x)) & kMask;
+  }
+  static __device__ __forceinline__ K bits(double x) {
+    return static_cast<uint64_t>(__double_as_longlong(x));
+  }
+  static __device__ __forceinline__ double value(K b) {
+    return __longlong_as_double(static_cast<long long>(b));
   }
 };
 
@@ -493,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, COVAP_COLLECT_CTAS) topk_collect_ker
           ++st;
         } else if (key >= k_cand) {
           A.cand_idx[cb + sc] = i;
-          cand_key[cb + sc] = key;
+          cand_key[cb + sc] = KeyOf<T>::bits(x[w]);  // with the sign: the value itself
           atomicAdd(&hist2[digit2_of<T>(key)], 1u);
           ++sc;
         }
@@ -609,7 +622,8 @@ __global__ void __launch_bounds__(kThreads, COVAP_COLLECT_CTAS) topk_collect_ker
 // selection.  The candidates of all tensors form one flat index space (the
 // CTA scans cand_cnt into shared memory), so the work is balanced however
 // unevenly the candidates fall and no tensor waits for another.  The pass is
-// latency-bound (a dependent key -> r[i] gather per taken candidate), so every
+// latency-bound (the candidate lists carry each value's bit pattern, so the
+// pass reads no r; the appends and the scattered residual / kept stores remain), so every
 // lane keeps kF2 candidates in flight and the grid fills the SMs.  Appends are
 // warp-aggregated per tensor (one atomic per tensor present in the warp).
 #ifndef COVAP_F2_INFLIGHT
@@ -664,17 +678,17 @@ __global__ void __launch_bounds__(kThreads) topk_filter2_kernel(TopkArgs A) {
       }
       tq[q] = lo;
       const uint64_t at = A.t_begin[lo] + (e - s_pre[lo]);
-      kq[q] = vq[q] ? ck[at] : K(0);
+      kq[q] = vq[q] ? ck[at] : K(0);  // the candidate's whole bit pattern
       iq[q] = vq[q] ? A.cand_idx[at] : 0u;
     }
     T cq[kF2];
     bool tk[kF2], nx[kF2];
 #pragma unroll
     for (int q = 0; q < kF2; ++q) {  // then the gathers of the taken values
-      const uint32_t d = digit2_of<T>(kq[q]), d2 = vq[q] ? A.thr2[tq[q]] : 0u;
+      const uint32_t d = digit2_of<T>(kq[q] & KeyOf<T>::kMask), d2 = vq[q] ? A.thr2[tq[q]] : 0u;
       tk[q] = vq[q] && d > d2;
       nx[q] = vq[q] && d == d2;
-      cq[q] = tk[q] ? r[iq[q]] : T(0);
+      cq[q] = tk[q] ? KeyOf<T>::value(kq[q]) : T(0);  // no gather of r
     }
 #pragma unroll
     for (int q = 0; q < kF2; ++q) {
@@ -815,7 +829,7 @@ __global__ void __launch_bounds__(kThreads) topk_final_kernel(TopkArgs A) {
     const uint32_t slot = append_slot(take, &s_count);
     if (take) {
       const uint32_t i = cx[e];
-      const T c = r[i];
+      const T c = KeyOf<T>::value(ck[e]);  // the stored pattern is r[i]'s
       list_idx[base + slot] = i;
       list_val[base + slot] = c;
       if (kept) kept[i] = kept_value(c, A.kept_mean);
